@@ -1,0 +1,144 @@
+/*
+ * ibmi_b200.h — C ABI of the B200-native IBMI sweep (libibmi_b200.so).
+ *
+ * The reference (arxiv 2502.06377, package `ibmi`, pure Python) has no FFI:
+ * its boundary is the Python API re-exported at
+ * /root/reference/pkg/src/ibmi/__init__.py:57-77 and the internal seam
+ * linalg.py ("the only place that talks to LAPACK/BLAS", linalg.py:1-8)
+ * together with the per-set operator _BlockOp (solver.py:109-129).  Each entry
+ * point below names the reference function it replaces.  The Python host
+ * package `paper_2502_06377_b200` binds these with ctypes and re-exposes the
+ * reference's names; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - every function returns an ibmi_status (0 = OK); the message of the last
+ *     failure on the calling thread is ibmi_last_error();
+ *   - matrices are float64, row-major, leading dimension in elements;
+ *     `on_device` = 1 means the pointer is CUDA device memory on the context's
+ *     device, 0 means host memory (pinned or pageable);
+ *   - a context is one solve: not re-entrant, all work on its stream.
+ */
+#ifndef IBMI_B200_H
+#define IBMI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IBMI_OK = 0,
+  IBMI_ERR_INVALID = 1,        /* bad argument                      -> ValueError            */
+  IBMI_ERR_DIM = 2,            /* shapes disagree                   -> DimensionMismatch     */
+  IBMI_ERR_INDEX = 3,          /* set outside [0, p)                -> IndexOutOfRange       */
+  IBMI_ERR_NOT_SPD = 4,        /* non-positive Cholesky pivot       -> NotPositiveDefinite   */
+  IBMI_ERR_NOT_SYMMETRIC = 5,  /* max|a-aT| > 1e-12 max|a|          -> ValueError            */
+  IBMI_ERR_CUDA = 6,           /* CUDA runtime failure              -> DeviceError           */
+  IBMI_ERR_OOM = 7,            /* device allocation failed          -> OutOfMemoryBudget     */
+  IBMI_ERR_STATE = 8,          /* call out of order (e.g. sweep before setup)                */
+  IBMI_ERR_UNSUPPORTED = 9     /* not implemented on this path                               */
+} ibmi_status;
+
+typedef enum {
+  IBMI_GUESS_IDENTITY = 0,     /* solver.py:158-159                                         */
+  IBMI_GUESS_JACOBI = 1,       /* BASELINE c1/c2: Σ0[c1,c1] = diag(1/A_ii) (not in reference) */
+  IBMI_GUESS_MATRIX = 2,       /* caller-supplied c1×c1 block (any host-side guess)         */
+  IBMI_GUESS_LOCAL = 3         /* solver.py:162-164: spd_inverse(A[c1,c1]) on the device     */
+} ibmi_guess;
+
+typedef struct ibmi_ctx ibmi_ctx;
+
+/* Thread-local message of the last failure (never NULL). */
+const char* ibmi_last_error(void);
+/* Library version string, e.g. "ibmi_b200 0.1.0 sm_100a". */
+const char* ibmi_version(void);
+
+/* Create a context for a p×p problem on `device`; `stream` is a cudaStream_t
+ * (NULL: the library creates its own non-blocking stream).
+ * Replaces the allocation half of solve() (solver.py:233-251). */
+int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream);
+int ibmi_destroy(ibmi_ctx* ctx);
+
+/* Copy A in (host or device), zero the padding, and check symmetry of the
+ * whole matrix with the reference's tolerance (linalg.py:68-77).
+ * Replaces np.asarray(a, float64) at solver.py:234. */
+int ibmi_set_matrix(ibmi_ctx* ctx, const double* a, int64_t lda, int on_device);
+
+/* K contiguous sets [lo[j], hi[j]); complement of set j is [0,lo) ∪ [hi,p).
+ * Replaces the comps/ops construction at solver.py:241-242 (the index
+ * validation of partition.py:102-121 stays on the host). */
+int ibmi_set_partition(ibmi_ctx* ctx, int k, const int64_t* lo, const int64_t* hi);
+
+/* Per set: symmetry check of A_II, Cholesky (dpotrf, linalg.py:104), inverse
+ * (dpotrs against I + symmetrise, linalg.py:119,130) and W = A_II⁻¹ A_Ic
+ * (solver.py:119-120).  On IBMI_ERR_NOT_SPD, *fail_set / *fail_pivot hold the
+ * set and the block-local elimination step (LAPACK info-1, linalg.py:105-106).
+ * `first`/`count` select sets (count < 0: all). */
+int ibmi_setup(ibmi_ctx* ctx, int first, int count, int* fail_set, int64_t* fail_pivot);
+
+/* Σ = I, then Σ[c1,c1] = guess (solver.py:244-251; JACOBI is the BASELINE
+ * extension).  For IBMI_GUESS_MATRIX `guess` is c1×c1 with leading dim ldg. */
+int ibmi_init_sigma(ibmi_ctx* ctx, int guess_kind, const double* guess, int64_t ldg, int on_device);
+
+/* Overwrite / read Σ (p×p). get_sigma replaces SolveReport.result (solver.py:277). */
+int ibmi_set_sigma(ibmi_ctx* ctx, const double* s, int64_t lds, int on_device);
+int ibmi_get_sigma(ibmi_ctx* ctx, double* out, int64_t ldo, int on_device);
+
+/* The normalised default_rng(0x5EED) restart vector of length n used when the
+ * power iteration collapses to σ = 0 (linalg.py:237-244). */
+int ibmi_set_restart_vector(ibmi_ctx* ctx, int64_t n, const double* v);
+
+/* One block update of set k: M = W Σ_cc; Σ_Ic = −M; Σ_cI = −Mᵀ;
+ * Σ_II = A_II⁻¹ + M Wᵀ (symmetric).  Replaces _BlockOp.apply (solver.py:122-129). */
+int ibmi_block_update(ibmi_ctx* ctx, int k);
+
+/* ‖Σ_II A_Ic + Σ_Ic A_cc‖₂ for set k by power iteration with the reference's
+ * stopping rule.  Replaces error_estimate (solver.py:147-155) and two_norm /
+ * _power_sigma_max (linalg.py:223-274).  *converged = 0 means the cap was hit
+ * (the caller emits NoConvergenceWarning, linalg.py:267-273). */
+int ibmi_error_estimate(ibmi_ctx* ctx, int k, double rtol, int max_iters, double* err, int* iters,
+                        int* converged);
+
+/* One sweep: block updates of all sets in order, then the estimate on the last
+ * set (solver.py:257-265).  Replayed from a captured CUDA graph. */
+int ibmi_sweep(ibmi_ctx* ctx, double rtol, int max_iters, double* err, int* iters, int* converged);
+
+/* As ibmi_sweep without the graph, with per-kernel-class device times in ms
+ * (CUDA events on the context stream):
+ * times[0] panel GEMMs M=WΣcc, [1] Σ_II GEMMs, [2] estimate GEMM B,
+ * [3] Gram GEMM, [4] power iteration, [5] whole sweep. */
+int ibmi_sweep_timed(ibmi_ctx* ctx, double rtol, int max_iters, double* err, int* iters, int* converged,
+                     float* times);
+
+/* ‖I − AΣ‖_F (BASELINE c2 stopping norm), fused GEMM + reduction. */
+int ibmi_frobenius_residual(ibmi_ctx* ctx, double* out);
+
+/* Bytes of device memory held by the context. */
+int ibmi_device_bytes(ibmi_ctx* ctx, int64_t* bytes);
+
+/* ---- stand-alone dense building blocks (linalg.py seam), device pointers ---- */
+
+/* C = alpha · X · Yᵀ + beta · C ; X m×k (ldx), Y n×k (ldy), C m×n (ldc).
+ * Replaces the `@` products of solver.py:120,124-125,154. */
+int ibmi_dgemm_nt(int64_t m, int64_t n, int64_t k, double alpha, const double* x, int64_t ldx,
+                  const double* y, int64_t ldy, double beta, double* c, int64_t ldc, void* stream);
+
+/* out = A⁻¹ for SPD A (n×n) via blocked Cholesky; replaces spd_inverse
+ * (linalg.py:122-130).  On IBMI_ERR_NOT_SPD *fail_pivot = elimination step. */
+int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
+                     void* stream);
+
+/* ‖B‖₂ of a device matrix (rows×cols, ldb) by power iteration with the
+ * reference's stopping rule; replaces two_norm (linalg.py:256-274).
+ * `restart_v` (host, length cols) is the normalised default_rng(0x5EED) draw. */
+int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* restart_v, double rtol,
+                  int max_iters, double* sigma, int* iters, int* converged, void* stream);
+
+/* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */
+int ibmi_probe_fp64_peak(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IBMI_B200_H */

@@ -1,0 +1,53 @@
+"""B200-native IBMI sweep (iterative block matrix inversion, arXiv 2502.06377).
+
+Drop-in for the reference package's solver path: the names re-exported here
+follow ``ibmi/__init__.py:11-79`` for the solver, partition and exception
+surfaces.  All arithmetic runs in ``libibmi_b200.so`` (FP64 DMMA kernels for
+sm_100a, C ABI in ``include/ibmi_b200.h``); there is no CPU fallback.
+"""
+
+from .exceptions import (  # noqa: F401
+    DeviceError,
+    DimensionMismatch,
+    DuplicateWithinSet,
+    IndexOutOfRange,
+    InvalidHyperparameter,
+    InvalidOverlap,
+    IoError,
+    NoConvergenceWarning,
+    NotPerfectSquare,
+    NotPositiveDefinite,
+    OutOfMemoryBudget,
+    TooManyBlocks,
+    UncoveredIndices,
+    ZeroPivot,
+)
+from .partition import (  # noqa: F401
+    Partition,
+    complement,
+    contiguous_partition,
+    load_partition_json,
+    overlap_depth,
+    red_black_partition,
+    validate,
+)
+from .solver import (  # noqa: F401
+    GUESS_CHOICES,
+    IbmiConfig,
+    SolveReport,
+    block_update,
+    error_estimate,
+    initial_guess_identity,
+    initial_guess_local_inverse,
+    make_initial_guess,
+    solve,
+)
+
+__version__ = "0.1.0"
+
+
+def load_library():
+    """Load libibmi_b200.so now (raises if it is missing)."""
+    from . import _abi
+
+    return _abi.lib()

@@ -1,0 +1,115 @@
+"""ctypes binding of ``libibmi_b200.so`` (declared in ``include/ibmi_b200.h``).
+
+There is no CPU fallback: if the shared library is missing or cannot be
+loaded, :func:`lib` raises.  Status codes become the reference's exception
+classes (`/root/reference/pkg/src/ibmi/exceptions.py`) via :func:`check`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .exceptions import DeviceError, DimensionMismatch, IndexOutOfRange, NotPositiveDefinite, OutOfMemoryBudget
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libibmi_b200.so")
+
+OK, ERR_INVALID, ERR_DIM, ERR_INDEX, ERR_NOT_SPD, ERR_NOT_SYMMETRIC, ERR_CUDA, ERR_OOM, ERR_STATE, ERR_UNSUPPORTED = range(10)
+GUESS_IDENTITY, GUESS_JACOBI, GUESS_MATRIX, GUESS_LOCAL = range(4)
+
+# (name, restype, argtypes) — the full exported surface of include/ibmi_b200.h
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_I64 = C.c_int64
+SIGNATURES = [
+    ("ibmi_last_error", C.c_char_p, []),
+    ("ibmi_version", C.c_char_p, []),
+    ("ibmi_create", C.c_int, [C.POINTER(_P), C.c_int, _I64, _P]),
+    ("ibmi_destroy", C.c_int, [_P]),
+    ("ibmi_set_matrix", C.c_int, [_P, _P, _I64, C.c_int]),
+    ("ibmi_set_partition", C.c_int, [_P, C.c_int, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("ibmi_setup", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(_I64)]),
+    ("ibmi_init_sigma", C.c_int, [_P, C.c_int, _P, _I64, C.c_int]),
+    ("ibmi_set_sigma", C.c_int, [_P, _P, _I64, C.c_int]),
+    ("ibmi_get_sigma", C.c_int, [_P, _P, _I64, C.c_int]),
+    ("ibmi_set_restart_vector", C.c_int, [_P, _I64, _D]),
+    ("ibmi_block_update", C.c_int, [_P, C.c_int]),
+    ("ibmi_error_estimate", C.c_int, [_P, C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("ibmi_sweep", C.c_int, [_P, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("ibmi_sweep_timed", C.c_int, [_P, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_float)]),
+    ("ibmi_frobenius_residual", C.c_int, [_P, _D]),
+    ("ibmi_device_bytes", C.c_int, [_P, C.POINTER(_I64)]),
+    ("ibmi_dgemm_nt", C.c_int, [_I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, C.c_double, _P, _I64, _P]),
+    ("ibmi_spd_inverse", C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(_I64), _P]),
+    ("ibmi_two_norm", C.c_int, [_I64, _I64, _P, _I64, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int),
+                                C.POINTER(C.c_int), _P]),
+    ("ibmi_probe_fp64_peak", C.c_int, [C.c_int, _D]),
+]
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load (once) and return the CUDA library; raise if it is unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2502_06377_b200.build` "
+                    "(there is no CPU fallback)")
+            h = C.CDLL(LIB_PATH)
+            for name, res, args in SIGNATURES:
+                f = getattr(h, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = h
+    return _lib
+
+
+def last_error() -> str:
+    return lib().ibmi_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = "", *, fail_set: int | None = None, fail_pivot: int | None = None) -> None:
+    """Raise the reference's exception class for a non-zero status."""
+    if rc == OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == ERR_NOT_SPD:
+        raise NotPositiveDefinite(int(fail_pivot if fail_pivot is not None else -1),
+                                  f"non-positive pivot at elimination step {fail_pivot}"
+                                  + (f" (set {fail_set})" if fail_set is not None and fail_set >= 0 else ""),
+                                  set_index=fail_set)
+    if rc in (ERR_INVALID, ERR_NOT_SYMMETRIC, ERR_STATE):
+        raise ValueError(msg)
+    if rc == ERR_DIM:
+        raise DimensionMismatch(msg)
+    if rc == ERR_INDEX:
+        raise IndexOutOfRange(msg)
+    if rc == ERR_OOM:
+        raise OutOfMemoryBudget(msg)
+    if rc == ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise DeviceError(msg)
+
+
+def dptr(arr) -> int:
+    """Raw address of a numpy array or a CUDA tensor (``data_ptr``)."""
+    if isinstance(arr, np.ndarray):
+        return arr.ctypes.data
+    return int(arr.data_ptr())
+
+
+def dbl_ptr(arr: np.ndarray):
+    return arr.ctypes.data_as(_D)

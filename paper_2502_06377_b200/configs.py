@@ -1,0 +1,187 @@
+"""The five BASELINE problems, pinned.
+
+`BASELINE.json.configs` describes the inputs in prose; this module fixes every
+open choice once so the oracle fixtures, the parity tests and ``bench.py`` see
+bit-identical matrices:
+
+* seeds: ``numpy.random.default_rng(seed)``, one generator per config, draws
+  in the order written below (B6);
+* c3/c4 points are stably sorted by their first coordinate (B2);
+* partitions are ``contiguous_partition(p, K, f)`` with (K, f) = (2, 0),
+  (2, 0), (8, .125), (8, .125), (16, .125) (B1);
+* Σ₀ is ``diag(1/A_ii)`` on c1/c2 (guess ``"jacobi"``), identity otherwise (B3);
+* stopping: c1 estimate ≤ 1e-10, c2 ``‖I − AΣ‖_F < 1e-9``, c3–c5 estimate ≤ 1e-8 (B4);
+* ``max_iterations`` 1500 on c2, 500 otherwise (B5).
+
+No public dataset is involved: BASELINE's own recipes are the benchmark
+inputs, generated synthetically here.  c5 (p = 65536, 34 GB) is generated on
+the GPU by :func:`make_matrix_c5_device` because a host ``B·Bᵀ`` of that size
+is hours of CPU time.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .partition import Partition, contiguous_partition
+
+__all__ = ["ProblemConfig", "CONFIGS", "get_config", "make_matrix", "make_matrix_c5_device",
+           "sweep_flops", "setup_flops"]
+
+
+@dataclass(frozen=True)
+class ProblemConfig:
+    name: str
+    p: int
+    k: int
+    overlap: float
+    guess: str          # "jacobi" or "identity"
+    tol: float
+    stopping: str       # "estimate" or "frobenius"
+    max_iterations: int
+    description: str
+
+    def partition(self) -> Partition:
+        return contiguous_partition(self.p, self.k, self.overlap)
+
+
+CONFIGS = {
+    "c1": ProblemConfig("c1", 512, 2, 0.0, "jacobi", 1e-10, "estimate", 500,
+                        "p=512 A=Q diag(10^U(0,2)) Q^T, Haar Q; 2 blocks 256/256; Sigma0=diag(1/A_ii); tol 1e-10"),
+    "c2": ProblemConfig("c2", 4096, 2, 0.0, "jacobi", 1e-9, "frobenius", 1500,
+                        "p=4096 A=Q diag(10^U(0,3)) Q^T; 2 blocks 2048/2048; until ||I-A Sigma||_F<1e-9"),
+    "c3": ProblemConfig("c3", 8192, 8, 0.125, "identity", 1e-8, "estimate", 500,
+                        "p=8192 SE kernel l=0.1 on x-sorted U[0,1]^2 points + 1e-2 I; 8 blocks 1152/1280, overlap 256"),
+    "c4": ProblemConfig("c4", 16384, 8, 0.125, "identity", 1e-8, "estimate", 500,
+                        "p=16384 Matern-3/2 l=0.2 on x-sorted U[0,1]^3 points + 1e-3 I; 8 blocks 2304/2560, overlap 512"),
+    "c5": ProblemConfig("c5", 65536, 16, 0.125, "identity", 1e-8, "estimate", 500,
+                        "p=65536 A=B B^T/p + 0.5 I, B standard normal; 16 blocks 4608/5120, overlap 1024"),
+}
+
+
+def get_config(name: str) -> ProblemConfig:
+    return CONFIGS[name]
+
+
+def _haar_spd(p: int, seed: int, decades: float) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    g = rng.standard_normal((p, p))
+    q, r = np.linalg.qr(g)
+    q = q * np.sign(np.diag(r))
+    lam = 10.0 ** rng.uniform(0.0, decades, p)
+    a = (q * lam) @ q.T
+    return 0.5 * (a + a.T)
+
+
+def _sorted_points(p: int, dim: int, seed: int) -> np.ndarray:
+    x = np.random.default_rng(seed).uniform(size=(p, dim))
+    return x[np.argsort(x[:, 0], kind="stable")]
+
+
+def _kernel(points: np.ndarray, fn, nugget: float, chunk: int = 1024) -> np.ndarray:
+    """Dense ``fn(d²)`` over all point pairs, unit diagonal, plus ``nugget·I``.
+
+    ``d²`` is a sum over coordinates taken in the same order for (i, j) and
+    (j, i), so the result is exactly symmetric without a fix-up pass.
+    """
+    p = points.shape[0]
+    out = np.empty((p, p))
+    for lo in range(0, p, chunk):
+        hi = min(lo + chunk, p)
+        d2 = np.zeros((hi - lo, p))
+        for ax in range(points.shape[1]):
+            diff = points[lo:hi, ax][:, None] - points[None, :, ax]
+            d2 += diff * diff
+        out[lo:hi] = fn(d2)
+    idx = np.arange(p)
+    out[idx, idx] = 1.0 + nugget
+    return out
+
+
+def _squared_exponential(d2: np.ndarray, ell: float = 0.1) -> np.ndarray:
+    return np.exp(-d2 / (2.0 * ell * ell))
+
+
+def _matern32(d2: np.ndarray, ell: float = 0.2) -> np.ndarray:
+    s = np.sqrt(3.0) * np.sqrt(d2) / ell
+    return (1.0 + s) * np.exp(-s)
+
+
+def make_matrix(name: str, seed: int = 0) -> np.ndarray:
+    """Host float64 A for c1–c4 (C-order, exactly symmetric)."""
+    if name == "c1":
+        return _haar_spd(512, seed, 2.0)
+    if name == "c2":
+        return _haar_spd(4096, seed, 3.0)
+    if name == "c3":
+        return _kernel(_sorted_points(8192, 2, seed), _squared_exponential, 1e-2)
+    if name == "c4":
+        return _kernel(_sorted_points(16384, 3, seed), _matern32, 1e-3)
+    if name == "c5":
+        raise ValueError("c5 is generated on the device: use make_matrix_c5_device")
+    raise KeyError(name)
+
+
+def make_matrix_c5_device(seed: int = 0, p: int = 65536, device="cuda"):
+    """c5's ``A = B·Bᵀ/p + 0.5·I`` built on the GPU (torch Philox normals,
+    seeded).  Input generation only: the product is a plain library GEMM."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    a = torch.empty((p, p), dtype=torch.float64, device=device)
+    panel = 8192
+    b = torch.randn((p, p), dtype=torch.float64, device=device, generator=gen)
+    for lo in range(0, p, panel):
+        hi = min(lo + panel, p)
+        torch.matmul(b[lo:hi], b.T, out=a[lo:hi])
+    del b
+    a.mul_(1.0 / p)
+    a = 0.5 * (a + a.T) if p <= 16384 else _symmetrize_inplace(a)
+    a.diagonal().add_(0.5)
+    return a
+
+
+def _symmetrize_inplace(a):
+    """Average with the transpose tile by tile (no second p×p buffer)."""
+    p = a.shape[0]
+    t = 8192
+    for i in range(0, p, t):
+        for j in range(0, i + 1, t):
+            blk = 0.5 * (a[i:i + t, j:j + t] + a[j:j + t, i:i + t].T)
+            a[i:i + t, j:j + t] = blk
+            a[j:j + t, i:i + t] = blk.T
+    return a
+
+
+def _set_sizes(cfg: ProblemConfig):
+    part = cfg.partition()
+    return [len(s) for s in part.sets]
+
+
+def sweep_flops(cfg_or_sizes, p: int | None = None) -> float:
+    """Algorithmic FLOPs of one sweep as the reference evaluates them
+    (solver.py:124-125 per set, :154 for the estimate), no symmetry discount:
+    ``Σ_k (2 b c² + 2 b² c) + 2 b_K² c_K + 2 b_K c_K²``."""
+    if isinstance(cfg_or_sizes, ProblemConfig):
+        sizes, p = _set_sizes(cfg_or_sizes), cfg_or_sizes.p
+    else:
+        sizes = list(cfg_or_sizes)
+    tot = 0.0
+    for b in sizes:
+        c = p - b
+        tot += 2.0 * b * c * c + 2.0 * b * b * c
+    b = sizes[-1]
+    c = p - b
+    return tot + 2.0 * b * b * c + 2.0 * b * c * c
+
+
+def setup_flops(cfg_or_sizes, p: int | None = None) -> float:
+    """Once-per-solve FLOPs: ``Σ_k (b³/3 + 2b³ + 2b²c)`` (potrf + potrs(I) + W)."""
+    if isinstance(cfg_or_sizes, ProblemConfig):
+        sizes, p = _set_sizes(cfg_or_sizes), cfg_or_sizes.p
+    else:
+        sizes = list(cfg_or_sizes)
+    return sum(b ** 3 / 3.0 + 2.0 * b ** 3 + 2.0 * b * b * (p - b) for b in sizes)

@@ -1,0 +1,1007 @@
+// libibmi_b200.so — B200-native IBMI sweep behind a C ABI (include/ibmi_b200.h).
+//
+// Device data layout (row-major FP64, leading dimension ld = roundup(p, 32),
+// padding columns zero):
+//   A        p × ld        the SPD input, read-only after set_matrix
+//   Σ        p × ld        the approximation of A⁻¹, full symmetric storage
+//   W_k      b_k × ld      A_II⁻¹ A_Ic in GLOBAL column coordinates (columns of
+//                          I_k zero), one per set, cached for the whole solve
+//                          (reference _BlockOp.w, solver.py:120)
+//   ainv_k   b_k × ldb     A_II⁻¹ (exactly symmetric)
+//   B        b_K × ldc     estimate matrix Σ_II A_Ic + Σ_Ic A_cc (solver.py:154)
+//   G        n × n         its Gram matrix (B·Bᵀ or Bᵀ·B, whichever is smaller)
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ibmi_b200.h"
+#include "gemm_nt.cuh"
+#include "small_kernels.cuh"
+
+using namespace ibmi;
+
+namespace {
+
+thread_local std::string g_err = "";
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      int code_ = (e_ == cudaErrorMemoryAllocation) ? IBMI_ERR_OOM : IBMI_ERR_CUDA;           \
+      return fail(code_, std::string(#expr) + ": " + cudaGetErrorString(e_));                 \
+    }                                                                                         \
+  } while (0)
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// ---------------------------------------------------------------- GEMM launch
+struct GemmOp {
+  const double* X = nullptr; int64_t ldx = 0; RowMap xm = contig_map(0); bool xt = false;
+  const double* Y = nullptr; int64_t ldy = 0; RowMap yn = contig_map(0); bool yt = false;
+  int64_t M = 0, N = 0;
+  int nseg = 0; KSeg seg[2];
+  double* C = nullptr; int64_t ldc = 0; RowMap cm = contig_map(0), cn = contig_map(0);
+  double alpha = 1.0, beta = 0.0;
+  const double* D = nullptr; int64_t ldd = 0; RowMap dm = contig_map(0), dn = contig_map(0);
+  bool mirror = false, lower = false;
+  double* partial = nullptr;     // non-null -> Frobenius epilogue
+  void add_seg(int64_t x0, int64_t y0, int64_t len) {
+    if (len > 0) seg[nseg++] = KSeg{x0, y0, (int)len};
+  }
+};
+
+template <bool XT, bool YT, bool V16, int EPI>
+cudaError_t ensure_attr() {
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_nt_kernel<XT, YT, V16, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = true;
+  }
+  return cudaSuccess;
+}
+
+template <bool XT, bool YT, bool V16, int EPI>
+cudaError_t launch_inst(const GemmParams& P, int grid, cudaStream_t s) {
+  cudaError_t e = ensure_attr<XT, YT, V16, EPI>();
+  if (e != cudaSuccess) return e;
+  gemm_nt_kernel<XT, YT, V16, EPI><<<grid, G_THREADS, GEMM_SMEM, s>>>(P);
+  return cudaGetLastError();
+}
+
+// Set the dynamic-smem attribute of every instantiation up front (outside any
+// graph capture).
+cudaError_t prepare_gemm_attributes() {
+#define PREP(XT, YT, V, E) \
+  { cudaError_t e = ensure_attr<XT, YT, V, E>(); if (e != cudaSuccess) return e; }
+  PREP(false, false, true, EPI_STORE) PREP(false, false, false, EPI_STORE)
+  PREP(false, true, true, EPI_STORE) PREP(false, true, false, EPI_STORE)
+  PREP(true, true, true, EPI_STORE) PREP(true, true, false, EPI_STORE)
+  PREP(true, false, true, EPI_STORE) PREP(true, false, false, EPI_STORE)
+  PREP(false, false, true, EPI_FROB) PREP(false, false, false, EPI_FROB)
+  PREP(false, true, true, EPI_FROB) PREP(false, true, false, EPI_FROB)
+  PREP(true, true, true, EPI_FROB) PREP(true, true, false, EPI_FROB)
+  PREP(true, false, true, EPI_FROB) PREP(true, false, false, EPI_FROB)
+#undef PREP
+  return cudaSuccess;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int gemm_grid(const GemmOp& op) {
+  const int tm = (int)((op.M + GB_M - 1) / GB_M), tn = (int)((op.N + GB_N - 1) / GB_N);
+  return op.lower ? tm * (tm + 1) / 2 : tm * tn;
+}
+
+cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
+  if (op.M <= 0 || op.N <= 0) return cudaSuccess;
+  GemmParams P;
+  memset(&P, 0, sizeof(P));
+  P.X = op.X; P.ldx = op.ldx; P.xm = op.xm;
+  P.Y = op.Y; P.ldy = op.ldy; P.yn = op.yn;
+  P.M = (int)op.M; P.N = (int)op.N;
+  P.nseg = op.nseg;
+  P.kt0 = 0; P.kt_total = 0;
+  for (int i = 0; i < op.nseg; ++i) {
+    P.seg[i] = op.seg[i];
+    const int kt = (op.seg[i].len + GB_K - 1) / GB_K;
+    if (i == 0) P.kt0 = kt;
+    P.kt_total += kt;
+  }
+  if (op.nseg == 1) P.seg[1] = op.seg[0];
+  P.C = op.C; P.ldc = op.ldc; P.cm = op.cm; P.cn = op.cn;
+  P.alpha = op.alpha; P.beta = op.beta;
+  P.D = op.D ? op.D : op.C; P.ldd = op.D ? op.ldd : op.ldc; P.dm = op.dm; P.dn = op.dn;
+  P.mirror = op.mirror; P.lower = op.lower;
+  P.tiles_m = (P.M + GB_M - 1) / GB_M;
+  P.tiles_n = (P.N + GB_N - 1) / GB_N;
+  P.partial = op.partial;
+  const int grid = gemm_grid(op);
+  // 16-byte cp.async only when every operand address it forms is 16B aligned
+  bool v16 = aligned16(op.X) && aligned16(op.Y) && (op.ldx % 2 == 0) && (op.ldy % 2 == 0);
+  for (int i = 0; i < op.nseg; ++i) v16 = v16 && (op.seg[i].x0 % 2 == 0) && (op.seg[i].y0 % 2 == 0);
+  if (op.xt) v16 = v16 && (op.xm.off0 % 2 == 0);
+  if (op.yt) v16 = v16 && (op.yn.off0 % 2 == 0);
+  const bool frob = op.partial != nullptr;
+#define DISPATCH(XT, YT)                                                                        \
+  if (frob) return v16 ? launch_inst<XT, YT, true, EPI_FROB>(P, grid, s)                       \
+                       : launch_inst<XT, YT, false, EPI_FROB>(P, grid, s);                     \
+  return v16 ? launch_inst<XT, YT, true, EPI_STORE>(P, grid, s) : launch_inst<XT, YT, false, EPI_STORE>(P, grid, s);
+  if (!op.xt && !op.yt) { DISPATCH(false, false) }
+  if (!op.xt && op.yt) { DISPATCH(false, true) }
+  if (op.xt && op.yt) { DISPATCH(true, true) }
+  DISPATCH(true, false)
+#undef DISPATCH
+}
+
+dim3 grid2d(int64_t rows, int64_t cols) {
+  const int gx = (int)std::max<int64_t>(1, (cols + 255) / 256);
+  const int gy = (int)std::min<int64_t>(std::max<int64_t>(rows, 1), 65535);
+  return dim3(gx, gy);
+}
+
+// ------------------------------------------------------ blocked SPD inverse
+// Scratch for one factorisation of order n.
+struct CholScratch {
+  double* ws = nullptr; int64_t ldw = 0;      // n × ldw  (matrix, then factor, then L⁻¹)
+  double* dinv = nullptr;                      // nblocks × 64 × 64 diagonal-block inverses
+  double* tmp = nullptr;                       // n × 64
+  int* info = nullptr;
+  int cap = 0;
+  size_t bytes = 0;
+  void release() {
+    if (ws) cudaFree(ws);
+    if (dinv) cudaFree(dinv);
+    if (tmp) cudaFree(tmp);
+    if (info) cudaFree(info);
+    ws = dinv = tmp = nullptr; info = nullptr; cap = 0; bytes = 0;
+  }
+};
+
+int ensure_scratch(CholScratch& cs, int n) {
+  if (n <= cs.cap) return IBMI_OK;
+  cs.release();
+  const int64_t ldw = round_up(n, 32);
+  const int nb = (n + CHOL_NB - 1) / CHOL_NB;
+  CUDA_TRY(cudaMalloc(&cs.ws, (size_t)n * ldw * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&cs.dinv, (size_t)nb * CHOL_NB * CHOL_NB * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&cs.tmp, (size_t)n * CHOL_NB * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&cs.info, sizeof(int)));
+  cs.ldw = ldw;
+  cs.cap = n;
+  cs.bytes = (size_t)n * ldw * 8 + (size_t)nb * CHOL_NB * CHOL_NB * 8 + (size_t)n * CHOL_NB * 8 + 4;
+  return IBMI_OK;
+}
+
+// Factor the n×n SPD matrix whose LOWER triangle is in cs.ws (upper zero):
+// blocked right-looking Cholesky (LAPACK dpotrf lower, linalg.py:104).
+// Returns IBMI_ERR_NOT_SPD with *pivot = first failing elimination step.
+int potrf_blocked(CholScratch& cs, int n, cudaStream_t s, int64_t* pivot) {
+  const int init = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(cs.info, &init, sizeof(int), cudaMemcpyHostToDevice, s));
+  double* a = cs.ws;
+  const int64_t ld = cs.ldw;
+  for (int j0 = 0, blk = 0; j0 < n; j0 += CHOL_NB, ++blk) {
+    const int jb = std::min(CHOL_NB, n - j0);
+    const int j1 = j0 + jb;
+    double* dblk = cs.dinv + (size_t)blk * CHOL_NB * CHOL_NB;
+    potf2_trti2_kernel<<<1, 256, 0, s>>>(a + (int64_t)j0 * ld + j0, ld, jb, dblk, CHOL_NB, cs.info, j0);
+    CUDA_TRY(cudaGetLastError());
+    if (j1 >= n) break;
+    // panel: L[j1:, j0:j1] = A[j1:, j0:j1] · L_jj⁻ᵀ   (in place, one N tile)
+    GemmOp pn;
+    pn.X = a; pn.ldx = ld; pn.xm = contig_map(j1);
+    pn.Y = dblk; pn.ldy = CHOL_NB; pn.yn = contig_map(0);
+    pn.M = n - j1; pn.N = jb;
+    pn.add_seg(j0, 0, jb);
+    pn.C = a; pn.ldc = ld; pn.cm = contig_map(j1); pn.cn = contig_map(j0);
+    CUDA_TRY(launch_gemm(pn, s));
+    // trailing: A[j1:, j1:] -= P Pᵀ  (lower tiles only)
+    GemmOp tr;
+    tr.X = a; tr.ldx = ld; tr.xm = contig_map(j1);
+    tr.Y = a; tr.ldy = ld; tr.yn = contig_map(j1);
+    tr.M = n - j1; tr.N = n - j1;
+    tr.add_seg(j0, j0, jb);
+    tr.C = a; tr.ldc = ld; tr.cm = contig_map(j1); tr.cn = contig_map(j1);
+    tr.alpha = -1.0; tr.beta = 1.0; tr.D = a; tr.ldd = ld; tr.dm = contig_map(j1); tr.dn = contig_map(j1);
+    tr.lower = true;
+    CUDA_TRY(launch_gemm(tr, s));
+  }
+  int h = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(&h, cs.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (h != INT_MAX) {
+    *pivot = h;
+    return fail(IBMI_ERR_NOT_SPD, "non-positive pivot at elimination step " + std::to_string(h));
+  }
+  return IBMI_OK;
+}
+
+// In-place L -> L⁻¹ (LAPACK dtrtri lower, blocked right-to-left), then
+// out = L⁻ᵀ L⁻¹ (lower tiles, mirrored: exactly symmetric, like the
+// reference's 0.5(inv + invᵀ), linalg.py:130).
+int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t s) {
+  double* a = cs.ws;
+  const int64_t ld = cs.ldw;
+  const int nblk = (n + CHOL_NB - 1) / CHOL_NB;
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int j0 = blk * CHOL_NB;
+    const int jb = std::min(CHOL_NB, n - j0);
+    const int j1 = j0 + jb;
+    double* dblk = cs.dinv + (size_t)blk * CHOL_NB * CHOL_NB;
+    if (j1 < n) {
+      // T = X[j1:, j1:] · L[j1:, j0:j1]
+      GemmOp t1;
+      t1.X = a; t1.ldx = ld; t1.xm = contig_map(j1);
+      t1.Y = a; t1.ldy = ld; t1.yn = contig_map(j0); t1.yt = true;
+      t1.M = n - j1; t1.N = jb;
+      t1.add_seg(j1, j1, n - j1);
+      t1.C = cs.tmp; t1.ldc = CHOL_NB;
+      CUDA_TRY(launch_gemm(t1, s));
+      // X[j1:, j0:j1] = −T · L_jj⁻¹
+      GemmOp t2;
+      t2.X = cs.tmp; t2.ldx = CHOL_NB;
+      t2.Y = dblk; t2.ldy = CHOL_NB; t2.yt = true;
+      t2.M = n - j1; t2.N = jb;
+      t2.add_seg(0, 0, jb);
+      t2.C = a; t2.ldc = ld; t2.cm = contig_map(j1); t2.cn = contig_map(j0);
+      t2.alpha = -1.0;
+      CUDA_TRY(launch_gemm(t2, s));
+    }
+    copy2d_kernel<<<grid2d(jb, jb), 256, 0, s>>>(dblk, CHOL_NB, contig_map(0), contig_map(0),
+                                                 a + (int64_t)j0 * ld + j0, ld, jb, jb, 0);
+    CUDA_TRY(cudaGetLastError());
+  }
+  GemmOp la;   // out[m][n] = Σ_k X[k][m] X[k][n]
+  la.X = a; la.ldx = ld; la.xt = true;
+  la.Y = a; la.ldy = ld; la.yt = true;
+  la.M = n; la.N = n;
+  la.add_seg(0, 0, n);
+  la.C = out; la.ldc = ldo;
+  la.lower = true; la.mirror = true;
+  CUDA_TRY(launch_gemm(la, s));
+  return IBMI_OK;
+}
+
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct SetDev {
+  int64_t lo = 0, hi = 0;
+  int b = 0;
+  double* W = nullptr;      // b × ld
+  double* ainv = nullptr;   // b × ldb
+  int64_t ldb = 0;
+  bool ready = false;
+};
+
+struct ibmi_ctx {
+  int device = 0;
+  int64_t p = 0, ld = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double* A = nullptr;
+  double* S = nullptr;
+  bool a_set = false;
+  std::vector<SetDev> sets;
+  CholScratch cs;
+  // estimate buffers
+  double* Bm = nullptr; int64_t ldB = 0; int64_t B_cap = 0;
+  double* Gm = nullptr; int64_t ldG = 0; int64_t G_cap = 0;
+  double* vec = nullptr; int64_t vec_cap = 0;
+  double* part = nullptr; int part_cap = 0;
+  double* vr = nullptr; int64_t vr_n = 0;
+  double* frob_part = nullptr; int frob_cap = 0;
+  double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
+  double* hpin = nullptr;         // pinned mirror of dscal
+  int sms = 148;
+  int power_blocks = 148;
+  int power_threads = 512;
+  size_t power_smem_cap = 200 * 1024;
+  cudaGraphExec_t graph = nullptr;
+  bool graph_tried = false, graph_ok = false;
+  double graph_rtol = -1.0;
+  int graph_max = -1;
+  size_t bytes = 0;
+};
+
+namespace {
+
+int ensure_buf(double** p, int64_t* cap, int64_t need, size_t* bytes) {
+  if (need <= *cap) return IBMI_OK;
+  if (*p) { cudaFree(*p); *bytes -= (size_t)(*cap) * 8; }
+  *p = nullptr;
+  *cap = 0;
+  CUDA_TRY(cudaMalloc(p, (size_t)need * sizeof(double)));
+  *cap = need;
+  *bytes += (size_t)need * 8;
+  return IBMI_OK;
+}
+
+void invalidate_graph(ibmi_ctx* c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  c->graph = nullptr;
+  c->graph_tried = false;
+  c->graph_ok = false;
+}
+
+int symcheck(ibmi_ctx* c, int64_t off, int64_t n, const char* what) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(c->dscal + 8);
+  CUDA_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), c->stream));
+  const int nt = (int)((n + 31) / 32);
+  symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, c->stream>>>(c->A, c->ld, off, (int)n, d);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(c->hpin + 8, c->dscal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const double mabs = c->hpin[8], skew = c->hpin[9];
+  if (mabs == 0.0) return IBMI_OK;
+  if (!(skew <= 1e-12 * mabs)) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%s is not symmetric: max |a - a.T| = %.3e exceeds 1.0e-12 * max|a| = %.3e", what,
+             skew, 1e-12 * mabs);
+    return fail(IBMI_ERR_NOT_SYMMETRIC, buf);
+  }
+  return IBMI_OK;
+}
+
+// ---- one block update: the hot path (solver.py:122-129)
+// `mid` (optional) is recorded between the two GEMMs (for ibmi_sweep_timed).
+int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
+  const SetDev& s = c->sets[k];
+  const int64_t p = c->p, lo = s.lo, hi = s.hi, b = s.b, cc = p - b;
+  // K1: Σ[I, c] = −W Σ[c, c];  Σ[c, I] = its transpose (mirror store)
+  GemmOp k1;
+  k1.X = s.W; k1.ldx = c->ld; k1.xm = contig_map(0);
+  k1.Y = c->S; k1.ldy = c->ld; k1.yn = complement_map(lo, hi);
+  k1.M = b; k1.N = cc;
+  k1.add_seg(0, 0, lo);
+  k1.add_seg(hi, hi, p - hi);
+  k1.C = c->S; k1.ldc = c->ld; k1.cm = contig_map(lo); k1.cn = complement_map(lo, hi);
+  k1.alpha = -1.0; k1.mirror = true;
+  CUDA_TRY(launch_gemm(k1, c->stream));
+  if (mid) CUDA_TRY(cudaEventRecord(mid, c->stream));
+  // K2: Σ[I, I] = A_II⁻¹ − Σ[I, c] W_cᵀ   (= ainv + M Wᵀ), lower tiles mirrored
+  GemmOp k2;
+  k2.X = c->S; k2.ldx = c->ld; k2.xm = contig_map(lo);
+  k2.Y = s.W; k2.ldy = c->ld; k2.yn = contig_map(0);
+  k2.M = b; k2.N = b;
+  k2.add_seg(0, 0, lo);
+  k2.add_seg(hi, hi, p - hi);
+  k2.C = c->S; k2.ldc = c->ld; k2.cm = contig_map(lo); k2.cn = contig_map(lo);
+  k2.alpha = -1.0; k2.beta = 1.0; k2.D = s.ainv; k2.ldd = s.ldb;
+  k2.lower = true; k2.mirror = true;
+  CUDA_TRY(launch_gemm(k2, c->stream));
+  return IBMI_OK;
+}
+
+int ensure_estimate_buffers(ibmi_ctx* c, int64_t b, int64_t cc) {
+  const int64_t ldB = round_up(std::max<int64_t>(cc, 1), 32);
+  if (ensure_buf(&c->Bm, &c->B_cap, b * ldB, &c->bytes)) return IBMI_ERR_OOM;
+  c->ldB = ldB;
+  const int64_t n = std::min(b, cc);
+  const int64_t ldG = round_up(n, 32);
+  if (ensure_buf(&c->Gm, &c->G_cap, n * ldG, &c->bytes)) return IBMI_ERR_OOM;
+  c->ldG = ldG;
+  if (ensure_buf(&c->vec, &c->vec_cap, 2 * std::max(b, cc), &c->bytes)) return IBMI_ERR_OOM;
+  int64_t pc = c->part_cap;
+  if (ensure_buf(&c->part, &pc, 4 * (int64_t)c->power_blocks, &c->bytes)) return IBMI_ERR_OOM;
+  c->part_cap = (int)pc;
+  return IBMI_OK;
+}
+
+// ---- ‖B‖₂ of a device matrix by the Gram-form power iteration
+// (linalg.py:223-274).  Buffers: G (n×ldG, n = min(rows, cols)), vec (2·max),
+// part (4·blocks), out (3 doubles), vr (cols, normalised restart vector).
+struct NormBufs {
+  double* G; int64_t ldG;
+  double* vec;
+  double* part;
+  double* out;
+  const double* vr;
+  int blocks, threads;
+  size_t smem_cap;
+};
+
+int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, double rtol, int max_iters,
+                     const NormBufs& nb, cudaStream_t st, cudaEvent_t ev_gram = nullptr) {
+  const int mode = (b <= cc) ? 0 : 1;
+  const int64_t n = mode == 0 ? b : cc;
+  GemmOp gg;
+  if (mode == 0) {   // G = B Bᵀ
+    gg.X = Bm; gg.ldx = ldB;
+    gg.Y = Bm; gg.ldy = ldB;
+    gg.add_seg(0, 0, cc);
+  } else {           // H = Bᵀ B
+    gg.X = Bm; gg.ldx = ldB; gg.xt = true;
+    gg.Y = Bm; gg.ldy = ldB; gg.yt = true;
+    gg.add_seg(0, 0, b);
+  }
+  gg.M = n; gg.N = n;
+  gg.C = nb.G; gg.ldc = nb.ldG;
+  gg.lower = true; gg.mirror = true;
+  CUDA_TRY(launch_gemm(gg, st));
+  if (mode == 0) {
+    const int threads = 256;
+    const int blocks = (int)((b * 32 + threads - 1) / threads);
+    rowsum_scaled_kernel<<<blocks, threads, 0, st>>>(Bm, ldB, (int)b, (int)cc, 1.0 / std::sqrt((double)cc), nb.vec);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (ev_gram) CUDA_TRY(cudaEventRecord(ev_gram, st));
+  PowerParams P;
+  P.G = nb.G; P.ldg = nb.ldG; P.n = (int)n;
+  P.B = Bm; P.ldb = ldB; P.brows = (int)b; P.bcols = (int)cc;
+  P.vr = nb.vr;
+  P.vec = nb.vec;
+  P.part = nb.part;
+  P.rtol = rtol;
+  P.max_iters = max_iters;
+  P.mode = mode;
+  P.out = nb.out;
+  P.smem_cap = (int)(nb.smem_cap / sizeof(double));
+  const size_t smem = (size_t)std::min<int64_t>(n, P.smem_cap) * sizeof(double);
+  void* args[] = {&P};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)power_gram_kernel, dim3(nb.blocks), dim3(nb.threads), args, smem,
+                                       st));
+  return IBMI_OK;
+}
+
+int alloc_norm_bufs(NormBufs& nb, int64_t b, int64_t cc, int blocks, int threads, size_t smem_cap) {
+  const int64_t n = std::min(b, cc);
+  nb.ldG = round_up(n, 32);
+  nb.G = nb.vec = nb.part = nb.out = nullptr;
+  nb.blocks = blocks; nb.threads = threads; nb.smem_cap = smem_cap;
+  CUDA_TRY(cudaMalloc(&nb.G, (size_t)n * nb.ldG * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&nb.vec, (size_t)2 * std::max(b, cc) * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&nb.part, (size_t)4 * blocks * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&nb.out, 4 * sizeof(double)));
+  return IBMI_OK;
+}
+
+void free_norm_bufs(NormBufs& nb) {
+  for (double* q : {nb.G, nb.vec, nb.part, nb.out})
+    if (q) cudaFree(q);
+}
+
+void power_launch_shape(int device, int* blocks, int* threads, size_t* smem_cap) {
+  int sms = 148, maxb = 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  *threads = 512;
+  *smem_cap = 200 * 1024;
+  cudaFuncSetAttribute(power_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_cap);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, power_gram_kernel, *threads, *smem_cap);
+  *blocks = sms * std::max(1, std::min(maxb, 1));
+}
+
+// ---- error estimate for set k (solver.py:147-155 + linalg.py:223-274)
+// ev (optional): [0] after the B GEMM, [1] after the Gram GEMM.
+int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaEvent_t* ev = nullptr) {
+  const SetDev& s = c->sets[k];
+  const int64_t p = c->p, lo = s.lo, hi = s.hi, b = s.b, cc = p - b;
+  if (cc <= 0) return fail(IBMI_ERR_DIM, "set covers every index: empty complement");
+  int rc = ensure_estimate_buffers(c, b, cc);
+  if (rc) return rc;
+  if (c->vr == nullptr || c->vr_n != cc) {
+    return fail(IBMI_ERR_STATE, "restart vector of length " + std::to_string(cc) + " not set");
+  }
+  // B[m][n] = Σ_k Σ[I_m][k] A[c_n][k]   (A symmetric: A[k][c_n] = A[c_n][k])
+  GemmOp gb;
+  gb.X = c->S; gb.ldx = c->ld; gb.xm = contig_map(lo);
+  gb.Y = c->A; gb.ldy = c->ld; gb.yn = complement_map(lo, hi);
+  gb.M = b; gb.N = cc;
+  gb.add_seg(0, 0, p);
+  gb.C = c->Bm; gb.ldc = c->ldB;
+  CUDA_TRY(launch_gemm(gb, c->stream));
+  if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
+  NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
+              c->power_smem_cap};
+  rc = enqueue_two_norm(c->Bm, c->ldB, b, cc, rtol, max_iters, nb, c->stream, ev ? ev[1] : nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(c->hpin, c->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  return IBMI_OK;
+}
+
+int read_power(ibmi_ctx* c, double* err, int* iters, int* conv) {
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (err) *err = c->hpin[0];
+  if (conv) *conv = c->hpin[1] != 0.0 ? 1 : 0;
+  if (iters) *iters = (int)c->hpin[2];
+  return IBMI_OK;
+}
+
+int check_ready(ibmi_ctx* c) {
+  if (!c) return fail(IBMI_ERR_INVALID, "null context");
+  if (!c->a_set) return fail(IBMI_ERR_STATE, "matrix not set");
+  if (c->sets.empty()) return fail(IBMI_ERR_STATE, "partition not set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return IBMI_OK;
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+const char* ibmi_last_error(void) { return g_err.c_str(); }
+const char* ibmi_version(void) { return "ibmi_b200 0.1.0 sm_100a (FP64 DMMA)"; }
+
+int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
+  if (!out) return fail(IBMI_ERR_INVALID, "out is null");
+  *out = nullptr;
+  if (p < 2) return fail(IBMI_ERR_DIM, "matrix order must be >= 2");
+  CUDA_TRY(cudaSetDevice(device));
+  ibmi_ctx* c = new ibmi_ctx();
+  c->device = device;
+  c->p = p;
+  c->ld = round_up(p, 32);
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return fail(IBMI_ERR_CUDA, cudaGetErrorString(e)); }
+    c->own_stream = true;
+  }
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  prepare_gemm_attributes();
+  power_launch_shape(device, &c->power_blocks, &c->power_threads, &c->power_smem_cap);
+  const size_t mat = (size_t)p * c->ld * sizeof(double);
+  cudaError_t e1 = cudaMalloc(&c->A, mat);
+  cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&c->S, mat) : e1;
+  cudaError_t e3 = e2 == cudaSuccess ? cudaMalloc(&c->dscal, 16 * sizeof(double)) : e2;
+  cudaError_t e4 = e3 == cudaSuccess ? cudaMallocHost(&c->hpin, 16 * sizeof(double)) : e3;
+  if (e4 != cudaSuccess) {
+    ibmi_destroy(c);
+    return fail(e4 == cudaErrorMemoryAllocation ? IBMI_ERR_OOM : IBMI_ERR_CUDA,
+                std::string("allocating A/Σ: ") + cudaGetErrorString(e4));
+  }
+  c->bytes = 2 * mat + 16 * 8;
+  *out = c;
+  return IBMI_OK;
+}
+
+int ibmi_destroy(ibmi_ctx* c) {
+  if (!c) return IBMI_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  invalidate_graph(c);
+  for (auto& s : c->sets) {
+    if (s.W) cudaFree(s.W);
+    if (s.ainv) cudaFree(s.ainv);
+  }
+  c->cs.release();
+  for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal})
+    if (q) cudaFree(q);
+  if (c->hpin) cudaFreeHost(c->hpin);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return IBMI_OK;
+}
+
+int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
+  if (!c || !a) return fail(IBMI_ERR_INVALID, "null argument");
+  if (lda < c->p) return fail(IBMI_ERR_DIM, "lda < p");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int64_t p = c->p;
+  CUDA_TRY(cudaMemsetAsync(c->A, 0, (size_t)p * c->ld * sizeof(double), c->stream));
+  CUDA_TRY(cudaMemcpy2DAsync(c->A, c->ld * sizeof(double), a, lda * sizeof(double), p * sizeof(double), p,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  c->a_set = true;
+  for (auto& s : c->sets) s.ready = false;
+  invalidate_graph(c);
+  int rc = symcheck(c, 0, p, "matrix");
+  if (rc) { c->a_set = false; return rc; }
+  return IBMI_OK;
+}
+
+int ibmi_set_partition(ibmi_ctx* c, int k, const int64_t* lo, const int64_t* hi) {
+  if (!c || !lo || !hi) return fail(IBMI_ERR_INVALID, "null argument");
+  if (k < 1) return fail(IBMI_ERR_INVALID, "need at least one set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (int j = 0; j < k; ++j) {
+    if (lo[j] < 0 || hi[j] > c->p || lo[j] >= hi[j])
+      return fail(IBMI_ERR_INDEX, "set " + std::to_string(j) + " has indices outside [0, p)");
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (auto& s : c->sets) {
+    if (s.W) cudaFree(s.W);
+    if (s.ainv) cudaFree(s.ainv);
+    c->bytes -= (size_t)s.b * c->ld * 8 + (size_t)s.b * s.ldb * 8;
+  }
+  c->sets.assign(k, SetDev());
+  for (int j = 0; j < k; ++j) {
+    c->sets[j].lo = lo[j];
+    c->sets[j].hi = hi[j];
+    c->sets[j].b = (int)(hi[j] - lo[j]);
+    c->sets[j].ldb = round_up(c->sets[j].b, 32);
+  }
+  invalidate_graph(c);
+  return IBMI_OK;
+}
+
+int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_pivot) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (fail_set) *fail_set = -1;
+  if (fail_pivot) *fail_pivot = -1;
+  const int K = (int)c->sets.size();
+  if (count < 0) count = K - first;
+  if (first < 0 || first + count > K) return fail(IBMI_ERR_INVALID, "set range out of bounds");
+  cudaStream_t st = c->stream;
+  for (int k = first; k < first + count; ++k) {
+    SetDev& s = c->sets[k];
+    const int64_t b = s.b, lo = s.lo, hi = s.hi, p = c->p;
+    rc = symcheck(c, lo, b, "matrix");
+    if (rc) { if (fail_set) *fail_set = k; return rc; }
+    if (!s.W) {
+      CUDA_TRY(cudaMalloc(&s.W, (size_t)b * c->ld * sizeof(double)));
+      CUDA_TRY(cudaMalloc(&s.ainv, (size_t)b * s.ldb * sizeof(double)));
+      c->bytes += (size_t)b * c->ld * 8 + (size_t)b * s.ldb * 8;
+    }
+    size_t before = c->cs.bytes;
+    rc = ensure_scratch(c->cs, (int)b);
+    if (rc) return rc;
+    c->bytes += c->cs.bytes - before;
+    // A_II (lower) -> scratch
+    copy2d_kernel<<<grid2d(b, b), 256, 0, st>>>(c->A, c->ld, contig_map(lo), contig_map(lo), c->cs.ws, c->cs.ldw,
+                                               (int)b, (int)b, 1);
+    CUDA_TRY(cudaGetLastError());
+    int64_t piv = -1;
+    rc = potrf_blocked(c->cs, (int)b, st, &piv);
+    if (rc) {
+      if (fail_set) *fail_set = k;
+      if (fail_pivot) *fail_pivot = piv;
+      return rc;
+    }
+    rc = potri_blocked(c->cs, (int)b, s.ainv, s.ldb, st);
+    if (rc) return rc;
+    // W = A_II⁻¹ A[I, c]  written at global columns, zero on I
+    CUDA_TRY(cudaMemsetAsync(s.W, 0, (size_t)b * c->ld * sizeof(double), st));
+    GemmOp gw;
+    gw.X = s.ainv; gw.ldx = s.ldb;
+    gw.Y = c->A; gw.ldy = c->ld; gw.yn = complement_map(lo, hi);
+    gw.M = b; gw.N = p - b;
+    gw.add_seg(0, lo, b);
+    gw.C = s.W; gw.ldc = c->ld; gw.cn = complement_map(lo, hi);
+    CUDA_TRY(launch_gemm(gw, st));
+    s.ready = true;
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  invalidate_graph(c);
+  return IBMI_OK;
+}
+
+int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int on_device) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  const int64_t p = c->p;
+  const SetDev& s0 = c->sets[0];
+  const int64_t c0 = p - s0.b;
+  cudaStream_t st = c->stream;
+  fill2d_kernel<<<grid2d(p, c->ld), 256, 0, st>>>(c->S, c->ld, (int)p, (int)c->ld, 0.0, 1.0);
+  CUDA_TRY(cudaGetLastError());
+  if (c0 == 0) return IBMI_OK;
+  const RowMap cmap = complement_map(s0.lo, s0.hi);
+  if (kind == IBMI_GUESS_IDENTITY) {
+  } else if (kind == IBMI_GUESS_JACOBI) {
+    jacobi_diag_kernel<<<(int)((c0 + 255) / 256), 256, 0, st>>>(c->A, c->ld, c->S, c->ld, cmap, (int)c0);
+    CUDA_TRY(cudaGetLastError());
+  } else if (kind == IBMI_GUESS_MATRIX) {
+    if (!guess || ldg < c0) return fail(IBMI_ERR_DIM, "guess must be c1 x c1");
+    double* tmp = nullptr;
+    CUDA_TRY(cudaMalloc(&tmp, (size_t)c0 * c0 * sizeof(double)));
+    cudaError_t e = cudaMemcpy2DAsync(tmp, c0 * 8, guess, ldg * 8, c0 * 8, c0,
+                                      on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(tmp, c0, c->S, c->ld, cmap, cmap, (int)c0, (int)c0);
+      e = cudaGetLastError();
+    }
+    cudaStreamSynchronize(st);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+  } else if (kind == IBMI_GUESS_LOCAL) {
+    CholScratch cs;
+    rc = ensure_scratch(cs, (int)c0);
+    if (rc) { cs.release(); return rc; }
+    double* inv = nullptr;
+    cudaError_t e = cudaMalloc(&inv, (size_t)c0 * cs.ldw * sizeof(double));
+    if (e != cudaSuccess) { cs.release(); return fail(IBMI_ERR_OOM, cudaGetErrorString(e)); }
+    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 1);
+    int64_t piv = -1;
+    rc = potrf_blocked(cs, (int)c0, st, &piv);
+    if (!rc) rc = potri_blocked(cs, (int)c0, inv, cs.ldw, st);
+    if (!rc) {
+      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(inv, cs.ldw, c->S, c->ld, cmap, cmap, (int)c0, (int)c0);
+      cudaStreamSynchronize(st);
+    }
+    cudaFree(inv);
+    cs.release();
+    if (rc) return rc;
+  } else {
+    return fail(IBMI_ERR_INVALID, "unknown guess kind " + std::to_string(kind));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return IBMI_OK;
+}
+
+int ibmi_set_sigma(ibmi_ctx* c, const double* s, int64_t lds, int on_device) {
+  if (!c || !s) return fail(IBMI_ERR_INVALID, "null argument");
+  if (lds < c->p) return fail(IBMI_ERR_DIM, "lds < p");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemsetAsync(c->S, 0, (size_t)c->p * c->ld * sizeof(double), c->stream));
+  CUDA_TRY(cudaMemcpy2DAsync(c->S, c->ld * 8, s, lds * 8, c->p * 8, c->p,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return IBMI_OK;
+}
+
+int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
+  if (!c || !out) return fail(IBMI_ERR_INVALID, "null argument");
+  if (ldo < c->p) return fail(IBMI_ERR_DIM, "ldo < p");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, c->S, c->ld * 8, c->p * 8, c->p,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return IBMI_OK;
+}
+
+int ibmi_set_restart_vector(ibmi_ctx* c, int64_t n, const double* v) {
+  if (!c || !v || n < 1) return fail(IBMI_ERR_INVALID, "bad restart vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->vr_n != n) {
+    if (c->vr) cudaFree(c->vr);
+    c->vr = nullptr;
+    c->vr_n = 0;
+    CUDA_TRY(cudaMalloc(&c->vr, (size_t)n * sizeof(double)));
+    c->vr_n = n;
+    invalidate_graph(c);
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->vr, v, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return IBMI_OK;
+}
+
+int ibmi_block_update(ibmi_ctx* c, int k) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (k < 0 || k >= (int)c->sets.size()) return fail(IBMI_ERR_INVALID, "set index out of range");
+  if (!c->sets[k].ready) return fail(IBMI_ERR_STATE, "set not set up");
+  rc = enqueue_block_update(c, k);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return IBMI_OK;
+}
+
+int ibmi_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, double* err, int* iters, int* conv) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  if (k < 0 || k >= (int)c->sets.size()) return fail(IBMI_ERR_INVALID, "set index out of range");
+  if (max_iters < 1) return fail(IBMI_ERR_INVALID, "max_iters must be >= 1");
+  rc = enqueue_error_estimate(c, k, rtol, max_iters);
+  if (rc) return rc;
+  return read_power(c, err, iters, conv);
+}
+
+static int enqueue_sweep(ibmi_ctx* c, double rtol, int max_iters) {
+  for (int k = 0; k < (int)c->sets.size(); ++k) {
+    int rc = enqueue_block_update(c, k);
+    if (rc) return rc;
+  }
+  return enqueue_error_estimate(c, (int)c->sets.size() - 1, rtol, max_iters);
+}
+
+int ibmi_sweep(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters, int* conv) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  for (auto& s : c->sets)
+    if (!s.ready) return fail(IBMI_ERR_STATE, "setup not complete");
+  if (max_iters < 1) return fail(IBMI_ERR_INVALID, "max_iters must be >= 1");
+  // make sure lazily-allocated buffers exist before any capture
+  const SetDev& last = c->sets.back();
+  rc = ensure_estimate_buffers(c, last.b, c->p - last.b);
+  if (rc) return rc;
+  if (c->graph_tried && (c->graph_rtol != rtol || c->graph_max != max_iters)) invalidate_graph(c);
+  if (!c->graph_tried) {
+    c->graph_tried = true;
+    c->graph_rtol = rtol;
+    c->graph_max = max_iters;
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      int erc = enqueue_sweep(c, rtol, max_iters);
+      cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
+      if (erc == IBMI_OK && ec == cudaSuccess && g) {
+        if (cudaGraphInstantiate(&c->graph, g, 0) == cudaSuccess) c->graph_ok = true;
+      }
+      if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();   // clear any capture error; fall back to direct launches
+    if (!c->graph_ok && c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  }
+  if (c->graph_ok) {
+    CUDA_TRY(cudaGraphLaunch(c->graph, c->stream));
+  } else {
+    rc = enqueue_sweep(c, rtol, max_iters);
+    if (rc) return rc;
+  }
+  return read_power(c, err, iters, conv);
+}
+
+int ibmi_sweep_timed(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters, int* conv, float* times) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  for (auto& s : c->sets)
+    if (!s.ready) return fail(IBMI_ERR_STATE, "setup not complete");
+  const int K = (int)c->sets.size();
+  std::vector<cudaEvent_t> ev(2 * K + 4);
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  float t[6] = {0, 0, 0, 0, 0, 0};
+  CUDA_TRY(cudaEventRecord(ev[0], c->stream));
+  for (int k = 0; k < K; ++k) {
+    rc = enqueue_block_update(c, k, ev[1 + 2 * k]);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(ev[2 + 2 * k], c->stream));
+  }
+  rc = enqueue_error_estimate(c, K - 1, rtol, max_iters, &ev[2 * K + 1]);
+  if (rc) return rc;
+  CUDA_TRY(cudaEventRecord(ev[2 * K + 3], c->stream));
+  rc = read_power(c, err, iters, conv);
+  if (rc) return rc;
+  float ms;
+  for (int k = 0; k < K; ++k) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev[2 * k], ev[1 + 2 * k]));
+    t[0] += ms;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev[1 + 2 * k], ev[2 + 2 * k]));
+    t[1] += ms;
+  }
+  CUDA_TRY(cudaEventElapsedTime(&ms, ev[2 * K], ev[2 * K + 1]));
+  t[2] = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, ev[2 * K + 1], ev[2 * K + 2]));
+  t[3] = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, ev[2 * K + 2], ev[2 * K + 3]));
+  t[4] = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[2 * K + 3]));
+  t[5] = ms;
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (times) memcpy(times, t, sizeof(t));
+  return IBMI_OK;
+}
+
+int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  const int64_t p = c->p;
+  GemmOp fr;
+  fr.X = c->A; fr.ldx = c->ld;
+  fr.Y = c->S; fr.ldy = c->ld;
+  fr.M = p; fr.N = p;
+  fr.add_seg(0, 0, p);
+  const int nparts = gemm_grid(fr);
+  int64_t cap = c->frob_cap;
+  if (ensure_buf(&c->frob_part, &cap, nparts, &c->bytes)) return IBMI_ERR_OOM;
+  c->frob_cap = (int)cap;
+  fr.partial = c->frob_part;
+  CUDA_TRY(launch_gemm(fr, c->stream));
+  reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->frob_part, nparts, c->dscal + 3);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(c->hpin + 3, c->dscal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (out) *out = c->hpin[3];
+  return IBMI_OK;
+}
+
+int ibmi_device_bytes(ibmi_ctx* c, int64_t* bytes) {
+  if (!c || !bytes) return fail(IBMI_ERR_INVALID, "null argument");
+  *bytes = (int64_t)c->bytes;
+  return IBMI_OK;
+}
+
+int ibmi_dgemm_nt(int64_t m, int64_t n, int64_t k, double alpha, const double* x, int64_t ldx, const double* y,
+                  int64_t ldy, double beta, double* c, int64_t ldc, void* stream) {
+  if (m < 0 || n < 0 || k < 0) return fail(IBMI_ERR_DIM, "negative dimension");
+  if (!x || !y || !c) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (m > INT_MAX || n > INT_MAX || k > INT_MAX) return fail(IBMI_ERR_DIM, "dimension exceeds int32");
+  GemmOp op;
+  op.X = x; op.ldx = ldx;
+  op.Y = y; op.ldy = ldy;
+  op.M = m; op.N = n;
+  op.add_seg(0, 0, k);
+  op.C = c; op.ldc = ldc;
+  op.alpha = alpha; op.beta = beta; op.D = c; op.ldd = ldc;
+  CUDA_TRY(launch_gemm(op, (cudaStream_t)stream));
+  return IBMI_OK;
+}
+
+int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
+                     void* stream) {
+  if (n < 1) return fail(IBMI_ERR_DIM, "matrix must be nonempty");
+  if (!a || !out) return fail(IBMI_ERR_INVALID, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  CholScratch cs;
+  int rc = ensure_scratch(cs, (int)n);
+  if (rc) { cs.release(); return rc; }
+  copy2d_kernel<<<grid2d(n, n), 256, 0, st>>>(a, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)n, (int)n, 1);
+  int64_t piv = -1;
+  rc = potrf_blocked(cs, (int)n, st, &piv);
+  if (rc == IBMI_ERR_NOT_SPD && fail_pivot) *fail_pivot = piv;
+  if (!rc) rc = potri_blocked(cs, (int)n, out, ldo, st);
+  cudaStreamSynchronize(st);
+  cs.release();
+  return rc;
+}
+
+int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* restart_v, double rtol,
+                  int max_iters, double* sigma, int* iters, int* converged, void* stream) {
+  if (rows < 1 || cols < 1) return fail(IBMI_ERR_DIM, "matrix must be nonempty");
+  if (!b || !restart_v) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (max_iters < 1) return fail(IBMI_ERR_INVALID, "max_iters must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  NormBufs nb;
+  int blocks, threads;
+  size_t cap;
+  power_launch_shape(dev, &blocks, &threads, &cap);
+  double* vr = nullptr;
+  int rc = alloc_norm_bufs(nb, rows, cols, blocks, threads, cap);
+  if (!rc && cudaMalloc(&vr, (size_t)cols * sizeof(double)) != cudaSuccess) rc = fail(IBMI_ERR_OOM, "restart vector");
+  if (!rc && cudaMemcpyAsync(vr, restart_v, (size_t)cols * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    rc = fail(IBMI_ERR_CUDA, "copying restart vector");
+  nb.vr = vr;
+  if (!rc) rc = enqueue_two_norm(b, ldb, rows, cols, rtol, max_iters, nb, st);
+  double h[3] = {0, 0, 0};
+  if (!rc && cudaMemcpyAsync(h, nb.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = fail(IBMI_ERR_CUDA, "reading result");
+  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = fail(IBMI_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+  free_norm_bufs(nb);
+  if (vr) cudaFree(vr);
+  if (rc) return rc;
+  if (sigma) *sigma = h[0];
+  if (converged) *converged = h[1] != 0.0;
+  if (iters) *iters = (int)h[2];
+  return IBMI_OK;
+}
+
+int ibmi_probe_fp64_peak(int device, double* tflops) {
+  if (!tflops) return fail(IBMI_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, 8));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const int warps = 8, iters = 20000;
+  dmma_probe_kernel<<<sms * 2, warps * 32>>>(d, 200, 1.0000001, 0.999999);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    CUDA_TRY(cudaEventRecord(e0));
+    dmma_probe_kernel<<<sms * 2, warps * 32>>>(d, iters, 1.0000001, 0.999999);
+    CUDA_TRY(cudaEventRecord(e1));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double flops = 2.0 * 256 * 8 * (double)iters * warps * sms * 2;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  return IBMI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,369 @@
+// Small / bandwidth-bound kernels of the IBMI B200 library.
+#pragma once
+#include <cooperative_groups.h>
+#include "common.cuh"
+
+namespace ibmi {
+namespace cg = cooperative_groups;
+
+constexpr int CHOL_NB = 64;   // diagonal block of the blocked Cholesky / trtri
+
+// ---------------------------------------------------------------------------
+// Diagonal-block factor: L = chol(A_jj) (lower), Linv = L⁻¹, both nb×nb.
+// Replaces the unblocked part of LAPACK dpotrf called at linalg.py:104.  A
+// non-positive (or NaN) pivot at local step k records `base + k` into *info
+// (atomicMin keeps the first failing elimination step, LAPACK's info - 1).
+__global__ void __launch_bounds__(256) potf2_trti2_kernel(double* a, int64_t lda, int n, double* linv,
+                                                           int64_t ldl, int* info, int base) {
+  // One array holds both triangles: L[i][j] (j <= i) at T[i][j], L⁻¹[i][j]
+  // (j <= i) at T[j][i + 1] (strictly above the diagonal).
+  __shared__ double T[CHOL_NB][CHOL_NB + 2];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    if (j <= i) T[i][j] = a[(int64_t)i * lda + j];
+  }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const double d = T[k][k];
+    const double s = sqrt(d);
+    if (tid == 0 && !(d > 0.0)) atomicMin(info, base + k);
+    __syncthreads();
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) T[i][k] /= s;
+    if (tid == 0) T[k][k] = s;
+    __syncthreads();
+    const int w = n - k - 1;
+    for (int e = tid; e < w * w; e += blockDim.x) {
+      const int i = k + 1 + e / w, j = k + 1 + e % w;
+      if (j <= i) T[i][j] -= T[i][k] * T[j][k];
+    }
+    __syncthreads();
+  }
+  // L⁻¹ by row-wise forward substitution; 4 threads share each dot product.
+  for (int i = 0; i < n; ++i) {
+    const int j = tid >> 2;
+    const int q = tid & 3;
+    double s = 0.0;
+    if (j <= i && j < n) {
+      for (int k = j + q; k < i; k += 4) s += T[i][k] * T[j][k + 1];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (q == 0 && j <= i && j < n) T[j][i + 1] = ((i == j ? 1.0 : 0.0) - s) / T[i][i];
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e % n;
+    a[(int64_t)i * lda + j] = j <= i ? T[i][j] : 0.0;
+    linv[(int64_t)i * ldl + j] = j <= i ? T[j][i + 1] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 2-D copy through row/column maps: dst[i][j] = src[rm(i)][cm(j)]
+// mode 0: full, mode 1: lower triangle, zero strict upper.
+__global__ void copy2d_kernel(const double* __restrict__ src, int64_t lds, RowMap rm, RowMap cmap,
+                              double* __restrict__ dst, int64_t ldd, int rows, int cols, int mode) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+    if (j >= cols) continue;
+    double v = 0.0;
+    if (mode == 0 || j <= i) v = src[map_idx(rm, i) * lds + map_idx(cmap, j)];
+    dst[(int64_t)i * ldd + j] = v;
+  }
+}
+
+// dst[rm(i)][cm(j)] = src[i][j]  (scatter through maps)
+__global__ void scatter2d_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                                 int64_t ldd, RowMap rm, RowMap cmap, int rows, int cols) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+    if (j >= cols) continue;
+    dst[map_idx(rm, i) * ldd + map_idx(cmap, j)] = src[(int64_t)i * lds + j];
+  }
+}
+
+__global__ void fill2d_kernel(double* __restrict__ dst, int64_t ldd, int rows, int cols, double v,
+                              double diag) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+    if (j >= cols) continue;
+    dst[(int64_t)i * ldd + j] = (i == j) ? diag : v;
+  }
+}
+
+// Σ[c(i)][c(i)] = 1 / A[c(i)][c(i)]   (Jacobi seed of BASELINE c1/c2)
+__global__ void jacobi_diag_kernel(const double* __restrict__ a, int64_t lda, double* __restrict__ s,
+                                   int64_t lds, RowMap cmap, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t g = map_idx(cmap, i);
+  s[g * lds + g] = 1.0 / a[g * lda + g];
+}
+
+// max|a| and max|a - aᵀ| over the n×n block starting at (off, off).
+// Non-negative doubles order like their bit patterns, so atomicMax on u64.
+__global__ void symcheck_kernel(const double* __restrict__ a, int64_t lda, int64_t off, int n,
+                                unsigned long long* out) {
+  __shared__ double tile[32][33];
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj > bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  double mabs = 0.0, mskew = 0.0;
+  for (int r = ty; r < 32; r += blockDim.y) {
+    const int i = bj * 32 + r, j = bi * 32 + tx;
+    tile[r][tx] = (i < n && j < n) ? a[(off + i) * lda + off + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += blockDim.y) {
+    const int i = bi * 32 + r, j = bj * 32 + tx;
+    if (i < n && j < n) {
+      const double v = a[(off + i) * lda + off + j];
+      mabs = fmax(mabs, fabs(v));
+      mskew = fmax(mskew, fabs(v - tile[tx][r]));
+      if (v != v) mskew = __longlong_as_double(0x7ff8000000000000ll);
+    }
+  }
+  mabs = warp_max(mabs);
+  mskew = warp_max(mskew);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, (unsigned long long)__double_as_longlong(mabs));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(mskew));
+  }
+}
+
+// y[r] = sum_j B[r][j] * v   (power-iteration start y1 = B·(1/√c)·1, linalg.py:230,235)
+__global__ void rowsum_scaled_kernel(const double* __restrict__ b, int64_t ldb, int rows, int cols, double v,
+                                     double* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const double* row = b + (int64_t)warp * ldb;
+  double s = 0.0;
+  for (int j = lane; j < cols; j += 32) s = fma(row[j], v, s);
+  s = warp_sum(s);
+  if (lane == 0) y[warp] = s;
+}
+
+// Deterministic sum of `n` partials -> out[0] = sqrt(sum) (frobenius) and out[1] = sum.
+__global__ void reduce_partials_kernel(const double* __restrict__ part, int n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    out[0] = sqrt(tot);
+    out[1] = tot;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Power iteration for ‖B‖₂ on the Gram matrix (exact restatement of
+// linalg.py:223-253), one cooperative persistent kernel, one
+// grid barrier per iteration, deterministic fixed-order reductions so every
+// CTA takes the same branch.
+//
+//   mode 0 ("row Gram", G = B·Bᵀ, n = rows of B):
+//     y_1 = B·(1/√c)·1 (given), σ_k = ‖y_k‖, z = G y_k, nw = √(y_kᵀ z) (= ‖Bᵀ y_k‖),
+//     y_{k+1} = z / nw.
+//   mode 1 ("column Gram", H = Bᵀ·B, n = cols of B):
+//     v_1 = (1/√n)·1, z = H v_k, σ_k = √(v_kᵀ z) (= ‖B v_k‖), nw = ‖z‖, v_{k+1} = z / nw.
+//
+// The σ == 0 restart (linalg.py:237-244) uses the host-generated
+// default_rng(0x5EED) vector `vr` (normalised); mode 0 forms y = B·vr.
+struct PowerParams {
+  const double* G; int64_t ldg; int n;
+  const double* B; int64_t ldb; int brows, bcols;
+  const double* vr;
+  double* vec;      // 2*n
+  double* part;     // 2 * gridDim.x * 2
+  double rtol;
+  int max_iters;
+  int mode;
+  int smem_cap;     // doubles of dynamic shared memory available for staging
+  double* out;      // sigma, converged, iterations
+};
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { red[2 * w] = a; red[2 * w + 1] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sa = 0.0, sb = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { sa += red[2 * i]; sb += red[2 * i + 1]; }
+    a = sa; b = sb;
+  }
+}
+
+// Fixed-order reduce of the per-CTA partials (same result in every CTA).
+__device__ __forceinline__ void grid_sum2(const double* part, int nb, double& a, double& b, double* bc) {
+  if (threadIdx.x < 32) {
+    double sa = 0.0, sb = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) { sa += part[2 * i]; sb += part[2 * i + 1]; }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (threadIdx.x == 0) { bc[0] = sa; bc[1] = sb; }
+  }
+  __syncthreads();
+  a = bc[0];
+  b = bc[1];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(512) power_gram_kernel(PowerParams P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double ys[];           // n doubles (the current iterate, scaled)
+  __shared__ double red[64];
+  __shared__ double bc[2];
+  const int nwarps = blockDim.x >> 5;
+  const int gw = blockIdx.x * nwarps + (threadIdx.x >> 5);
+  const int tw = gridDim.x * nwarps;
+  const int lane = threadIdx.x & 31;
+  const int n = P.n;
+  int cur = 0, phase = 0, it = 1;
+  bool restarted = false;
+  double prev = -1.0, sigma = 0.0, sc = 1.0;
+  const bool stage = n <= P.smem_cap;
+
+  // z = M·(xs·xin) on this warp's rows, written to zout; partial sums of
+  // (xs·xin)·z and z·z.  `stage` copies the input vector to shared memory
+  // (n ≤ smem_cap); otherwise it is read through L2 (__ldcg: other CTAs wrote it).
+  auto matvec = [&](const double* M, int64_t ldm, int rows, int cols, const double* xin, double xs, bool stage,
+                    double* zout, double& pyz, double& pzz) {
+    if (stage) {
+      for (int j = threadIdx.x; j < cols; j += blockDim.x) ys[j] = xs * __ldcg(xin + j);
+      __syncthreads();
+    }
+    pyz = 0.0;
+    pzz = 0.0;
+    for (int r = gw; r < rows; r += tw) {
+      const double* row = M + (int64_t)r * ldm;
+      double s = 0.0;
+      if (stage) {
+        for (int j = lane; j < cols; j += 32) s = fma(row[j], ys[j], s);
+      } else {
+        for (int j = lane; j < cols; j += 32) s = fma(row[j], xs * __ldcg(xin + j), s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        zout[r] = s;
+        if (r < cols) pyz = fma(stage ? ys[r] : xs * __ldcg(xin + r), s, pyz);
+        pzz = fma(s, s, pzz);
+      }
+    }
+    __syncthreads();
+  };
+
+  auto publish = [&](double a, double b) {   // block partial -> part[phase]
+    block_sum2(a, b, red);
+    if (threadIdx.x == 0) {
+      P.part[(size_t)(phase & 1) * 2 * gridDim.x + 2 * blockIdx.x] = a;
+      P.part[(size_t)(phase & 1) * 2 * gridDim.x + 2 * blockIdx.x + 1] = b;
+    }
+    grid.sync();
+    double ra, rb;
+    grid_sum2(P.part + (size_t)(phase & 1) * 2 * gridDim.x, gridDim.x, ra, rb, bc);
+    ++phase;
+    return make_double2(ra, rb);
+  };
+
+  double conv = 0.0;
+  if (P.mode == 0) {
+    // σ_1 = ‖y_1‖
+    double pz = 0.0;
+    for (int r = gw; r < n; r += tw)
+      if (lane == 0) pz = fma(__ldcg(P.vec + r), __ldcg(P.vec + r), pz);
+    double2 s = publish(0.0, pz);
+    sigma = sqrt(s.y);
+    for (;;) {
+      if (sigma == 0.0) {
+        if (restarted) { sigma = 0.0; conv = 1.0; break; }
+        // y = B·vr
+        double pyz, pzz;
+        matvec(P.B, P.ldb, P.brows, P.bcols, P.vr, 1.0, false, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+        cur ^= 1;
+        s = publish(0.0, pzz);
+        restarted = true;
+        prev = -1.0;
+        if (it >= P.max_iters) { sigma = 0.0; conv = 0.0; it = P.max_iters; break; }
+        ++it;
+        sigma = sqrt(s.y);
+        sc = 1.0;
+        continue;
+      }
+      if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
+      prev = sigma;
+      double pyz, pzz;
+      matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+      s = publish(pyz, pzz);
+      const double nw = sqrt(s.x);
+      if (nw == 0.0) { conv = 1.0; break; }
+      if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+      sigma = sqrt(s.y) / nw;
+      sc = 1.0 / nw;
+      cur ^= 1;
+      ++it;
+    }
+  } else {
+    // v_1 = 1/√n (reference np.full(n, 1/sqrt(n)))
+    const double v1 = 1.0 / sqrt((double)n);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) P.vec[j] = v1;
+    grid.sync();
+    for (;;) {
+      double pyz, pzz;
+      matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+      double2 s = publish(pyz, pzz);
+      sigma = sqrt(fmax(s.x, 0.0));
+      if (sigma == 0.0) {
+        if (restarted) { conv = 1.0; break; }
+        if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+          P.vec[(size_t)cur * n + j] = P.vr[j];
+        grid.sync();
+        restarted = true;
+        prev = -1.0;
+        sc = 1.0;
+        ++it;
+        continue;
+      }
+      if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
+      prev = sigma;
+      const double nw = sqrt(s.y);
+      if (nw == 0.0) { conv = 1.0; break; }
+      if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+      sc = 1.0 / nw;
+      cur ^= 1;
+      ++it;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    P.out[0] = sigma;
+    P.out[1] = conv;
+    P.out[2] = (double)it;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA throughput probe (the FP64 roofline denominator, measured on the box).
+__global__ void dmma_probe_kernel(double* out, int iters, double a, double b) {
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; i++) { c[i][0] = threadIdx.x; c[i][1] = i; }
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) dmma_8x8x4(c[i][0], c[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+}  // namespace ibmi

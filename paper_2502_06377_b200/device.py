@@ -1,0 +1,229 @@
+"""Device-resident IBMI state: one ``ibmi_ctx`` of the CUDA library.
+
+:class:`DeviceSolver` owns A, Σ, the per-set caches (A_II⁻¹, W) and the
+estimate buffers in HBM, and exposes the sweep pieces the reference's
+``solve`` loop is made of (`/root/reference/pkg/src/ibmi/solver.py:241-270`).
+Non-contiguous partitions whose sets are pairwise disjoint (red-black,
+custom disjoint JSON) are relabelled so every set is a run (the sweep is
+permutation-equivariant: Σ(PAPᵀ) = PΣ(A)Pᵀ); Σ is mapped back on the way out.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi
+from .partition import Partition, block_permutation, complement, contiguous_ranges
+
+RESTART_SEED = 0x5EED   # reference linalg.py:49
+
+
+def restart_vector(n: int) -> np.ndarray:
+    """The normalised ``default_rng(0x5EED)`` draw of linalg.py:240-241."""
+    v = np.random.default_rng(RESTART_SEED).standard_normal(n)
+    return np.ascontiguousarray(v / np.linalg.norm(v))
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda", False))
+
+
+class DeviceSolver:
+    """IBMI state for one solve on one GPU.
+
+    ``a`` is a float64 numpy array (copied host→device) or a float64 CUDA
+    torch tensor (copied device→device).  ``ranges`` is a list of ``(lo, hi)``
+    runs, or pass ``partition=`` to derive them (and a relabelling if needed).
+    """
+
+    def __init__(self, a, ranges=None, *, partition: Partition | None = None, device: int = 0,
+                 stream: int | None = None, perm: np.ndarray | None = None):
+        L = _abi.lib()
+        self._L = L
+        self.device = int(device)
+        self.perm = None
+        if partition is not None:
+            ranges = contiguous_ranges(partition)
+            if ranges is None:
+                bp = block_permutation(partition)
+                if bp is None:
+                    raise NotImplementedError(
+                        "overlapping non-contiguous partitions are not supported on the B200 path yet")
+                self.perm, ranges = bp
+        elif perm is not None:
+            self.perm = np.asarray(perm, dtype=np.int64)
+        if ranges is None:
+            raise ValueError("need ranges or partition")
+        self.ranges = [(int(lo), int(hi)) for lo, hi in ranges]
+        on_dev = _is_cuda_tensor(a)
+        if on_dev:
+            import torch
+
+            if a.dtype != torch.float64:
+                a = a.to(torch.float64)
+            if a.stride(1) != 1:
+                a = a.contiguous()
+            if self.perm is not None:
+                idx = torch.as_tensor(self.perm, device=a.device)
+                a = a.index_select(0, idx).index_select(1, idx).contiguous()
+            p, lda = a.shape[0], a.stride(0)
+            self._a_keep = a
+        else:
+            a = np.asarray(a, dtype=np.float64)
+            if self.perm is not None:
+                a = a[np.ix_(self.perm, self.perm)]
+            a = np.ascontiguousarray(a)
+            p, lda = a.shape[0], a.shape[1]
+        self.p = int(p)
+        h = C.c_void_p()
+        _abi.check(L.ibmi_create(C.byref(h), self.device, self.p, C.c_void_p(stream or 0)), "ibmi_create")
+        self._h = h
+        try:
+            _abi.check(L.ibmi_set_matrix(h, C.c_void_p(_abi.dptr(a)), lda, int(on_dev)), "set_matrix")
+            k = len(self.ranges)
+            lo = (C.c_int64 * k)(*[r[0] for r in self.ranges])
+            hi = (C.c_int64 * k)(*[r[1] for r in self.ranges])
+            _abi.check(L.ibmi_set_partition(h, k, lo, hi), "set_partition")
+            self._restart_n = None
+            self._set_restart(self.p - (self.ranges[-1][1] - self.ranges[-1][0]))
+        except BaseException:
+            self.close()
+            raise
+        self._a_keep = None
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.ibmi_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- pieces
+    def _set_restart(self, n: int):
+        if n >= 1 and n != self._restart_n:
+            v = restart_vector(n)
+            _abi.check(self._L.ibmi_set_restart_vector(self._h, n, _abi.dbl_ptr(v)), "set_restart_vector")
+            self._restart_n = n
+
+    def setup(self, first: int = 0, count: int = -1):
+        fs, fp = C.c_int(-1), C.c_int64(-1)
+        rc = self._L.ibmi_setup(self._h, first, count, C.byref(fs), C.byref(fp))
+        _abi.check(rc, "setup", fail_set=fs.value, fail_pivot=fp.value)
+
+    def init_sigma(self, kind: int = _abi.GUESS_IDENTITY, guess: np.ndarray | None = None):
+        if kind == _abi.GUESS_MATRIX:
+            g = np.ascontiguousarray(np.asarray(guess, dtype=np.float64))
+            if self.perm is not None:
+                g = self._permute_guess(g)
+            _abi.check(self._L.ibmi_init_sigma(self._h, kind, C.c_void_p(g.ctypes.data), g.shape[1], 0), "init_sigma")
+        else:
+            _abi.check(self._L.ibmi_init_sigma(self._h, kind, None, 0, 0), "init_sigma")
+
+    def _permute_guess(self, g):
+        # guess is over the ascending original complement of set 0; the
+        # device complement of set 0 is perm[[0,lo) ∪ [hi,p)] in that order.
+        lo, hi = self.ranges[0]
+        dev_c = np.concatenate([self.perm[:lo], self.perm[hi:]])
+        order = np.argsort(np.argsort(dev_c))   # rank of each device index in the ascending list
+        return np.ascontiguousarray(g[np.ix_(order, order)])
+
+    def set_sigma(self, s):
+        if _is_cuda_tensor(s):
+            import torch
+
+            s = s.to(torch.float64).contiguous()
+            if self.perm is not None:
+                idx = torch.as_tensor(self.perm, device=s.device)
+                s = s.index_select(0, idx).index_select(1, idx).contiguous()
+            _abi.check(self._L.ibmi_set_sigma(self._h, C.c_void_p(s.data_ptr()), s.stride(0), 1), "set_sigma")
+            return
+        s = np.asarray(s, dtype=np.float64)
+        if self.perm is not None:
+            s = s[np.ix_(self.perm, self.perm)]
+        s = np.ascontiguousarray(s)
+        _abi.check(self._L.ibmi_set_sigma(self._h, C.c_void_p(s.ctypes.data), s.shape[1], 0), "set_sigma")
+
+    def sigma(self, out: np.ndarray | None = None, on_device: bool = False):
+        """Σ as a host numpy array (default) or a CUDA torch tensor."""
+        if on_device:
+            import torch
+
+            t = torch.empty((self.p, self.p), dtype=torch.float64, device=f"cuda:{self.device}")
+            _abi.check(self._L.ibmi_get_sigma(self._h, C.c_void_p(t.data_ptr()), self.p, 1), "get_sigma")
+            if self.perm is not None:
+                inv = torch.as_tensor(np.argsort(self.perm), device=t.device)
+                t = t.index_select(0, inv).index_select(1, inv)
+            return t
+        host = np.empty((self.p, self.p)) if (out is None or self.perm is not None) else out
+        _abi.check(self._L.ibmi_get_sigma(self._h, C.c_void_p(host.ctypes.data), host.shape[1], 0), "get_sigma")
+        if self.perm is not None:
+            inv = np.argsort(self.perm)
+            host = host[np.ix_(inv, inv)]
+            if out is not None:
+                out[...] = host
+                return out
+        return host
+
+    def block_update(self, k: int):
+        _abi.check(self._L.ibmi_block_update(self._h, int(k)), "block_update")
+
+    def error_estimate(self, k: int, rtol: float, max_iters: int):
+        lo, hi = self.ranges[k]
+        self._set_restart(self.p - (hi - lo))
+        e, it, cv = C.c_double(), C.c_int(), C.c_int()
+        _abi.check(self._L.ibmi_error_estimate(self._h, int(k), float(rtol), int(max_iters), C.byref(e),
+                                               C.byref(it), C.byref(cv)), "error_estimate")
+        return e.value, it.value, bool(cv.value)
+
+    def sweep(self, rtol: float, max_iters: int):
+        lo, hi = self.ranges[-1]
+        self._set_restart(self.p - (hi - lo))
+        e, it, cv = C.c_double(), C.c_int(), C.c_int()
+        _abi.check(self._L.ibmi_sweep(self._h, float(rtol), int(max_iters), C.byref(e), C.byref(it), C.byref(cv)),
+                   "sweep")
+        return e.value, it.value, bool(cv.value)
+
+    def sweep_timed(self, rtol: float, max_iters: int):
+        """Sweep without the graph, returning per-kernel-class device ms."""
+        lo, hi = self.ranges[-1]
+        self._set_restart(self.p - (hi - lo))
+        e, it, cv = C.c_double(), C.c_int(), C.c_int()
+        t = (C.c_float * 6)()
+        _abi.check(self._L.ibmi_sweep_timed(self._h, float(rtol), int(max_iters), C.byref(e), C.byref(it),
+                                            C.byref(cv), t), "sweep_timed")
+        keys = ("panel_gemm", "diag_gemm", "estimate_gemm", "gram_gemm", "power_iteration", "sweep")
+        return e.value, it.value, bool(cv.value), dict(zip(keys, list(t)))
+
+    def frobenius(self) -> float:
+        out = C.c_double()
+        _abi.check(self._L.ibmi_frobenius_residual(self._h, C.byref(out)), "frobenius_residual")
+        return out.value
+
+    def device_bytes(self) -> int:
+        b = C.c_int64()
+        _abi.check(self._L.ibmi_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+
+def probe_fp64_peak(device: int = 0) -> float:
+    """Measured DMMA FP64 throughput in TFLOP/s (roofline denominator)."""
+    out = C.c_double()
+    _abi.check(_abi.lib().ibmi_probe_fp64_peak(int(device), C.byref(out)), "probe_fp64_peak")
+    return out.value
+
+
+def complement_of(part: Partition, j: int) -> np.ndarray:
+    return complement(part, j)

@@ -1,0 +1,235 @@
+"""Drop-in IBMI solver API on the B200 path.
+
+Names, signatures, defaults, return types and error behaviour follow the
+reference's ``ibmi.solver`` (`/root/reference/pkg/src/ibmi/solver.py:41-278`);
+every flop runs in ``libibmi_b200.so`` (FP64 DMMA kernels on sm_100a).  There
+is no CPU fallback: without the CUDA library these functions raise.
+
+Extensions (all optional, defaults reproduce the reference):
+
+* ``IbmiConfig.initial_guess="jacobi"``: Σ₀[c₁,c₁] = diag(1/A_ii) (BASELINE c1/c2);
+* ``IbmiConfig.stopping="frobenius"``: stop on ‖I − AΣ‖_F < tol (BASELINE c2);
+* ``SolveReport.power_iterations`` / ``residual_trace`` / ``setup_seconds``;
+* ``solve(..., result_on_device=True)`` returns Σ as a CUDA tensor.
+"""
+
+from __future__ import annotations
+
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .device import DeviceSolver
+from .exceptions import DimensionMismatch, NoConvergenceWarning
+from .partition import Partition, complement, validate
+
+__all__ = [
+    "GUESS_CHOICES",
+    "IbmiConfig",
+    "SolveReport",
+    "block_update",
+    "error_estimate",
+    "initial_guess_identity",
+    "initial_guess_local_inverse",
+    "make_initial_guess",
+    "solve",
+]
+
+POWER_RTOL = 1e-9          # reference linalg.py:47
+POWER_MAX_ITERS = 5000     # reference linalg.py:48
+
+GUESS_IDENTITY = "identity"
+GUESS_LOCAL_INVERSE = "local"
+GUESS_MONTE_CARLO = "mc"
+GUESS_TAKAHASHI = "takahashi"
+GUESS_JACOBI = "jacobi"
+GUESS_CHOICES = (GUESS_IDENTITY, GUESS_LOCAL_INVERSE, GUESS_MONTE_CARLO, GUESS_TAKAHASHI, GUESS_JACOBI)
+STOPPING_CHOICES = ("estimate", "frobenius")
+
+
+@dataclass(frozen=True)
+class IbmiConfig:
+    """Solver controls (reference solver.py:62-91, same fields and checks)."""
+
+    tol: float = 1e-8
+    max_iterations: int = 500
+    initial_guess: str = GUESS_IDENTITY
+    mc_samples: int = 100
+    mc_seed: int = 0
+    norm_rtol: float = POWER_RTOL
+    norm_max_iters: int = POWER_MAX_ITERS
+    stopping: str = "estimate"
+
+    def __post_init__(self):
+        if not self.tol > 0:
+            raise ValueError(f"tol must be positive, got {self.tol}")
+        if self.max_iterations < 1:
+            raise ValueError(f"max_iterations must be >= 1, got {self.max_iterations}")
+        if self.initial_guess not in GUESS_CHOICES:
+            raise ValueError(
+                f"unknown initial guess {self.initial_guess!r}; expected one of {GUESS_CHOICES}")
+        if self.initial_guess == GUESS_MONTE_CARLO and self.mc_samples < 1:
+            raise ValueError(f"mc_samples must be >= 1, got {self.mc_samples}")
+        if self.stopping not in STOPPING_CHOICES:
+            raise ValueError(f"unknown stopping rule {self.stopping!r}; expected one of {STOPPING_CHOICES}")
+
+
+@dataclass
+class SolveReport:
+    """Outcome of one solve (reference solver.py:94-106) plus device extras."""
+
+    iterations: int
+    converged: bool
+    error_trace: list[float]
+    wall_times: list[float]
+    result: object = field(repr=False)
+    power_iterations: list[int] = field(default_factory=list)
+    residual_trace: list[float] = field(default_factory=list)
+    setup_seconds: float = 0.0
+
+    @property
+    def total_seconds(self) -> float:
+        return float(sum(self.wall_times))
+
+
+def initial_guess_identity(comp_size: int) -> np.ndarray:
+    """solver.py:158-159."""
+    return np.eye(comp_size)
+
+
+def initial_guess_local_inverse(a, comp) -> np.ndarray:
+    """solver.py:162-164 — inverse of A[c, c], computed on the GPU."""
+    from .linalg import spd_inverse
+
+    comp = np.asarray(comp, dtype=np.intp)
+    a = np.asarray(a, dtype=np.float64)
+    return spd_inverse(a[np.ix_(comp, comp)])
+
+
+def make_initial_guess(a, comp, cfg: IbmiConfig) -> np.ndarray:
+    """solver.py:215-222 for the guesses available on the device path."""
+    if cfg.initial_guess == GUESS_IDENTITY:
+        return initial_guess_identity(len(comp))
+    if cfg.initial_guess == GUESS_LOCAL_INVERSE:
+        return initial_guess_local_inverse(a, comp)
+    if cfg.initial_guess == GUESS_JACOBI:
+        d = np.diag(np.asarray(a, dtype=np.float64))[np.asarray(comp, dtype=np.intp)]
+        return np.diag(1.0 / d)
+    raise NotImplementedError(f"initial guess {cfg.initial_guess!r} is not available on the B200 path yet")
+
+
+_GUESS_KIND = {GUESS_IDENTITY: _abi.GUESS_IDENTITY, GUESS_JACOBI: _abi.GUESS_JACOBI,
+               GUESS_LOCAL_INVERSE: _abi.GUESS_LOCAL}
+
+
+def _shape_of(a):
+    return tuple(a.shape) if hasattr(a, "shape") else np.asarray(a).shape
+
+
+def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
+          result_on_device: bool = False, callback=None) -> SolveReport:
+    """Approximate ``inv(A)`` by sweeping block updates over ``part``
+    (reference solver.py:225-278).
+
+    Each sweep applies the sets' updates in order, then evaluates the
+    reference's error estimate on the last set; the solve stops when it is
+    ≤ ``cfg.tol`` (or ‖I − AΣ‖_F < tol with ``stopping="frobenius"``).
+    Hitting ``max_iterations`` gives ``converged=False``; it is not raised.
+    ``a`` may be a numpy array or a float64 CUDA tensor already in HBM.
+    """
+    cfg = cfg or IbmiConfig()
+    if not hasattr(a, "is_cuda"):
+        a = np.asarray(a, dtype=np.float64)
+    validate(part)
+    if _shape_of(a) != (part.p, part.p):
+        raise DimensionMismatch(
+            f"matrix shape {_shape_of(a)} does not match partition over {part.p} indices")
+    if cfg.initial_guess not in _GUESS_KIND:
+        raise NotImplementedError(f"initial guess {cfg.initial_guess!r} is not available on the B200 path yet")
+
+    with DeviceSolver(a, partition=part, device=device) as ds:
+        t0 = time.perf_counter()
+        ds.setup()
+        ds.init_sigma(_GUESS_KIND[cfg.initial_guess])
+        setup_s = time.perf_counter() - t0
+        errs, walls, pits, resid = [], [], [], []
+        converged, it = False, 0
+        while it < cfg.max_iterations:
+            start = time.perf_counter()
+            it += 1
+            err, pit, pconv = ds.sweep(cfg.norm_rtol, cfg.norm_max_iters)
+            fr = ds.frobenius() if cfg.stopping == "frobenius" else None
+            walls.append(time.perf_counter() - start)
+            if not pconv:
+                warnings.warn(
+                    f"two_norm: power iteration did not stabilize in {cfg.norm_max_iters} "
+                    f"iterations; returning last estimate {err:.6e}", NoConvergenceWarning, stacklevel=2)
+            errs.append(err)
+            pits.append(pit)
+            if fr is not None:
+                resid.append(fr)
+            if callback is not None:
+                callback(it, err, fr)
+            if (fr < cfg.tol) if fr is not None else (err <= cfg.tol):
+                converged = True
+                break
+        result = ds.sigma(on_device=result_on_device)
+    return SolveReport(iterations=it, converged=converged, error_trace=errs, wall_times=walls, result=result,
+                       power_iterations=pits, residual_trace=resid, setup_seconds=setup_s)
+
+
+def _single_set(a, sigma, idx, comp):
+    """Shared argument handling of block_update / error_estimate: returns the
+    device layout (ranges or a relabelling putting idx first)."""
+    p = sigma.shape[0]
+    idx = np.asarray(idx, dtype=np.intp).ravel()
+    comp = np.asarray(comp, dtype=np.intp).ravel()
+    allidx = np.concatenate([idx, comp])
+    if idx.size == 0 or allidx.size != p or not np.array_equal(np.sort(allidx), np.arange(p)):
+        raise ValueError("idx and comp must partition every row/column index")
+    if np.array_equal(idx, np.arange(idx[0], idx[0] + idx.size)) and \
+            np.array_equal(comp, np.concatenate([np.arange(0, idx[0]), np.arange(idx[-1] + 1, p)])):
+        return [(int(idx[0]), int(idx[-1]) + 1)], None
+    # relabel: idx first (in the given order), then comp in the given order
+    return [(0, idx.size)], np.concatenate([idx, comp]).astype(np.int64)
+
+
+def block_update(a, sigma, idx, comp) -> None:
+    """Apply one block-inverse update to ``sigma`` in place (solver.py:132-144).
+
+    Like the reference, only a float64 ndarray ``sigma`` is updated in place;
+    any other input is converted and the result is discarded.
+    """
+    a = np.asarray(a, dtype=np.float64)
+    sigma = np.asarray(sigma)
+    if a.shape != sigma.shape or a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionMismatch(f"matrix/approximation shapes differ: {a.shape} vs {sigma.shape}")
+    target = sigma if sigma.dtype == np.float64 else np.asarray(sigma, dtype=np.float64)
+    ranges, perm = _single_set(a, target, idx, comp)
+    with DeviceSolver(a, ranges, perm=perm) as ds:
+        ds.setup()
+        ds.set_sigma(target)
+        ds.block_update(0)
+        out = ds.sigma()
+    target[...] = out
+
+
+def error_estimate(a, sigma, idx, comp, rtol: float = POWER_RTOL, max_iters: int = POWER_MAX_ITERS) -> float:
+    """Spectral norm of ``S_I A_{I,c} + S_{I,c} A_c`` (solver.py:147-155)."""
+    a = np.asarray(a, dtype=np.float64)
+    sigma = np.asarray(sigma, dtype=np.float64)
+    if a.shape != sigma.shape or a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionMismatch(f"matrix/approximation shapes differ: {a.shape} vs {sigma.shape}")
+    ranges, perm = _single_set(a, sigma, idx, comp)
+    if ranges[0][1] - ranges[0][0] == a.shape[0]:
+        raise DimensionMismatch("matrix must be nonempty, got shape (%d, 0)" % a.shape[0])
+    with DeviceSolver(a, ranges, perm=perm) as ds:
+        ds.set_sigma(sigma)
+        err, _, conv = ds.error_estimate(0, rtol, max_iters)
+    if not conv:
+        warnings.warn(f"two_norm: power iteration did not stabilize in {max_iters} iterations; "
+                      f"returning last estimate {err:.6e}", NoConvergenceWarning, stacklevel=2)
+    return err

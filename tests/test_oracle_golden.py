@@ -1,0 +1,56 @@
+"""Pin the CPU oracle (oracle/ibmi_oracle.py) to the reference's own outputs
+frozen in tests/golden/ by tests/golden/make_golden.py (which imports the
+reference package and asserted bit-equality there)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import ibmi_oracle as orc
+from paper_2502_06377_b200 import configs, contiguous_partition
+
+
+def test_oracle_small_solves_bitwise():
+    pins = golden("pins.npz")
+    for n in range(5):
+        a = pins[f"case{n}_a"]
+        p, k, f = pins[f"case{n}_pkf"]
+        part = contiguous_partition(int(p), int(k), float(f))
+        o = orc.solve(a, part.sets, tol=1e-12, max_iterations=60)
+        assert np.array_equal(o["result"], pins[f"case{n}_sigma"])
+        assert np.array_equal(np.array(o["error_trace"]), pins[f"case{n}_errs"])
+        idx, comp = part.sets[0], orc.complement(int(p), part.sets[0])
+        s = np.eye(int(p)) + 0.01 * np.ones((int(p), int(p)))
+        orc.BlockOp(a, idx, comp).apply(s)
+        assert np.array_equal(s, pins[f"case{n}_bu"])
+        assert orc.error_estimate(a, s, idx, comp)[0] == pins[f"case{n}_ee"][0]
+
+
+def test_oracle_not_spd_and_restart():
+    pins = golden("pins.npz")
+    from paper_2502_06377_b200 import NotPositiveDefinite
+
+    with pytest.raises(NotPositiveDefinite) as ei:
+        orc.spd_inverse(pins["notspd_a"])
+    assert ei.value.index == pins["notspd_index"][0]
+    s, c, it = orc.power_sigma_max(pins["restart_b"])
+    assert (s, float(c), float(it)) == tuple(pins["restart_out"])
+
+
+def test_oracle_c1_full_solve_bitwise():
+    g = golden("c1.npz")
+    cfg = configs.get_config("c1")
+    a = configs.make_matrix("c1")
+    o = orc.solve(a, cfg.partition().sets, tol=cfg.tol, max_iterations=cfg.max_iterations, guess="jacobi")
+    assert o["iterations"] == int(g["iterations"][0]) == 107
+    assert np.array_equal(o["result"], g["sigma"])
+    assert np.array_equal(np.array(o["error_trace"]), g["error_trace"])
+
+
+def test_oracle_c2_first_sweeps():
+    g = golden("c2.npz")
+    cfg = configs.get_config("c2")
+    a = configs.make_matrix("c2")
+    o = orc.solve(a, cfg.partition().sets, tol=cfg.tol, max_iterations=2, guess="jacobi", stopping="frobenius")
+    assert np.array_equal(np.array(o["error_trace"]), g["error_trace"][:2])
+    np.testing.assert_allclose(o["frobenius_trace"], g["frobenius_trace"][:2], rtol=1e-12)
