@@ -135,6 +135,12 @@ int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64
 int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* restart_v, double rtol,
                   int max_iters, double* sigma, int* iters, int* converged, void* stream);
 
+/* Tuning knobs (process-wide; contexts re-capture their sweep graph):
+ * key 0: GEMM configuration of the hot NT kernels (0: 8 warps 64x32, BK16;
+ *        1: 16 warps 32x32, BK16 [default]; 2: 16 warps 32x32, BK32);
+ * key 1: split-K factor of the Σ_II GEMM (0 = auto); key 2: of the Gram GEMM. */
+int ibmi_tune(int key, int value);
+
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */
 int ibmi_probe_fp64_peak(int device, double* tflops);
 

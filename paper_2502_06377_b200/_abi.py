@@ -48,6 +48,7 @@ SIGNATURES = [
     ("ibmi_spd_inverse", C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(_I64), _P]),
     ("ibmi_two_norm", C.c_int, [_I64, _I64, _P, _I64, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), _P]),
+    ("ibmi_tune", C.c_int, [C.c_int, C.c_int]),
     ("ibmi_probe_fp64_peak", C.c_int, [C.c_int, _D]),
 ]
 

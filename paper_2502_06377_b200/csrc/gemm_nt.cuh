@@ -6,16 +6,18 @@
 // FP64 tensor path is the warp-synchronous DMMA.8x8x4 issued by
 // mma.sync.m8n8k4.f64 (37.1 TFLOP/s measured on B200 = 148 SM x 128 flop/clk x
 // 1.965 GHz).  This kernel is built to keep that pipe saturated:
-//   * 128x128 CTA tile, 8 warps of 64x32, 64 FP64 accumulators per thread;
-//   * 4-stage cp.async shared-memory pipeline, BK = 16;
-//   * k-slot permutation: lane (g, t) holds k = 2t and 2t+1 of every 8-k half,
+//   * 128x128 CTA tile, WM x WN warp tiles (64x32 / 32x32), FP64 accumulators
+//     in registers;
+//   * multi-stage cp.async shared-memory pipeline (BK = 16 or 32);
+//   * k-slot permutation: lane (g, t) holds k = 2t and 2t+1 of every 8-k group,
 //     so one LDS.128 feeds two DMMAs (XOR-swizzled rows -> conflict-free);
 //   * operands are addressed through RowMaps (at most one gap) and up to two
 //     K segments, so Σ[c, c] of a contiguous set is read in place, never
 //     gathered;
 //   * fused epilogues: scaled store (+beta*D), mirrored (transposed) store for
 //     the Σ[c, I] = -Mᵀ half of the update, lower-triangle-only tiles for
-//     symmetric products, and a (δ - acc)² reduction for ‖I − AΣ‖_F.
+//     symmetric products, split-K partial tiles, and a (δ - acc)² reduction
+//     for ‖I − AΣ‖_F.
 //
 // Every GEMM of the sweep (solver.py:124-125, :154), of the setup
 // (solver.py:119-120) and of the residual is of this NT form because A and Σ
@@ -27,19 +29,35 @@ namespace ibmi {
 
 constexpr int GB_M = 128;
 constexpr int GB_N = 128;
-constexpr int GB_K = 16;
-constexpr int G_STAGES = 4;
-constexpr int G_THREADS = 256;
-constexpr int T_LD = 130;                          // padded row of a transposed tile
-constexpr int TILE_DBL = (GB_K * T_LD > GB_M * GB_K) ? GB_K * T_LD : GB_M * GB_K;  // 2080
-constexpr size_t GEMM_SMEM = (size_t)G_STAGES * 2 * TILE_DBL * sizeof(double);   // 133120
+constexpr int T_PAD = 2;                 // transposed tile row = 128 + 2 doubles
+
+template <int BK_, int STAGES_, int WM_, int WN_>
+struct GemmCfg {
+  static constexpr int BK = BK_;
+  static constexpr int STAGES = STAGES_;
+  static constexpr int WM = WM_;
+  static constexpr int WN = WN_;
+  static constexpr int WARPS_M = GB_M / WM;
+  static constexpr int WARPS_N = GB_N / WN;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int MI = WM / 8;      // 8x8 sub-tiles per warp in M
+  static constexpr int NJ = WN / 8;
+  static constexpr int T_LD = GB_M + T_PAD;
+  static constexpr int TILE_DBL = (BK * T_LD > GB_M * BK) ? BK * T_LD : GB_M * BK;
+  static constexpr size_t SMEM = (size_t)STAGES * 2 * TILE_DBL * sizeof(double);
+  static constexpr int MIN_BLOCKS = 1;
+};
+
+using CfgA = GemmCfg<16, 4, 64, 32>;     // 256 threads, 2 warps / scheduler
+using CfgB = GemmCfg<16, 4, 32, 32>;     // 512 threads, 4 warps / scheduler
+using CfgC = GemmCfg<32, 3, 32, 32>;     // 512 threads, BK 32
 
 struct KSeg {
   int64_t x0, y0;  // first physical K column (or row, for transposed operands) of X and Y
   int len;
 };
 
-enum { EPI_STORE = 0, EPI_FROB = 1 };
+enum { EPI_STORE = 0, EPI_FROB = 1, EPI_PARTIAL = 2 };
 
 struct GemmParams {
   const double* X; int64_t ldx; RowMap xm;   // XT=false: X[xm(m)*ldx + x0 + k]; XT=true: X[(x0+k)*ldx + xm.off0 + m]
@@ -47,30 +65,36 @@ struct GemmParams {
   int M, N;
   int nseg; KSeg seg[2];
   int kt0, kt_total;                         // k-tiles in segment 0, in total
+  int splits;                                // split-K factor (EPI_PARTIAL)
   double* C; int64_t ldc; RowMap cm, cn;
   double alpha, beta;
   const double* D; int64_t ldd; RowMap dm, dn;
   int mirror;                                // also store C[cn(n)][cm(m)]
   int lower;                                 // only tiles tm >= tn; in diagonal tiles only m >= n
   int tiles_m, tiles_n;
-  double* partial;                           // EPI_FROB: one partial sum per CTA
+  double* partial;                           // EPI_FROB: one partial sum per CTA; EPI_PARTIAL: split tiles
 };
 
+template <int BK>
 __device__ __forceinline__ int swz(int r, int k) {   // non-transposed tile element (r, k)
-  return r * GB_K + ((((k >> 1) ^ ((r & 1) << 2))) << 1) + (k & 1);
+  return r * BK + ((((k >> 1) ^ ((r & 1) << 2))) << 1) + (k & 1);
 }
 
-// Issue the cp.async loads of k-tile `kt` of one operand into `dst`.
-template <bool TR, bool V16>
+// Issue the cp.async loads of k-tile `ktl` of one operand into `dst`.
+template <class CF, bool TR, bool V16>
 __device__ __forceinline__ void load_operand(double* dst, const double* base, int64_t ld, const RowMap& map,
                                              int rows_total, int r0, const KSeg& sg, int ktl, int tid) {
-  const int kbase = ktl * GB_K;
+  constexpr int BK = CF::BK;
+  constexpr int NT = CF::THREADS;
+  const int kbase = ktl * BK;
   if (!TR) {
     if (V16) {
-      const int ch = tid & 7;
+      constexpr int CPR = BK / 2;                    // 16-byte chunks per row
+      constexpr int PER = GB_M * CPR / NT;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = (tid >> 3) + 32 * i;
+      for (int i = 0; i < PER; ++i) {
+        const int q = tid + NT * i;
+        const int r = q / CPR, ch = q % CPR;
         const int gr = r0 + r;
         const int kc = kbase + 2 * ch;
         int bytes = 0;
@@ -80,13 +104,14 @@ __device__ __forceinline__ void load_operand(double* dst, const double* base, in
           bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
           if (bytes) src = base + map_idx(map, gr) * ld + sg.x0 + kc;
         }
-        cp_async16(dst + r * GB_K + ((ch ^ ((r & 1) << 2)) << 1), src, bytes);
+        cp_async16(dst + r * BK + ((ch ^ ((r & 1) << 2)) << 1), src, bytes);
       }
     } else {
-      const int e = tid & 15;
+      constexpr int PER = GB_M * BK / NT;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = (tid >> 4) + 16 * i;
+      for (int i = 0; i < PER; ++i) {
+        const int q = tid + NT * i;
+        const int r = q / BK, e = q % BK;
         const int gr = r0 + r;
         const int kc = kbase + e;
         int bytes = 0;
@@ -95,16 +120,18 @@ __device__ __forceinline__ void load_operand(double* dst, const double* base, in
           bytes = 8;
           src = base + map_idx(map, gr) * ld + sg.x0 + kc;
         }
-        cp_async8(dst + swz(r, e), src, bytes);
+        cp_async8(dst + swz<BK>(r, e), src, bytes);
       }
     }
   } else {
-    // transposed operand: tile is [GB_K k-rows][128 columns], columns contiguous from map.off0
+    // transposed operand: tile is [BK k-rows][128 columns], columns contiguous from map.off0
+    constexpr int TL = CF::T_LD;
     if (V16) {
-      const int ch = tid & 63;
+      constexpr int PER = BK * (GB_M / 2) / NT;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int kr = (tid >> 6) + 4 * i;
+      for (int i = 0; i < PER; ++i) {
+        const int q = tid + NT * i;
+        const int kr = q / (GB_M / 2), ch = q % (GB_M / 2);
         const int col = r0 + 2 * ch;
         int bytes = 0;
         const double* src = base;
@@ -113,13 +140,14 @@ __device__ __forceinline__ void load_operand(double* dst, const double* base, in
           bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
           if (bytes) src = base + (sg.x0 + kbase + kr) * ld + map.off0 + col;
         }
-        cp_async16(dst + kr * T_LD + 2 * ch, src, bytes);
+        cp_async16(dst + kr * TL + 2 * ch, src, bytes);
       }
     } else {
-      const int e = tid & 127;
+      constexpr int PER = BK * GB_M / NT;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int kr = (tid >> 7) + 2 * i;
+      for (int i = 0; i < PER; ++i) {
+        const int q = tid + NT * i;
+        const int kr = q / GB_M, e = q % GB_M;
         const int col = r0 + e;
         int bytes = 0;
         const double* src = base;
@@ -127,46 +155,60 @@ __device__ __forceinline__ void load_operand(double* dst, const double* base, in
           bytes = 8;
           src = base + (sg.x0 + kbase + kr) * ld + map.off0 + col;
         }
-        cp_async8(dst + kr * T_LD + e, src, bytes);
+        cp_async8(dst + kr * TL + e, src, bytes);
       }
     }
   }
 }
 
-template <bool XT, bool YT, bool V16, int EPI>
-__global__ void __launch_bounds__(G_THREADS, 1) gemm_nt_kernel(const GemmParams P) {
+template <class CF, bool XT, bool YT, bool V16, int EPI>
+__global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParams P) {
+  constexpr int BK = CF::BK, ST = CF::STAGES, MI = CF::MI, NJ = CF::NJ, TL = CF::T_LD;
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const int g = lane >> 2;
   const int t = lane & 3;
-  const int wm0 = (warp & 1) * 64;
-  const int wn0 = (warp >> 1) * 32;
+  const int wm0 = (warp % CF::WARPS_M) * CF::WM;
+  const int wn0 = (warp / CF::WARPS_M) * CF::WN;
 
+  int tile = blockIdx.x;
+  int split = 0;
+  if (EPI == EPI_PARTIAL) {
+    split = tile % P.splits;
+    tile /= P.splits;
+  }
   int tm, tn;
   if (P.lower) {
-    const int b = blockIdx.x;
-    int r = (int)((sqrt(8.0 * (double)b + 1.0) - 1.0) * 0.5);
-    while ((r + 1) * (r + 2) / 2 <= b) ++r;
-    while (r * (r + 1) / 2 > b) --r;
+    int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+    while (r * (r + 1) / 2 > tile) --r;
     tm = r;
-    tn = b - r * (r + 1) / 2;
+    tn = tile - r * (r + 1) / 2;
   } else {
-    tm = blockIdx.x % P.tiles_m;
-    tn = blockIdx.x / P.tiles_m;
+    tm = tile % P.tiles_m;
+    tn = tile / P.tiles_m;
   }
   const int m0 = tm * GB_M;
   const int n0 = tn * GB_N;
 
-  double acc[8][4][2];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // k-tile range of this CTA (split-K: contiguous chunk of the global k-tile list)
+  int kt_begin = 0, kt_end = P.kt_total;
+  if (EPI == EPI_PARTIAL) {
+    const int per = (P.kt_total + P.splits - 1) / P.splits;
+    kt_begin = min(P.kt_total, split * per);
+    kt_end = min(P.kt_total, kt_begin + per);
+  }
 
-  auto stage_x = [&](int s) { return smem + (size_t)s * 2 * TILE_DBL; };
-  auto stage_y = [&](int s) { return smem + (size_t)s * 2 * TILE_DBL + TILE_DBL; };
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto stage_x = [&](int s) { return smem + (size_t)s * 2 * CF::TILE_DBL; };
+  auto stage_y = [&](int s) { return smem + (size_t)s * 2 * CF::TILE_DBL + CF::TILE_DBL; };
 
   auto issue = [&](int s, int kt) {
     const int sgi = kt < P.kt0 ? 0 : 1;
@@ -174,61 +216,60 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_nt_kernel(const GemmParams 
     KSeg sx = P.seg[sgi];
     KSeg sy = sx;
     sy.x0 = sx.y0;
-    load_operand<XT, V16>(stage_x(s), P.X, P.ldx, P.xm, P.M, m0, sx, ktl, tid);
-    load_operand<YT, V16>(stage_y(s), P.Y, P.ldy, P.yn, P.N, n0, sy, ktl, tid);
+    load_operand<CF, XT, V16>(stage_x(s), P.X, P.ldx, P.xm, P.M, m0, sx, ktl, tid);
+    load_operand<CF, YT, V16>(stage_y(s), P.Y, P.ldy, P.yn, P.N, n0, sy, ktl, tid);
   };
 
-  const int KT = P.kt_total;
+  const int KT = kt_end - kt_begin;
 #pragma unroll
-  for (int s = 0; s < G_STAGES - 1; ++s) {
-    if (s < KT) issue(s, s);
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < KT) issue(s, kt_begin + s);
     cp_async_commit();
   }
 
   for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<G_STAGES - 2>();
+    cp_async_wait<ST - 2>();
     __syncthreads();
     {
-      const int nk = kt + G_STAGES - 1;
-      if (nk < KT) issue(nk % G_STAGES, nk);
+      const int nk = kt + ST - 1;
+      if (nk < KT) issue(nk % ST, kt_begin + nk);
       cp_async_commit();
     }
-    const double* xs = stage_x(kt % G_STAGES);
-    const double* ys = stage_y(kt % G_STAGES);
+    const double* xs = stage_x(kt % ST);
+    const double* ys = stage_y(kt % ST);
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int kk = half * 8;
-      double a[8][2], b[4][2];
+    for (int kk = 0; kk < BK; kk += 8) {
+      double a[MI][2], b[NJ][2];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < MI; ++i) {
         const int r = wm0 + 8 * i + g;
         if (!XT) {
-          const double2 v = *reinterpret_cast<const double2*>(xs + r * GB_K + ((((kk >> 1) + t) ^ ((r & 1) << 2)) << 1));
+          const double2 v = *reinterpret_cast<const double2*>(xs + r * BK + ((((kk >> 1) + t) ^ ((r & 1) << 2)) << 1));
           a[i][0] = v.x;
           a[i][1] = v.y;
         } else {
-          a[i][0] = xs[(kk + 2 * t) * T_LD + r];
-          a[i][1] = xs[(kk + 2 * t + 1) * T_LD + r];
+          a[i][0] = xs[(kk + 2 * t) * TL + r];
+          a[i][1] = xs[(kk + 2 * t + 1) * TL + r];
         }
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         const int r = wn0 + 8 * j + g;
         if (!YT) {
-          const double2 v = *reinterpret_cast<const double2*>(ys + r * GB_K + ((((kk >> 1) + t) ^ ((r & 1) << 2)) << 1));
+          const double2 v = *reinterpret_cast<const double2*>(ys + r * BK + ((((kk >> 1) + t) ^ ((r & 1) << 2)) << 1));
           b[j][0] = v.x;
           b[j][1] = v.y;
         } else {
-          b[j][0] = ys[(kk + 2 * t) * T_LD + r];
-          b[j][1] = ys[(kk + 2 * t + 1) * T_LD + r];
+          b[j][0] = ys[(kk + 2 * t) * TL + r];
+          b[j][1] = ys[(kk + 2 * t + 1) * TL + r];
         }
       }
 #pragma unroll
       for (int s = 0; s < 2; ++s)
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][s], b[j][s]);
+          for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i][s], b[j][s]);
     }
   }
   cp_async_wait<0>();
@@ -237,13 +278,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_nt_kernel(const GemmParams 
   if (EPI == EPI_STORE) {
     const bool diag_tile = P.lower && tm == tn;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < MI; ++i) {
       const int m = m0 + wm0 + 8 * i + g;
       if (m >= P.M) continue;
       const int64_t rowc = map_idx(P.cm, m);
       const int64_t rowd = P.beta != 0.0 ? map_idx(P.dm, m) : 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = n0 + wn0 + 8 * j + 2 * t + e;
@@ -257,16 +298,28 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_nt_kernel(const GemmParams 
         }
       }
     }
+  } else if (EPI == EPI_PARTIAL) {
+    // raw partial tile [128][128] of (tile, split), reduced later in fixed split order
+    double* dst = P.partial + ((size_t)blockIdx.x) * GB_M * GB_N;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int r = wm0 + 8 * i + g;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int c = wn0 + 8 * j + 2 * t;
+        *reinterpret_cast<double2*>(dst + r * GB_N + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    }
   } else {
     // ‖I − XYᵀ‖_F² partial: (δ(cm(m), cn(n)) − acc)²
     double s = 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < MI; ++i) {
       const int m = m0 + wm0 + 8 * i + g;
       if (m >= P.M) continue;
       const int64_t rowc = map_idx(P.cm, m);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = n0 + wn0 + 8 * j + 2 * t + e;
@@ -282,9 +335,42 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_nt_kernel(const GemmParams 
     __syncthreads();
     if (tid == 0) {
       double tot = 0.0;
-      for (int w = 0; w < G_THREADS / 32; ++w) tot += red[w];
+      for (int w = 0; w < CF::THREADS / 32; ++w) tot += red[w];
       P.partial[blockIdx.x] = tot;
     }
+  }
+}
+
+// Fixed-order reduction of split-K partial tiles + the STORE epilogue.
+// grid: one CTA per output tile, 256 threads.
+__global__ void splitk_reduce_kernel(const GemmParams P) {
+  const int tile = blockIdx.x;
+  int tm, tn;
+  if (P.lower) {
+    int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+    while (r * (r + 1) / 2 > tile) --r;
+    tm = r;
+    tn = tile - r * (r + 1) / 2;
+  } else {
+    tm = tile % P.tiles_m;
+    tn = tile / P.tiles_m;
+  }
+  const bool diag_tile = P.lower && tm == tn;
+  const double* src = P.partial + (size_t)tile * P.splits * GB_M * GB_N;
+  for (int e = threadIdx.x; e < GB_M * GB_N; e += blockDim.x) {
+    const int r = e / GB_N, c = e % GB_N;
+    const int m = tm * GB_M + r, n = tn * GB_N + c;
+    if (m >= P.M || n >= P.N) continue;
+    if (diag_tile && m < n) continue;
+    double acc = 0.0;
+    for (int s = 0; s < P.splits; ++s) acc += src[(size_t)s * GB_M * GB_N + e];
+    double v = P.alpha * acc;
+    const int64_t rowc = map_idx(P.cm, m);
+    if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + map_idx(P.dn, n)];
+    const int64_t colc = map_idx(P.cn, n);
+    P.C[rowc * P.ldc + colc] = v;
+    if (P.mirror) P.C[colc * P.ldc + rowc] = v;
   }
 }
 

@@ -55,56 +55,74 @@ struct GemmOp {
   const double* D = nullptr; int64_t ldd = 0; RowMap dm = contig_map(0), dn = contig_map(0);
   bool mirror = false, lower = false;
   double* partial = nullptr;     // non-null -> Frobenius epilogue
+  int splits = 1;                // split-K factor (needs ws: tiles*splits*128*128 doubles)
+  double* ws = nullptr;
   void add_seg(int64_t x0, int64_t y0, int64_t len) {
     if (len > 0) seg[nseg++] = KSeg{x0, y0, (int)len};
   }
 };
 
-template <bool XT, bool YT, bool V16, int EPI>
+// Tuning knobs (ibmi_tune): GEMM configuration of the hot NT kernels and
+// split-K factors of the small-grid GEMMs.
+int g_variant = 1;          // 0: CfgA (8 warps 64x32), 1: CfgB (16 warps 32x32), 2: CfgC (BK 32)
+int g_split_diag = 0;       // split-K of the Σ_II GEMM (0 = auto)
+int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
+int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
+
+template <class CF, bool XT, bool YT, bool V16, int EPI>
 cudaError_t ensure_attr() {
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
   if (!attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_nt_kernel<XT, YT, V16, EPI>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_nt_kernel<CF, XT, YT, V16, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
   return cudaSuccess;
 }
 
-template <bool XT, bool YT, bool V16, int EPI>
+template <class CF, bool XT, bool YT, bool V16, int EPI>
 cudaError_t launch_inst(const GemmParams& P, int grid, cudaStream_t s) {
-  cudaError_t e = ensure_attr<XT, YT, V16, EPI>();
+  cudaError_t e = ensure_attr<CF, XT, YT, V16, EPI>();
   if (e != cudaSuccess) return e;
-  gemm_nt_kernel<XT, YT, V16, EPI><<<grid, G_THREADS, GEMM_SMEM, s>>>(P);
+  gemm_nt_kernel<CF, XT, YT, V16, EPI><<<grid, CF::THREADS, CF::SMEM, s>>>(P);
   return cudaGetLastError();
 }
 
 // Set the dynamic-smem attribute of every instantiation up front (outside any
 // graph capture).
 cudaError_t prepare_gemm_attributes() {
-#define PREP(XT, YT, V, E) \
-  { cudaError_t e = ensure_attr<XT, YT, V, E>(); if (e != cudaSuccess) return e; }
-  PREP(false, false, true, EPI_STORE) PREP(false, false, false, EPI_STORE)
-  PREP(false, true, true, EPI_STORE) PREP(false, true, false, EPI_STORE)
-  PREP(true, true, true, EPI_STORE) PREP(true, true, false, EPI_STORE)
-  PREP(true, false, true, EPI_STORE) PREP(true, false, false, EPI_STORE)
-  PREP(false, false, true, EPI_FROB) PREP(false, false, false, EPI_FROB)
-  PREP(false, true, true, EPI_FROB) PREP(false, true, false, EPI_FROB)
-  PREP(true, true, true, EPI_FROB) PREP(true, true, false, EPI_FROB)
-  PREP(true, false, true, EPI_FROB) PREP(true, false, false, EPI_FROB)
+#define PREP(CF, XT, YT, V, E) \
+  { cudaError_t e = ensure_attr<CF, XT, YT, V, E>(); if (e != cudaSuccess) return e; }
+#define PREP_NN(CF) \
+  PREP(CF, false, false, true, EPI_STORE) PREP(CF, false, false, false, EPI_STORE) \
+  PREP(CF, false, false, true, EPI_FROB) PREP(CF, false, false, false, EPI_FROB) \
+  PREP(CF, false, false, true, EPI_PARTIAL) PREP(CF, false, false, false, EPI_PARTIAL)
+  PREP_NN(CfgA) PREP_NN(CfgB) PREP_NN(CfgC)
+  PREP(CfgA, false, true, true, EPI_STORE) PREP(CfgA, false, true, false, EPI_STORE)
+  PREP(CfgA, true, true, true, EPI_STORE) PREP(CfgA, true, true, false, EPI_STORE)
+  PREP(CfgA, true, false, true, EPI_STORE) PREP(CfgA, true, false, false, EPI_STORE)
+#undef PREP_NN
 #undef PREP
   return cudaSuccess;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int gemm_grid(const GemmOp& op) {
+int gemm_tiles(const GemmOp& op) {
   const int tm = (int)((op.M + GB_M - 1) / GB_M), tn = (int)((op.N + GB_N - 1) / GB_N);
   return op.lower ? tm * (tm + 1) / 2 : tm * tn;
+}
+int gemm_grid(const GemmOp& op) { return gemm_tiles(op); }
+
+template <class CF, bool V16>
+cudaError_t launch_nn(const GemmParams& P, int grid, int epi, cudaStream_t s) {
+  if (epi == EPI_FROB) return launch_inst<CF, false, false, V16, EPI_FROB>(P, grid, s);
+  if (epi == EPI_PARTIAL) return launch_inst<CF, false, false, V16, EPI_PARTIAL>(P, grid, s);
+  return launch_inst<CF, false, false, V16, EPI_STORE>(P, grid, s);
 }
 
 cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
@@ -116,9 +134,11 @@ cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
   P.M = (int)op.M; P.N = (int)op.N;
   P.nseg = op.nseg;
   P.kt0 = 0; P.kt_total = 0;
+  const bool nn = !op.xt && !op.yt;
+  const int bk = (nn && g_variant == 2) ? CfgC::BK : 16;
   for (int i = 0; i < op.nseg; ++i) {
     P.seg[i] = op.seg[i];
-    const int kt = (op.seg[i].len + GB_K - 1) / GB_K;
+    const int kt = (op.seg[i].len + bk - 1) / bk;
     if (i == 0) P.kt0 = kt;
     P.kt_total += kt;
   }
@@ -129,23 +149,57 @@ cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
   P.mirror = op.mirror; P.lower = op.lower;
   P.tiles_m = (P.M + GB_M - 1) / GB_M;
   P.tiles_n = (P.N + GB_N - 1) / GB_N;
-  P.partial = op.partial;
-  const int grid = gemm_grid(op);
+  const int tiles = gemm_tiles(op);
   // 16-byte cp.async only when every operand address it forms is 16B aligned
   bool v16 = aligned16(op.X) && aligned16(op.Y) && (op.ldx % 2 == 0) && (op.ldy % 2 == 0);
   for (int i = 0; i < op.nseg; ++i) v16 = v16 && (op.seg[i].x0 % 2 == 0) && (op.seg[i].y0 % 2 == 0);
   if (op.xt) v16 = v16 && (op.xm.off0 % 2 == 0);
   if (op.yt) v16 = v16 && (op.yn.off0 % 2 == 0);
-  const bool frob = op.partial != nullptr;
-#define DISPATCH(XT, YT)                                                                        \
-  if (frob) return v16 ? launch_inst<XT, YT, true, EPI_FROB>(P, grid, s)                       \
-                       : launch_inst<XT, YT, false, EPI_FROB>(P, grid, s);                     \
-  return v16 ? launch_inst<XT, YT, true, EPI_STORE>(P, grid, s) : launch_inst<XT, YT, false, EPI_STORE>(P, grid, s);
-  if (!op.xt && !op.yt) { DISPATCH(false, false) }
-  if (!op.xt && op.yt) { DISPATCH(false, true) }
-  if (op.xt && op.yt) { DISPATCH(true, true) }
-  DISPATCH(true, false)
-#undef DISPATCH
+  int epi = op.partial ? EPI_FROB : EPI_STORE;
+  int grid = tiles;
+  const bool split = nn && op.splits > 1 && op.ws != nullptr && !op.partial && P.kt_total >= op.splits;
+  if (split) {
+    epi = EPI_PARTIAL;
+    P.splits = op.splits;
+    P.partial = op.ws;
+    grid = tiles * op.splits;
+  } else {
+    P.splits = 1;
+    P.partial = op.partial;
+  }
+  cudaError_t err;
+  if (nn) {
+    if (g_variant == 0) err = v16 ? launch_nn<CfgA, true>(P, grid, epi, s) : launch_nn<CfgA, false>(P, grid, epi, s);
+    else if (g_variant == 2) err = v16 ? launch_nn<CfgC, true>(P, grid, epi, s) : launch_nn<CfgC, false>(P, grid, epi, s);
+    else err = v16 ? launch_nn<CfgB, true>(P, grid, epi, s) : launch_nn<CfgB, false>(P, grid, epi, s);
+  } else if (!op.xt && op.yt) {
+    err = v16 ? launch_inst<CfgA, false, true, true, EPI_STORE>(P, grid, s)
+              : launch_inst<CfgA, false, true, false, EPI_STORE>(P, grid, s);
+  } else if (op.xt && op.yt) {
+    err = v16 ? launch_inst<CfgA, true, true, true, EPI_STORE>(P, grid, s)
+              : launch_inst<CfgA, true, true, false, EPI_STORE>(P, grid, s);
+  } else {
+    err = v16 ? launch_inst<CfgA, true, false, true, EPI_STORE>(P, grid, s)
+              : launch_inst<CfgA, true, false, false, EPI_STORE>(P, grid, s);
+  }
+  if (err != cudaSuccess || !split) return err;
+  splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+// Split factor that fills the SMs: smallest s with tiles*s >= 0.9 * waves * SMs.
+int auto_split(int tiles, int kt_total, int sms) {
+  if (tiles >= 4 * sms) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 8; ++s) {
+    if (kt_total / s < 8) break;
+    const int ctas = tiles * s;
+    const int waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (waves * sms) * (1.0 - 0.01 * (s - 1));
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return best;
 }
 
 dim3 grid2d(int64_t rows, int64_t cols) {
@@ -307,6 +361,8 @@ struct ibmi_ctx {
   double* part = nullptr; int part_cap = 0;
   double* vr = nullptr; int64_t vr_n = 0;
   double* frob_part = nullptr; int frob_cap = 0;
+  double* splitws = nullptr; int64_t splitws_cap = 0;   // split-K partial tiles
+  int graph_gen = -1;
   double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
   double* hpin = nullptr;         // pinned mirror of dscal
   int sms = 148;
@@ -359,6 +415,17 @@ int symcheck(ibmi_ctx* c, int64_t off, int64_t n, const char* what) {
   return IBMI_OK;
 }
 
+// Split-K factor and workspace (doubles) for a GEMM on this context.
+int plan_split(const ibmi_ctx* c, const GemmOp& op, int forced, int64_t* ws_need) {
+  const int tiles = gemm_tiles(op);
+  int64_t klen = 0;
+  for (int i = 0; i < op.nseg; ++i) klen += op.seg[i].len;
+  const int bk = g_variant == 2 ? 32 : 16;
+  const int s = forced > 0 ? forced : auto_split(tiles, (int)((klen + bk - 1) / bk), c->sms);
+  if (ws_need) *ws_need = s > 1 ? (int64_t)tiles * s * GB_M * GB_N : 0;
+  return s;
+}
+
 // ---- one block update: the hot path (solver.py:122-129)
 // `mid` (optional) is recorded between the two GEMMs (for ibmi_sweep_timed).
 int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
@@ -385,6 +452,10 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k2.C = c->S; k2.ldc = c->ld; k2.cm = contig_map(lo); k2.cn = contig_map(lo);
   k2.alpha = -1.0; k2.beta = 1.0; k2.D = s.ainv; k2.ldd = s.ldb;
   k2.lower = true; k2.mirror = true;
+  int64_t need = 0;
+  k2.splits = plan_split(c, k2, g_split_diag, &need);
+  if (need > c->splitws_cap) k2.splits = 1;    // workspace is planned by plan_workspace()
+  k2.ws = c->splitws;
   CUDA_TRY(launch_gemm(k2, c->stream));
   return IBMI_OK;
 }
@@ -404,6 +475,37 @@ int ensure_estimate_buffers(ibmi_ctx* c, int64_t b, int64_t cc) {
   return IBMI_OK;
 }
 
+// Allocate the split-K workspace for every split GEMM of a sweep (before any
+// graph capture: nothing is allocated while capturing).
+int plan_workspace(ibmi_ctx* c) {
+  int64_t need = 0;
+  for (const SetDev& s : c->sets) {
+    GemmOp k2;
+    k2.M = s.b; k2.N = s.b; k2.lower = true;
+    k2.add_seg(0, 0, s.lo);
+    k2.add_seg(s.hi, s.hi, c->p - s.hi);
+    int64_t w = 0;
+    plan_split(c, k2, g_split_diag, &w);
+    need = std::max(need, w);
+  }
+  if (!c->sets.empty()) {
+    const SetDev& s = c->sets.back();
+    const int64_t cc = c->p - s.b;
+    if (s.b <= cc) {
+      GemmOp gg;
+      gg.M = s.b; gg.N = s.b; gg.lower = true;
+      gg.add_seg(0, 0, cc);
+      int64_t w = 0;
+      plan_split(c, gg, g_split_gram, &w);
+      need = std::max(need, w);
+    }
+  }
+  if (need > c->splitws_cap) {
+    if (ensure_buf(&c->splitws, &c->splitws_cap, need, &c->bytes)) return IBMI_ERR_OOM;
+  }
+  return IBMI_OK;
+}
+
 // ---- ‖B‖₂ of a device matrix by the Gram-form power iteration
 // (linalg.py:223-274).  Buffers: G (n×ldG, n = min(rows, cols)), vec (2·max),
 // part (4·blocks), out (3 doubles), vr (cols, normalised restart vector).
@@ -415,6 +517,9 @@ struct NormBufs {
   const double* vr;
   int blocks, threads;
   size_t smem_cap;
+  double* ws;           // split-K workspace for the Gram GEMM (may be null)
+  int64_t ws_cap;
+  int sms;
 };
 
 int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, double rtol, int max_iters,
@@ -434,6 +539,12 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
   gg.M = n; gg.N = n;
   gg.C = nb.G; gg.ldc = nb.ldG;
   gg.lower = true; gg.mirror = true;
+  if (nb.ws && mode == 0) {
+    const int bk = g_variant == 2 ? 32 : 16;
+    gg.splits = g_split_gram > 0 ? g_split_gram : auto_split(gemm_tiles(gg), (int)((cc + bk - 1) / bk), nb.sms);
+    if ((int64_t)gemm_tiles(gg) * gg.splits * GB_M * GB_N > nb.ws_cap) gg.splits = 1;
+    gg.ws = nb.ws;
+  }
   CUDA_TRY(launch_gemm(gg, st));
   if (mode == 0) {
     const int threads = 256;
@@ -465,6 +576,7 @@ int alloc_norm_bufs(NormBufs& nb, int64_t b, int64_t cc, int blocks, int threads
   nb.ldG = round_up(n, 32);
   nb.G = nb.vec = nb.part = nb.out = nullptr;
   nb.blocks = blocks; nb.threads = threads; nb.smem_cap = smem_cap;
+  nb.ws = nullptr; nb.ws_cap = 0; nb.sms = 148;
   CUDA_TRY(cudaMalloc(&nb.G, (size_t)n * nb.ldG * sizeof(double)));
   CUDA_TRY(cudaMalloc(&nb.vec, (size_t)2 * std::max(b, cc) * sizeof(double)));
   CUDA_TRY(cudaMalloc(&nb.part, (size_t)4 * blocks * sizeof(double)));
@@ -508,7 +620,7 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   CUDA_TRY(launch_gemm(gb, c->stream));
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
   NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
-              c->power_smem_cap};
+              c->power_smem_cap, c->splitws, c->splitws_cap, c->sms};
   rc = enqueue_two_norm(c->Bm, c->ldB, b, cc, rtol, max_iters, nb, c->stream, ev ? ev[1] : nullptr);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(c->hpin, c->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -583,7 +695,7 @@ int ibmi_destroy(ibmi_ctx* c) {
     if (s.ainv) cudaFree(s.ainv);
   }
   c->cs.release();
-  for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal})
+  for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal, c->splitws})
     if (q) cudaFree(q);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -779,6 +891,8 @@ int ibmi_block_update(ibmi_ctx* c, int k) {
   if (rc) return rc;
   if (k < 0 || k >= (int)c->sets.size()) return fail(IBMI_ERR_INVALID, "set index out of range");
   if (!c->sets[k].ready) return fail(IBMI_ERR_STATE, "set not set up");
+  rc = plan_workspace(c);
+  if (rc) return rc;
   rc = enqueue_block_update(c, k);
   if (rc) return rc;
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -790,6 +904,8 @@ int ibmi_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, double* 
   if (rc) return rc;
   if (k < 0 || k >= (int)c->sets.size()) return fail(IBMI_ERR_INVALID, "set index out of range");
   if (max_iters < 1) return fail(IBMI_ERR_INVALID, "max_iters must be >= 1");
+  rc = plan_workspace(c);
+  if (rc) return rc;
   rc = enqueue_error_estimate(c, k, rtol, max_iters);
   if (rc) return rc;
   return read_power(c, err, iters, conv);
@@ -813,6 +929,10 @@ int ibmi_sweep(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters,
   const SetDev& last = c->sets.back();
   rc = ensure_estimate_buffers(c, last.b, c->p - last.b);
   if (rc) return rc;
+  rc = plan_workspace(c);
+  if (rc) return rc;
+  if (c->graph_gen != g_tune_gen) invalidate_graph(c);
+  c->graph_gen = g_tune_gen;
   if (c->graph_tried && (c->graph_rtol != rtol || c->graph_max != max_iters)) invalidate_graph(c);
   if (!c->graph_tried) {
     c->graph_tried = true;
@@ -845,6 +965,8 @@ int ibmi_sweep_timed(ibmi_ctx* c, double rtol, int max_iters, double* err, int* 
   for (auto& s : c->sets)
     if (!s.ready) return fail(IBMI_ERR_STATE, "setup not complete");
   const int K = (int)c->sets.size();
+  rc = plan_workspace(c);
+  if (rc) return rc;
   std::vector<cudaEvent_t> ev(2 * K + 4);
   for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
   float t[6] = {0, 0, 0, 0, 0, 0};
@@ -971,6 +1093,27 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
   if (sigma) *sigma = h[0];
   if (converged) *converged = h[1] != 0.0;
   if (iters) *iters = (int)h[2];
+  return IBMI_OK;
+}
+
+int ibmi_tune(int key, int value) {
+  switch (key) {
+    case 0:
+      if (value < 0 || value > 2) return fail(IBMI_ERR_INVALID, "gemm variant must be 0, 1 or 2");
+      g_variant = value;
+      break;
+    case 1:
+      if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
+      g_split_diag = value;
+      break;
+    case 2:
+      if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
+      g_split_gram = value;
+      break;
+    default:
+      return fail(IBMI_ERR_INVALID, "unknown tuning key");
+  }
+  ++g_tune_gen;
   return IBMI_OK;
 }
 
