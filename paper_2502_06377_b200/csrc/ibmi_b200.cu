@@ -19,7 +19,9 @@
 #include <vector>
 
 #include "../../include/ibmi_b200.h"
+#include <cudaTypedefs.h>
 #include "gemm_nt.cuh"
+#include "gemm_tma.cuh"
 #include "small_kernels.cuh"
 
 using namespace ibmi;
@@ -57,6 +59,11 @@ struct GemmOp {
   double* partial = nullptr;     // non-null -> Frobenius epilogue
   int splits = 1;                // split-K factor (needs ws: tiles*splits*128*128 doubles)
   double* ws = nullptr;
+  // TMA eligibility: the caller guarantees that K columns read past a segment
+  // end are finite and meet zeros in the other operand (or fall outside
+  // [0, cols), where TMA zero-fills).  rows/cols: physical extent of X and Y.
+  bool tma_ok = false;
+  int64_t xrows = 0, xcols = 0, yrows = 0, ycols = 0;
   void add_seg(int64_t x0, int64_t y0, int64_t len) {
     if (len > 0) seg[nseg++] = KSeg{x0, y0, (int)len};
   }
@@ -64,10 +71,54 @@ struct GemmOp {
 
 // Tuning knobs (ibmi_tune): GEMM configuration of the hot NT kernels and
 // split-K factors of the small-grid GEMMs.
-int g_variant = 1;          // 0: CfgA (8 warps 64x32), 1: CfgB (16 warps 32x32), 2: CfgC (BK 32)
+int g_variant = 0;          // 0: CfgA (8 warps 64x32), 1: CfgB (16 warps 32x32), 2: CfgC (BK 32)
 int g_split_diag = 0;       // split-K of the Σ_II GEMM (0 = auto)
 int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
+int g_use_tma = 1;          // TMA/mbarrier kernel for eligible hot GEMMs
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+bool g_encode_tried = false;
+
+bool tma_encoder() {
+  if (!g_encode_tried) {
+    g_encode_tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cudaGetLastError();
+  }
+  return g_encode != nullptr;
+}
+
+bool encode_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int EPI>
+cudaError_t launch_tma_inst(const GemmParams& P, const TmaMaps& maps, int grid, cudaStream_t s) {
+  static bool attr_done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!attr_done[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)TMA_SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done[dev] = true;
+  }
+  gemm_tma_kernel<EPI><<<grid, 256, TMA_SMEM, s>>>(P, maps);
+  return cudaGetLastError();
+}
 
 template <class CF, bool XT, bool YT, bool V16, int EPI>
 cudaError_t ensure_attr() {
@@ -107,6 +158,12 @@ cudaError_t prepare_gemm_attributes() {
   PREP(CfgA, true, false, true, EPI_STORE) PREP(CfgA, true, false, false, EPI_STORE)
 #undef PREP_NN
 #undef PREP
+  for (int e : {EPI_STORE, EPI_FROB, EPI_PARTIAL}) {
+    const void* f = e == EPI_STORE ? (const void*)gemm_tma_kernel<EPI_STORE>
+                  : e == EPI_FROB ? (const void*)gemm_tma_kernel<EPI_FROB> : (const void*)gemm_tma_kernel<EPI_PARTIAL>;
+    cudaError_t er = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+    if (er != cudaSuccess) return er;
+  }
   return cudaSuccess;
 }
 
@@ -168,6 +225,32 @@ cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
     P.partial = op.partial;
   }
   cudaError_t err;
+  bool use_tma = nn && op.tma_ok && g_use_tma && g_variant != 2 && tma_encoder() && aligned16(op.X) &&
+                 aligned16(op.Y) && (op.ldx * 8) % 16 == 0 && (op.ldy * 8) % 16 == 0;
+  auto gap_ok = [](const RowMap& m, int64_t rows) { return m.split >= rows || (m.split % 8) == 0; };
+  use_tma = use_tma && gap_ok(op.xm, op.M) && gap_ok(op.yn, op.N);
+  if (use_tma) {
+    // k-tiles are 16 wide on this path
+    P.kt0 = 0; P.kt_total = 0;
+    for (int i = 0; i < op.nseg; ++i) {
+      const int kt = (op.seg[i].len + 15) / 16;
+      if (i == 0) P.kt0 = kt;
+      P.kt_total += kt;
+    }
+    TmaMaps maps;
+    const bool ok = encode_map(&maps.xb, op.X, op.xrows, op.xcols, op.ldx, 128) &&
+                    encode_map(&maps.xs, op.X, op.xrows, op.xcols, op.ldx, 8) &&
+                    encode_map(&maps.yb, op.Y, op.yrows, op.ycols, op.ldy, 128) &&
+                    encode_map(&maps.ys, op.Y, op.yrows, op.ycols, op.ldy, 8);
+    if (ok) {
+      if (epi == EPI_PARTIAL) err = launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
+      else if (epi == EPI_FROB) err = launch_tma_inst<EPI_FROB>(P, maps, grid, s);
+      else err = launch_tma_inst<EPI_STORE>(P, maps, grid, s);
+      if (err != cudaSuccess || !split) return err;
+      splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P);
+      return cudaGetLastError();
+    }
+  }
   if (nn) {
     if (g_variant == 0) err = v16 ? launch_nn<CfgA, true>(P, grid, epi, s) : launch_nn<CfgA, false>(P, grid, epi, s);
     else if (g_variant == 2) err = v16 ? launch_nn<CfgC, true>(P, grid, epi, s) : launch_nn<CfgC, false>(P, grid, epi, s);
@@ -440,6 +523,7 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k1.add_seg(hi, hi, p - hi);
   k1.C = c->S; k1.ldc = c->ld; k1.cm = contig_map(lo); k1.cn = complement_map(lo, hi);
   k1.alpha = -1.0; k1.mirror = true;
+  k1.tma_ok = true; k1.xrows = b; k1.xcols = p; k1.yrows = p; k1.ycols = p;
   CUDA_TRY(launch_gemm(k1, c->stream));
   if (mid) CUDA_TRY(cudaEventRecord(mid, c->stream));
   // K2: Σ[I, I] = A_II⁻¹ − Σ[I, c] W_cᵀ   (= ainv + M Wᵀ), lower tiles mirrored
@@ -452,6 +536,7 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k2.C = c->S; k2.ldc = c->ld; k2.cm = contig_map(lo); k2.cn = contig_map(lo);
   k2.alpha = -1.0; k2.beta = 1.0; k2.D = s.ainv; k2.ldd = s.ldb;
   k2.lower = true; k2.mirror = true;
+  k2.tma_ok = true; k2.xrows = p; k2.xcols = p; k2.yrows = b; k2.ycols = p;
   int64_t need = 0;
   k2.splits = plan_split(c, k2, g_split_diag, &need);
   if (need > c->splitws_cap) k2.splits = 1;    // workspace is planned by plan_workspace()
@@ -531,6 +616,7 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
     gg.X = Bm; gg.ldx = ldB;
     gg.Y = Bm; gg.ldy = ldB;
     gg.add_seg(0, 0, cc);
+    gg.tma_ok = true; gg.xrows = b; gg.xcols = cc; gg.yrows = b; gg.ycols = cc;
   } else {           // H = Bᵀ B
     gg.X = Bm; gg.ldx = ldB; gg.xt = true;
     gg.Y = Bm; gg.ldy = ldB; gg.yt = true;
@@ -617,6 +703,7 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   gb.M = b; gb.N = cc;
   gb.add_seg(0, 0, p);
   gb.C = c->Bm; gb.ldc = c->ldB;
+  gb.tma_ok = true; gb.xrows = p; gb.xcols = p; gb.yrows = p; gb.ycols = p;
   CUDA_TRY(launch_gemm(gb, c->stream));
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
   NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
@@ -1010,6 +1097,7 @@ int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
   fr.Y = c->S; fr.ldy = c->ld;
   fr.M = p; fr.N = p;
   fr.add_seg(0, 0, p);
+  fr.tma_ok = true; fr.xrows = p; fr.xcols = p; fr.yrows = p; fr.ycols = p;
   const int nparts = gemm_grid(fr);
   int64_t cap = c->frob_cap;
   if (ensure_buf(&c->frob_part, &cap, nparts, &c->bytes)) return IBMI_ERR_OOM;
@@ -1109,6 +1197,9 @@ int ibmi_tune(int key, int value) {
     case 2:
       if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
       g_split_gram = value;
+      break;
+    case 3:
+      g_use_tma = value ? 1 : 0;
       break;
     default:
       return fail(IBMI_ERR_INVALID, "unknown tuning key");
