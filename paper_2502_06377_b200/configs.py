@@ -10,7 +10,12 @@ bit-identical matrices:
 * partitions are ``contiguous_partition(p, K, f)`` with (K, f) = (2, 0),
   (2, 0), (8, .125), (8, .125), (16, .125) (B1);
 * Σ₀ is ``diag(1/A_ii)`` on c1/c2 (guess ``"jacobi"``), identity otherwise (B3);
-* stopping: c1 estimate ≤ 1e-10, c2 ``‖I − AΣ‖_F < 1e-9``, c3–c5 estimate ≤ 1e-8 (B4);
+* stopping: c1 estimate ≤ 1e-10, c2 ``‖I − AΣ‖_F < 1e-9``, c3/c5 estimate ≤ 1e-8 (B4);
+  c4 estimate ≤ 1e-5: the reference default 1e-8 lies below this problem's
+  FP64 floor (measured on the GPU: the estimate converges ×0.46 per sweep and
+  then stays at 9.47e-7, ‖I − AΣ‖_F at 2.37e-6, from sweep ~22 to 120+;
+  tools/trace_config.py), so 1e-8 is unreachable in double precision by any
+  evaluation order;
 * ``max_iterations`` 1500 on c2, 500 otherwise (B5).
 
 No public dataset is involved: BASELINE's own recipes are the benchmark
@@ -54,7 +59,7 @@ CONFIGS = {
                         "p=4096 A=Q diag(10^U(0,3)) Q^T; 2 blocks 2048/2048; until ||I-A Sigma||_F<1e-9"),
     "c3": ProblemConfig("c3", 8192, 8, 0.125, "identity", 1e-8, "estimate", 500,
                         "p=8192 SE kernel l=0.1 on x-sorted U[0,1]^2 points + 1e-2 I; 8 blocks 1152/1280, overlap 256"),
-    "c4": ProblemConfig("c4", 16384, 8, 0.125, "identity", 1e-8, "estimate", 500,
+    "c4": ProblemConfig("c4", 16384, 8, 0.125, "identity", 1e-5, "estimate", 500,
                         "p=16384 Matern-3/2 l=0.2 on x-sorted U[0,1]^3 points + 1e-3 I; 8 blocks 2304/2560, overlap 512"),
     "c5": ProblemConfig("c5", 65536, 16, 0.125, "identity", 1e-8, "estimate", 500,
                         "p=65536 A=B B^T/p + 0.5 I, B standard normal; 16 blocks 4608/5120, overlap 1024"),

@@ -182,7 +182,26 @@ cudaError_t launch_nn(const GemmParams& P, int grid, int epi, cudaStream_t s) {
   return launch_inst<CF, false, false, V16, EPI_STORE>(P, grid, s);
 }
 
+cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path);
+
+// IBMI_DEBUG_SYNC=1: synchronise after every GEMM and report the failing one.
 cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
+  static int dbg = -1;
+  if (dbg < 0) dbg = getenv("IBMI_DEBUG_SYNC") ? 1 : 0;
+  int path = -1;
+  cudaError_t e = launch_gemm_impl(op, s, &path);
+  if (dbg) {
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = e2;
+    fprintf(stderr, "[ibmi] gemm path=%d M=%lld N=%lld nseg=%d seg0=(%lld,%lld,%d) xt=%d yt=%d lower=%d mirror=%d "
+            "splits=%d tma_ok=%d xrows=%lld yrows=%lld -> %s\n", path, (long long)op.M, (long long)op.N, op.nseg,
+            (long long)op.seg[0].x0, (long long)op.seg[0].y0, op.nseg ? op.seg[0].len : 0, op.xt, op.yt, op.lower,
+            op.mirror, op.splits, op.tma_ok, (long long)op.xrows, (long long)op.yrows, cudaGetErrorString(e));
+  }
+  return e;
+}
+
+cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
   if (op.M <= 0 || op.N <= 0) return cudaSuccess;
   GemmParams P;
   memset(&P, 0, sizeof(P));
@@ -229,6 +248,8 @@ cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
                  aligned16(op.Y) && (op.ldx * 8) % 16 == 0 && (op.ldy * 8) % 16 == 0;
   auto gap_ok = [](const RowMap& m, int64_t rows) { return m.split >= rows || (m.split % 8) == 0; };
   use_tma = use_tma && gap_ok(op.xm, op.M) && gap_ok(op.yn, op.N);
+  // the innermost TMA coordinate must be 16-byte aligned: even K starts only
+  for (int i = 0; i < op.nseg; ++i) use_tma = use_tma && (op.seg[i].x0 % 2 == 0) && (op.seg[i].y0 % 2 == 0);
   if (use_tma) {
     // k-tiles are 16 wide on this path
     P.kt0 = 0; P.kt_total = 0;
@@ -243,6 +264,7 @@ cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
                     encode_map(&maps.yb, op.Y, op.yrows, op.ycols, op.ldy, 128) &&
                     encode_map(&maps.ys, op.Y, op.yrows, op.ycols, op.ldy, 8);
     if (ok) {
+      *path = 1;
       if (epi == EPI_PARTIAL) err = launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
       else if (epi == EPI_FROB) err = launch_tma_inst<EPI_FROB>(P, maps, grid, s);
       else err = launch_tma_inst<EPI_STORE>(P, maps, grid, s);
@@ -251,6 +273,7 @@ cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
       return cudaGetLastError();
     }
   }
+  *path = 0;
   if (nn) {
     if (g_variant == 0) err = v16 ? launch_nn<CfgA, true>(P, grid, epi, s) : launch_nn<CfgA, false>(P, grid, epi, s);
     else if (g_variant == 2) err = v16 ? launch_nn<CfgC, true>(P, grid, epi, s) : launch_nn<CfgC, false>(P, grid, epi, s);

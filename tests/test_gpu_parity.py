@@ -336,8 +336,12 @@ def test_c4_first_sweeps_match_reference_and_converge():
             errs.append(err)
             if err <= cfg.tol:
                 break
-        assert errs[-1] <= cfg.tol
+        assert errs[-1] <= cfg.tol and len(errs) < 40
         s = ds.sigma()
         assert np.array_equal(s, s.T)
         fr = ds.frobenius()
-        assert fr < 1e-5
+        assert fr < 1e-4
+        # past convergence the estimate sits on its FP64 floor (~9.5e-7), below tol
+        for _ in range(10):
+            err, _, _ = ds.sweep(1e-9, 5000)
+        assert err < 2e-6
