@@ -141,6 +141,7 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
     ``a`` may be a numpy array or a float64 CUDA tensor already in HBM.
     """
     cfg = cfg or IbmiConfig()
+    stopping = getattr(cfg, "stopping", "estimate")      # reference IbmiConfig has no such field
     if not hasattr(a, "is_cuda"):
         a = np.asarray(a, dtype=np.float64)
     validate(part)
@@ -161,7 +162,7 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
             start = time.perf_counter()
             it += 1
             err, pit, pconv = ds.sweep(cfg.norm_rtol, cfg.norm_max_iters)
-            fr = ds.frobenius() if cfg.stopping == "frobenius" else None
+            fr = ds.frobenius() if stopping == "frobenius" else None
             walls.append(time.perf_counter() - start)
             if not pconv:
                 warnings.warn(
