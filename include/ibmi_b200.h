@@ -135,6 +135,44 @@ int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64
 int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* restart_v, double rtol,
                   int max_iters, double* sigma, int* iters, int* converged, void* stream);
 
+/* ---- composable pieces for the sharded (multi-GPU) sweep ---- */
+
+/* One-gap index map: logical i -> (i < split ? off0 + i : off1 + (i - split)).
+ * A contiguous run starting at o is {INT64_MAX, o, 0}. */
+typedef struct {
+  int64_t split, off0, off1;
+} ibmi_map;
+
+/* General NT GEMM on device pointers (the kernels behind every call above):
+ *   v(m,n) = alpha * sum_k X(xm(m), k) * Y(yn(n), k) + beta * D(dm(m), dn(n))
+ * over up to two K segments [x0, x0+len) (in X) paired with [y0, y0+len) (in Y);
+ *   direct: C[cidx ? cidx[m] : cm(m)][cn(n)] = v;   mirror: C2[c2n(n)][c2m(m)] = v;
+ *   lower: only the lower triangle (M == N);  frob_out != NULL: instead of storing,
+ *   frob_out[0] = sqrt(sum (delta(row(m), cn(n)) - acc)^2), frob_out[1] = the sum.
+ * xrows/xcols/yrows/ycols are the operands' physical extents; tma_safe = 1 promises
+ * that K columns read past a segment end are finite and meet zeros in the other
+ * operand (lets the TMA kernel be used).  `ws` (ws_len doubles, may be NULL) is
+ * scratch for split-K / reduction partials; ibmi_gemm_workspace gives the size. */
+typedef struct {
+  const double* x; int64_t ldx; ibmi_map xm; int64_t xrows, xcols;
+  const double* y; int64_t ldy; ibmi_map yn; int64_t yrows, ycols;
+  int64_t m, n;
+  int nseg; int64_t seg_x0[2], seg_y0[2], seg_len[2];
+  double* c; int64_t ldc; ibmi_map cm, cn; const int64_t* cidx; int direct;
+  double* c2; int64_t ldc2; ibmi_map c2m, c2n; int mirror;
+  double alpha, beta; const double* d; int64_t ldd; ibmi_map dm, dn;
+  int lower, tma_safe, splits;
+  double* frob_out;
+  double* ws; int64_t ws_len;
+} ibmi_gemm_desc;
+
+int ibmi_gemm(const ibmi_gemm_desc* desc, void* stream);
+int ibmi_gemm_workspace(const ibmi_gemm_desc* desc, int64_t* doubles);
+
+/* Device pointer, shape and leading dimension of a context buffer:
+ * which = 0 A, 1 Σ, 2 W_k (b_k × ld, global columns), 3 A_II⁻¹ of set k. */
+int ibmi_export(ibmi_ctx* ctx, int which, int k, double** ptr, int64_t* rows, int64_t* cols, int64_t* ld);
+
 /* Tuning knobs (process-wide; contexts re-capture their sweep graph):
  * key 0: GEMM configuration of the hot NT kernels (0: 8 warps 64x32, BK16;
  *        1: 16 warps 32x32, BK16 [default]; 2: 16 warps 32x32, BK32);

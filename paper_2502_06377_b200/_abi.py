@@ -48,6 +48,10 @@ SIGNATURES = [
     ("ibmi_spd_inverse", C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(_I64), _P]),
     ("ibmi_two_norm", C.c_int, [_I64, _I64, _P, _I64, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), _P]),
+    ("ibmi_gemm", C.c_int, [_P, _P]),
+    ("ibmi_gemm_workspace", C.c_int, [_P, C.POINTER(_I64)]),
+    ("ibmi_export", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(_I64), C.POINTER(_I64),
+                              C.POINTER(_I64)]),
     ("ibmi_tune", C.c_int, [C.c_int, C.c_int]),
     ("ibmi_probe_fp64_peak", C.c_int, [C.c_int, _D]),
 ]
@@ -114,3 +118,36 @@ def dptr(arr) -> int:
 
 def dbl_ptr(arr: np.ndarray):
     return arr.ctypes.data_as(_D)
+
+
+RUN = 2 ** 62   # "no gap" split value of an ibmi_map
+
+
+class Map(C.Structure):
+    """``ibmi_map``: logical i -> i < split ? off0 + i : off1 + (i - split)."""
+    _fields_ = [("split", C.c_int64), ("off0", C.c_int64), ("off1", C.c_int64)]
+
+    @classmethod
+    def run(cls, off=0):
+        return cls(RUN, int(off), 0)
+
+    @classmethod
+    def gap(cls, split, off0, off1):
+        return cls(int(split), int(off0), int(off1))
+
+
+class GemmDesc(C.Structure):
+    """``ibmi_gemm_desc`` (include/ibmi_b200.h)."""
+    _fields_ = [
+        ("x", C.c_void_p), ("ldx", C.c_int64), ("xm", Map), ("xrows", C.c_int64), ("xcols", C.c_int64),
+        ("y", C.c_void_p), ("ldy", C.c_int64), ("yn", Map), ("yrows", C.c_int64), ("ycols", C.c_int64),
+        ("m", C.c_int64), ("n", C.c_int64),
+        ("nseg", C.c_int), ("seg_x0", C.c_int64 * 2), ("seg_y0", C.c_int64 * 2), ("seg_len", C.c_int64 * 2),
+        ("c", C.c_void_p), ("ldc", C.c_int64), ("cm", Map), ("cn", Map), ("cidx", C.c_void_p), ("direct", C.c_int),
+        ("c2", C.c_void_p), ("ldc2", C.c_int64), ("c2m", Map), ("c2n", Map), ("mirror", C.c_int),
+        ("alpha", C.c_double), ("beta", C.c_double), ("d", C.c_void_p), ("ldd", C.c_int64), ("dm", Map),
+        ("dn", Map),
+        ("lower", C.c_int), ("tma_safe", C.c_int), ("splits", C.c_int),
+        ("frob_out", C.c_void_p),
+        ("ws", C.c_void_p), ("ws_len", C.c_int64),
+    ]

@@ -69,7 +69,10 @@ struct GemmParams {
   double* C; int64_t ldc; RowMap cm, cn;
   double alpha, beta;
   const double* D; int64_t ldd; RowMap dm, dn;
-  int mirror;                                // also store C[cn(n)][cm(m)]
+  int mirror;                                // also store C2[c2n(n)][c2m(m)]
+  double* C2; int64_t ldc2; RowMap c2m, c2n;   // mirror target (defaults to C, cm, cn)
+  const int64_t* cidx;                       // optional: direct-store / δ row = cidx[m] instead of cm(m)
+  int direct;                                // write the direct store C[cm(m)][cn(n)] (default 1)
   int lower;                                 // only tiles tm >= tn; in diagonal tiles only m >= n
   int tiles_m, tiles_n;
   double* partial;                           // EPI_FROB: one partial sum per CTA; EPI_PARTIAL: split tiles
@@ -281,8 +284,9 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
     for (int i = 0; i < MI; ++i) {
       const int m = m0 + wm0 + 8 * i + g;
       if (m >= P.M) continue;
-      const int64_t rowc = map_idx(P.cm, m);
+      const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
       const int64_t rowd = P.beta != 0.0 ? map_idx(P.dm, m) : 0;
+      const int64_t mcol2 = map_idx(P.c2m, m);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
 #pragma unroll
@@ -292,9 +296,8 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
           if (diag_tile && m < n) continue;
           double v = P.alpha * acc[i][j][e];
           if (P.beta != 0.0) v += P.beta * P.D[rowd * P.ldd + map_idx(P.dn, n)];
-          const int64_t colc = map_idx(P.cn, n);
-          P.C[rowc * P.ldc + colc] = v;
-          if (P.mirror) P.C[colc * P.ldc + rowc] = v;
+          if (P.direct) P.C[rowc * P.ldc + map_idx(P.cn, n)] = v;
+          if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + mcol2] = v;
         }
       }
     }
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
     for (int i = 0; i < MI; ++i) {
       const int m = m0 + wm0 + 8 * i + g;
       if (m >= P.M) continue;
-      const int64_t rowc = map_idx(P.cm, m);
+      const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
@@ -366,11 +369,10 @@ __global__ void splitk_reduce_kernel(const GemmParams P) {
     double acc = 0.0;
     for (int s = 0; s < P.splits; ++s) acc += src[(size_t)s * GB_M * GB_N + e];
     double v = P.alpha * acc;
-    const int64_t rowc = map_idx(P.cm, m);
+    const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
     if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + map_idx(P.dn, n)];
-    const int64_t colc = map_idx(P.cn, n);
-    P.C[rowc * P.ldc + colc] = v;
-    if (P.mirror) P.C[colc * P.ldc + rowc] = v;
+    if (P.direct) P.C[rowc * P.ldc + map_idx(P.cn, n)] = v;
+    if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + map_idx(P.c2m, m)] = v;
   }
 }
 

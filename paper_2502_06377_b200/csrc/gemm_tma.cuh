@@ -207,8 +207,9 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
     for (int i = 0; i < MI; ++i) {
       const int m = m0 + xrow[i];
       if (m >= P.M) continue;
-      const int64_t rowc = map_idx(P.cm, m);
+      const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
       const int64_t rowd = P.beta != 0.0 ? map_idx(P.dm, m) : 0;
+      const int64_t mcol2 = map_idx(P.c2m, m);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
 #pragma unroll
@@ -218,9 +219,8 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
           if (diag_tile && m < n) continue;
           double v = P.alpha * acc[i][j][e];
           if (P.beta != 0.0) v += P.beta * P.D[rowd * P.ldd + map_idx(P.dn, n)];
-          const int64_t colc = map_idx(P.cn, n);
-          P.C[rowc * P.ldc + colc] = v;
-          if (P.mirror) P.C[colc * P.ldc + rowc] = v;
+          if (P.direct) P.C[rowc * P.ldc + map_idx(P.cn, n)] = v;
+          if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + mcol2] = v;
         }
       }
     }
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
     for (int i = 0; i < MI; ++i) {
       const int m = m0 + xrow[i];
       if (m >= P.M) continue;
-      const int64_t rowc = map_idx(P.cm, m);
+      const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
 #pragma unroll

@@ -56,6 +56,10 @@ struct GemmOp {
   double alpha = 1.0, beta = 0.0;
   const double* D = nullptr; int64_t ldd = 0; RowMap dm = contig_map(0), dn = contig_map(0);
   bool mirror = false, lower = false;
+  double* C2 = nullptr; int64_t ldc2 = 0; RowMap c2m = contig_map(0), c2n = contig_map(0);  // mirror target
+  bool c2_set = false;           // false: mirror into C with (cm, cn)
+  const int64_t* cidx = nullptr; // optional row index array for the direct store / δ
+  bool direct = true;
   double* partial = nullptr;     // non-null -> Frobenius epilogue
   int splits = 1;                // split-K factor (needs ws: tiles*splits*128*128 doubles)
   double* ws = nullptr;
@@ -223,6 +227,10 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
   P.alpha = op.alpha; P.beta = op.beta;
   P.D = op.D ? op.D : op.C; P.ldd = op.D ? op.ldd : op.ldc; P.dm = op.dm; P.dn = op.dn;
   P.mirror = op.mirror; P.lower = op.lower;
+  if (op.c2_set) { P.C2 = op.C2; P.ldc2 = op.ldc2; P.c2m = op.c2m; P.c2n = op.c2n; }
+  else { P.C2 = op.C; P.ldc2 = op.ldc; P.c2m = op.cm; P.c2n = op.cn; }
+  P.cidx = op.cidx;
+  P.direct = op.direct ? 1 : 0;
   P.tiles_m = (P.M + GB_M - 1) / GB_M;
   P.tiles_n = (P.N + GB_N - 1) / GB_N;
   const int tiles = gemm_tiles(op);
@@ -745,12 +753,23 @@ int read_power(ibmi_ctx* c, double* err, int* iters, int* conv) {
   return IBMI_OK;
 }
 
+// Σ is allocated on first use (a sharded rank that only borrows the setup
+// never pays for a p×p Σ).
+int ensure_sigma(ibmi_ctx* c) {
+  if (c->S) return IBMI_OK;
+  const size_t mat = (size_t)c->p * c->ld * sizeof(double);
+  CUDA_TRY(cudaMalloc(&c->S, mat));
+  CUDA_TRY(cudaMemsetAsync(c->S, 0, mat, c->stream));
+  c->bytes += mat;
+  return IBMI_OK;
+}
+
 int check_ready(ibmi_ctx* c) {
   if (!c) return fail(IBMI_ERR_INVALID, "null context");
   if (!c->a_set) return fail(IBMI_ERR_STATE, "matrix not set");
   if (c->sets.empty()) return fail(IBMI_ERR_STATE, "partition not set");
   CUDA_TRY(cudaSetDevice(c->device));
-  return IBMI_OK;
+  return ensure_sigma(c);
 }
 
 }  // namespace
@@ -782,15 +801,14 @@ int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
   power_launch_shape(device, &c->power_blocks, &c->power_threads, &c->power_smem_cap);
   const size_t mat = (size_t)p * c->ld * sizeof(double);
   cudaError_t e1 = cudaMalloc(&c->A, mat);
-  cudaError_t e2 = e1 == cudaSuccess ? cudaMalloc(&c->S, mat) : e1;
-  cudaError_t e3 = e2 == cudaSuccess ? cudaMalloc(&c->dscal, 16 * sizeof(double)) : e2;
+  cudaError_t e3 = e1 == cudaSuccess ? cudaMalloc(&c->dscal, 16 * sizeof(double)) : e1;
   cudaError_t e4 = e3 == cudaSuccess ? cudaMallocHost(&c->hpin, 16 * sizeof(double)) : e3;
   if (e4 != cudaSuccess) {
     ibmi_destroy(c);
     return fail(e4 == cudaErrorMemoryAllocation ? IBMI_ERR_OOM : IBMI_ERR_CUDA,
                 std::string("allocating A/Σ: ") + cudaGetErrorString(e4));
   }
-  c->bytes = 2 * mat + 16 * 8;
+  c->bytes = mat + 16 * 8;
   *out = c;
   return IBMI_OK;
 }
@@ -855,8 +873,11 @@ int ibmi_set_partition(ibmi_ctx* c, int k, const int64_t* lo, const int64_t* hi)
 }
 
 int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_pivot) {
-  int rc = check_ready(c);
-  if (rc) return rc;
+  if (!c) return fail(IBMI_ERR_INVALID, "null context");
+  if (!c->a_set) return fail(IBMI_ERR_STATE, "matrix not set");
+  if (c->sets.empty()) return fail(IBMI_ERR_STATE, "partition not set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = IBMI_OK;
   if (fail_set) *fail_set = -1;
   if (fail_pivot) *fail_pivot = -1;
   const int K = (int)c->sets.size();
@@ -963,6 +984,7 @@ int ibmi_set_sigma(ibmi_ctx* c, const double* s, int64_t lds, int on_device) {
   if (!c || !s) return fail(IBMI_ERR_INVALID, "null argument");
   if (lds < c->p) return fail(IBMI_ERR_DIM, "lds < p");
   CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc = ensure_sigma(c)) return rc;
   CUDA_TRY(cudaMemsetAsync(c->S, 0, (size_t)c->p * c->ld * sizeof(double), c->stream));
   CUDA_TRY(cudaMemcpy2DAsync(c->S, c->ld * 8, s, lds * 8, c->p * 8, c->p,
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
@@ -974,6 +996,7 @@ int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
   if (!c || !out) return fail(IBMI_ERR_INVALID, "null argument");
   if (ldo < c->p) return fail(IBMI_ERR_DIM, "ldo < p");
   CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc = ensure_sigma(c)) return rc;
   CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, c->S, c->ld * 8, c->p * 8, c->p,
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1205,6 +1228,91 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
   if (converged) *converged = h[1] != 0.0;
   if (iters) *iters = (int)h[2];
   return IBMI_OK;
+}
+
+static RowMap to_map(const ibmi_map& m) {
+  RowMap r;
+  r.split = (m.split < 0 || m.split > INT_MAX) ? INT_MAX : (int)m.split;
+  r.off0 = m.off0;
+  r.off1 = m.off1;
+  return r;
+}
+
+static int desc_to_op(const ibmi_gemm_desc* d, GemmOp& op) {
+  if (!d) return fail(IBMI_ERR_INVALID, "null descriptor");
+  if (d->m < 0 || d->n < 0 || d->m > INT_MAX || d->n > INT_MAX) return fail(IBMI_ERR_DIM, "bad m/n");
+  if (d->nseg < 0 || d->nseg > 2) return fail(IBMI_ERR_INVALID, "nseg must be 0, 1 or 2");
+  if (!d->x || !d->y) return fail(IBMI_ERR_INVALID, "null operand");
+  if (!d->frob_out && !d->c && d->direct) return fail(IBMI_ERR_INVALID, "null output");
+  if (d->lower && d->m != d->n) return fail(IBMI_ERR_DIM, "lower requires m == n");
+  op.X = d->x; op.ldx = d->ldx; op.xm = to_map(d->xm);
+  op.Y = d->y; op.ldy = d->ldy; op.yn = to_map(d->yn);
+  op.M = d->m; op.N = d->n;
+  for (int i = 0; i < d->nseg; ++i) {
+    if (d->seg_len[i] < 0 || d->seg_len[i] > INT_MAX) return fail(IBMI_ERR_DIM, "bad segment length");
+    op.add_seg(d->seg_x0[i], d->seg_y0[i], d->seg_len[i]);
+  }
+  op.C = d->c; op.ldc = d->ldc; op.cm = to_map(d->cm); op.cn = to_map(d->cn);
+  op.cidx = d->cidx; op.direct = d->direct != 0;
+  if (d->mirror) {
+    op.mirror = true;
+    if (d->c2) { op.c2_set = true; op.C2 = d->c2; op.ldc2 = d->ldc2; op.c2m = to_map(d->c2m); op.c2n = to_map(d->c2n); }
+  }
+  op.alpha = d->alpha; op.beta = d->beta;
+  op.D = d->d; op.ldd = d->ldd; op.dm = to_map(d->dm); op.dn = to_map(d->dn);
+  op.lower = d->lower != 0;
+  op.tma_ok = d->tma_safe != 0;
+  op.xrows = d->xrows; op.xcols = d->xcols; op.yrows = d->yrows; op.ycols = d->ycols;
+  op.splits = d->splits > 1 ? d->splits : 1;
+  return IBMI_OK;
+}
+
+int ibmi_gemm_workspace(const ibmi_gemm_desc* d, int64_t* doubles) {
+  GemmOp op;
+  int rc = desc_to_op(d, op);
+  if (rc) return rc;
+  const int64_t tiles = gemm_tiles(op);
+  int64_t need = 0;
+  if (d->frob_out) need = tiles;
+  else if (op.splits > 1) need = tiles * op.splits * GB_M * GB_N;
+  if (doubles) *doubles = need;
+  return IBMI_OK;
+}
+
+int ibmi_gemm(const ibmi_gemm_desc* d, void* stream) {
+  GemmOp op;
+  int rc = desc_to_op(d, op);
+  if (rc) return rc;
+  int64_t need = 0;
+  ibmi_gemm_workspace(d, &need);
+  if (need > 0 && (!d->ws || d->ws_len < need)) return fail(IBMI_ERR_INVALID, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d->frob_out) {
+    op.partial = d->ws;
+    CUDA_TRY(launch_gemm(op, st));
+    reduce_partials_kernel<<<1, 1024, 0, st>>>(d->ws, (int)need, d->frob_out);
+    CUDA_TRY(cudaGetLastError());
+    return IBMI_OK;
+  }
+  if (op.splits > 1) op.ws = d->ws;
+  CUDA_TRY(launch_gemm(op, st));
+  return IBMI_OK;
+}
+
+int ibmi_export(ibmi_ctx* c, int which, int k, double** ptr, int64_t* rows, int64_t* cols, int64_t* ld) {
+  if (!c || !ptr) return fail(IBMI_ERR_INVALID, "null argument");
+  if (which == 0) { *ptr = c->A; if (rows) *rows = c->p; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK; }
+  if (which == 1) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_sigma(c)) return rc;
+    *ptr = c->S; if (rows) *rows = c->p; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK;
+  }
+  if (k < 0 || k >= (int)c->sets.size()) return fail(IBMI_ERR_INVALID, "set index out of range");
+  const SetDev& s = c->sets[k];
+  if (!s.ready) return fail(IBMI_ERR_STATE, "set not set up");
+  if (which == 2) { *ptr = s.W; if (rows) *rows = s.b; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK; }
+  if (which == 3) { *ptr = s.ainv; if (rows) *rows = s.b; if (cols) *cols = s.b; if (ld) *ld = s.ldb; return IBMI_OK; }
+  return fail(IBMI_ERR_INVALID, "unknown buffer");
 }
 
 int ibmi_tune(int key, int value) {

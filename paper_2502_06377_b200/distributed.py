@@ -1,0 +1,448 @@
+"""Sharded IBMI sweep over several GPUs.
+
+One process per GPU, ``torch.distributed`` for the plumbing (NCCL on GPUs).
+
+Layout.  Σ is stored as block-cyclic **row panels** of ``panel`` rows: global
+row r lives on rank ``(r // panel) % world``.  Because Σ is symmetric these are
+also its column panels.  A, W_k = A_II⁻¹A_Ic and A_II⁻¹ are replicated.  The
+set-up kernels run on every rank: they are a few percent of a solve, cheaper
+than broadcasting W (42 GB at c5).
+
+One block update of set I = [lo, hi) on rank g (the reference's
+``_BlockOp.apply``, solver.py:122-129, split by columns):
+
+1. panel GEMM ``Mbuf = −W·Σ[c ∩ own_g, c]ᵀ`` (b × |c ∩ own_g|).  Its mirrored
+   epilogue writes ``Σ[c ∩ own_g, I] = −Mᵀ`` straight into the local panel;
+2. partial ``top_g = −Mbuf·W[:, c ∩ own_g]ᵀ`` → ``all_reduce`` → every rank
+   holds ``Σ_II = sym(A_II⁻¹ + M Wᵀ)`` and stores its own rows of it;
+3. exchange: the owner of row i ∈ I needs ``Σ[i, c] = −M[i, :]``, whose
+   columns are spread over all ranks → one ``all_to_all`` of b×c doubles.
+
+Error estimate (solver.py:147-155): the owners of I's rows compute their rows
+of ``B = Σ[I,:]·A[:,c]`` locally (A is replicated), ``all_gather`` assembles
+B, and the Gram power iteration runs replicated, giving the same σ on every
+rank.  ‖I − AΣ‖_F: local rows of ``ΣA`` with the fused (δ − x)² epilogue, then
+``all_reduce``.
+
+Compute goes through a backend.  :class:`CudaBackend` (this module) calls
+``libibmi_b200.so``.  The CPU tests inject a torch emulation, which lives in
+``tests/`` and never in the product.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _abi
+from .device import DeviceSolver, restart_vector
+from .partition import Partition, block_permutation, contiguous_ranges
+
+__all__ = ["RowPanels", "GemmSpec", "CudaBackend", "ShardedSolver"]
+
+
+# --------------------------------------------------------------------------- layout
+class RowPanels:
+    """Block-cyclic ownership of the p rows: row r → rank (r // panel) % world."""
+
+    def __init__(self, p: int, world: int, panel: int = 128):
+        self.p, self.world, self.panel = int(p), int(world), int(panel)
+        r = np.arange(self.p, dtype=np.int64)
+        self.owner = (r // self.panel) % self.world
+        self.rows = [np.nonzero(self.owner == h)[0].astype(np.int64) for h in range(self.world)]
+
+    def local_range(self, h: int, lo: int, hi: int) -> tuple[int, int]:
+        """Local index range [a0, a1) of rank h's rows inside [lo, hi)."""
+        rows = self.rows[h]
+        return int(np.searchsorted(rows, lo)), int(np.searchsorted(rows, hi))
+
+
+# --------------------------------------------------------------------------- GEMM spec
+@dataclass
+class GemmSpec:
+    """Backend-neutral description of one NT GEMM (mirrors ``ibmi_gemm_desc``).
+
+    Maps are ``(split, off0, off1)`` triples, or ``int`` for a plain run
+    starting at that offset.  Tensors are 2-D with unit column stride.
+    """
+
+    x: object
+    xm: object
+    y: object
+    yn: object
+    m: int
+    n: int
+    segs: list                       # [(x0, y0, len), ...] (≤ 2)
+    c: object = None
+    cm: object = 0
+    cn: object = 0
+    cidx: object = None              # int64 tensor: direct-store / δ row index of m
+    direct: bool = True
+    c2: object = None
+    c2m: object = 0
+    c2n: object = 0
+    mirror: bool = False
+    alpha: float = 1.0
+    beta: float = 0.0
+    d: object = None
+    dm: object = 0
+    dn: object = 0
+    lower: bool = False
+    tma_safe: bool = False
+    frob: bool = False               # return Σ (δ − acc)² instead of storing
+    xrows: int = 0
+    xcols: int = 0
+    yrows: int = 0
+    ycols: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+def _map3(m):
+    if isinstance(m, (int, np.integer)):
+        return (_abi.RUN, int(m), 0)
+    return tuple(int(v) for v in m)
+
+
+def map_indices(m, n: int) -> np.ndarray:
+    """Materialise a map over logical indices 0..n-1 (used by emulation backends)."""
+    split, off0, off1 = _map3(m)
+    i = np.arange(n, dtype=np.int64)
+    return np.where(i < split, off0 + i, off1 + (i - split))
+
+
+# --------------------------------------------------------------------------- CUDA backend
+class _CudaArray:
+    def __init__(self, ptr, rows, cols, ld):
+        self.__cuda_array_interface__ = {"shape": (int(rows), int(cols)), "typestr": "<f8",
+                                         "data": (int(ptr), False), "strides": (int(ld) * 8, 8), "version": 3}
+
+
+class CudaBackend:
+    """Compute through libibmi_b200.so on the current CUDA device."""
+
+    def __init__(self, device: int):
+        import torch
+
+        self.torch = torch
+        self.device = torch.device(f"cuda:{device}")
+        self.L = _abi.lib()
+        self._ctx = None
+        self._ws = None
+
+    # set-up: the single-GPU context does the per-set Cholesky / inverse / W
+    def setup(self, a, ranges):
+        torch = self.torch
+        self._ctx = DeviceSolver(a, ranges, device=self.device.index,
+                                 stream=torch.cuda.current_stream(self.device).cuda_stream)
+        self._ctx.setup()
+        h = self._ctx._h
+
+        def view(which, k=0):
+            ptr, r, c, ld = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+            _abi.check(self.L.ibmi_export(h, which, k, C.byref(ptr), C.byref(r), C.byref(c), C.byref(ld)), "export")
+            return torch.as_tensor(_CudaArray(ptr.value, r.value, c.value, ld.value), device=self.device)
+
+        A = view(0)
+        W = [view(2, k) for k in range(len(ranges))]
+        ainv = [view(3, k) for k in range(len(ranges))]
+        return A, W, ainv
+
+    def zeros(self, *shape):
+        return self.torch.zeros(shape, dtype=self.torch.float64, device=self.device)
+
+    def index_tensor(self, idx):
+        return self.torch.as_tensor(np.asarray(idx, dtype=np.int64), device=self.device)
+
+    def gemm(self, s: GemmSpec):
+        torch = self.torch
+        d = _abi.GemmDesc()
+        d.x, d.ldx, d.xm = s.x.data_ptr(), s.x.stride(0), _abi.Map(*_map3(s.xm))
+        d.xrows, d.xcols = s.xrows or s.x.shape[0], s.xcols or s.x.shape[1]
+        d.y, d.ldy, d.yn = s.y.data_ptr(), s.y.stride(0), _abi.Map(*_map3(s.yn))
+        d.yrows, d.ycols = s.yrows or s.y.shape[0], s.ycols or s.y.shape[1]
+        d.m, d.n = int(s.m), int(s.n)
+        segs = [g for g in s.segs if g[2] > 0]
+        d.nseg = len(segs)
+        for i, (x0, y0, ln) in enumerate(segs):
+            d.seg_x0[i], d.seg_y0[i], d.seg_len[i] = int(x0), int(y0), int(ln)
+        if s.c is not None:
+            d.c, d.ldc = s.c.data_ptr(), s.c.stride(0)
+        d.cm, d.cn = _abi.Map(*_map3(s.cm)), _abi.Map(*_map3(s.cn))
+        d.cidx = s.cidx.data_ptr() if s.cidx is not None else None
+        d.direct = int(bool(s.direct) and not s.frob)
+        if s.mirror:
+            d.mirror = 1
+            if s.c2 is not None:
+                d.c2, d.ldc2 = s.c2.data_ptr(), s.c2.stride(0)
+                d.c2m, d.c2n = _abi.Map(*_map3(s.c2m)), _abi.Map(*_map3(s.c2n))
+        d.alpha, d.beta = float(s.alpha), float(s.beta)
+        if s.d is not None:
+            d.d, d.ldd = s.d.data_ptr(), s.d.stride(0)
+            d.dm, d.dn = _abi.Map(*_map3(s.dm)), _abi.Map(*_map3(s.dn))
+        d.lower, d.tma_safe, d.splits = int(s.lower), int(s.tma_safe), 1
+        out = None
+        if s.frob:
+            out = torch.zeros(2, dtype=torch.float64, device=self.device)
+            d.frob_out = out.data_ptr()
+        need = C.c_int64()
+        _abi.check(self.L.ibmi_gemm_workspace(C.byref(d), C.byref(need)), "gemm_workspace")
+        if need.value:
+            if self._ws is None or self._ws.numel() < need.value:
+                self._ws = torch.empty(need.value, dtype=torch.float64, device=self.device)
+            d.ws, d.ws_len = self._ws.data_ptr(), self._ws.numel()
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _abi.check(self.L.ibmi_gemm(C.byref(d), stream), "gemm")
+        return out[1] if s.frob else None
+
+    def two_norm(self, b, rtol, max_iters):
+        torch = self.torch
+        v = restart_vector(b.shape[1])
+        sig, it, cv = C.c_double(), C.c_int(), C.c_int()
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _abi.check(self.L.ibmi_two_norm(b.shape[0], b.shape[1], C.c_void_p(b.data_ptr()), b.stride(0),
+                                        _abi.dbl_ptr(v), float(rtol), int(max_iters), C.byref(sig), C.byref(it),
+                                        C.byref(cv), stream), "two_norm")
+        return sig.value, it.value, bool(cv.value)
+
+    def close(self):
+        if self._ctx is not None:
+            self._ctx.close()
+            self._ctx = None
+
+
+# --------------------------------------------------------------------------- collectives
+class _Comm:
+    """torch.distributed calls, staging CUDA tensors through the host when the
+    process group cannot take them (gloo)."""
+
+    def __init__(self, group):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.backend = dist.get_backend(group)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _stage(self, t):
+        return self.backend == "gloo" and t.is_cuda
+
+    def all_reduce(self, t):
+        if self.world == 1:
+            return t
+        if self._stage(t):
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def all_to_all(self, out, inp, out_splits, in_splits):
+        if self.world == 1:
+            out.copy_(inp)
+            return out
+        if self._stage(inp):
+            ho = out.cpu()
+            self.dist.all_to_all_single(ho, inp.cpu(), out_splits, in_splits, group=self.group)
+            out.copy_(ho)
+        else:
+            self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+        return out
+
+    def all_gather_rows(self, t, counts):
+        """Concatenate every rank's rows (rank order); counts[h] = rows of rank h."""
+        torch = self.torch
+        if self.world == 1:
+            return t
+        mx = max(counts)
+        pad = torch.zeros((mx, t.shape[1]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        stage = self._stage(pad)
+        src = pad.cpu() if stage else pad
+        outs = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(outs, src, group=self.group)
+        out = torch.cat([o[:c] for o, c in zip(outs, counts)], dim=0)
+        return out.to(t.device) if stage else out
+
+
+# --------------------------------------------------------------------------- solver
+class ShardedSolver:
+    """IBMI state sharded by block-cyclic row panels over a process group.
+
+    Every rank passes the same ``a`` (host array or its own device copy) and
+    partition.  Set ranges must be contiguous runs; pairwise-disjoint
+    non-contiguous sets are relabelled first, as on one GPU.
+    """
+
+    def __init__(self, a, partition: Partition | None = None, ranges=None, *, group=None, panel: int = 128,
+                 backend=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch = torch
+        group = group or dist.group.WORLD
+        self.comm = _Comm(group)
+        self.rank, self.world = self.comm.rank, self.comm.world
+        self.perm = None
+        if partition is not None:
+            ranges = contiguous_ranges(partition)
+            if ranges is None:
+                bp = block_permutation(partition)
+                if bp is None:
+                    raise NotImplementedError("overlapping non-contiguous partitions are not supported")
+                self.perm, ranges = bp
+                a = np.asarray(a, dtype=np.float64)[np.ix_(self.perm, self.perm)]
+        self.ranges = [(int(lo), int(hi)) for lo, hi in ranges]
+        self.p = int(a.shape[0])
+        if backend is None:
+            backend = CudaBackend(device if device is not None else torch.cuda.current_device())
+        self.be = backend
+        self.layout = RowPanels(self.p, self.world, panel)
+        lay, g = self.layout, self.rank
+        self.own = lay.rows[g]
+        self.n_loc = len(self.own)
+        self.A, self.W, self.ainv = backend.setup(a, self.ranges)
+        self.ld = self.A.stride(0)
+        self.S = backend.zeros(max(self.n_loc, 1), self.ld)
+        self.own_t = backend.index_tensor(self.own)
+        self.plan = [self._plan_set(lo, hi) for (lo, hi) in self.ranges]
+
+    # ------------------------------------------------------------ per-set plan
+    def _plan_set(self, lo, hi):
+        lay, g, be = self.layout, self.rank, self.be
+        b, p = hi - lo, self.p
+        a0, a1 = lay.local_range(g, lo, hi)
+        n_cl = self.n_loc - (a1 - a0)
+        ranges_all = [lay.local_range(h, lo, hi) for h in range(self.world)]
+        rows_I = [lay.rows[h][r0:r1] for h, (r0, r1) in enumerate(ranges_all)]     # global rows of I per rank
+        n_I = [len(r) for r in rows_I]
+        send_perm = np.concatenate(rows_I) - lo if b else np.zeros(0, np.int64)   # M rows in destination order
+        n_cl_all = [len(lay.rows[h]) - n_I[h] for h in range(self.world)]
+        cols_c = []
+        for h in range(self.world):
+            r0, r1 = ranges_all[h]
+            rr = lay.rows[h]
+            cols_c.append(be.index_tensor(np.concatenate([rr[:r0], rr[r1:]])))
+        return dict(lo=lo, hi=hi, b=b, a0=a0, a1=a1, n_cl=n_cl, n_I=n_I, n_cl_all=n_cl_all,
+                    send_perm=be.index_tensor(send_perm),
+                    my_rows_rel=be.index_tensor(rows_I[g] - lo), cols_c=cols_c, rows_I=rows_I)
+
+    def _w_loc(self, k):
+        """W_k restricted to this rank's columns, compact (zeros stay on I)."""
+        cache = self.__dict__.setdefault("_wloc", {})
+        if k not in cache:
+            cache[k] = self.W[k].index_select(1, self.own_t).contiguous()
+        return cache[k]
+
+    # ------------------------------------------------------------ Σ₀
+    def init_sigma(self, guess: str = "identity"):
+        """Σ = I, Σ[c₁,c₁] = identity or diag(1/A_ii) (solver.py:244-251 + BASELINE jacobi)."""
+        torch = self.torch
+        self.S.zero_()
+        if self.n_loc == 0:
+            return
+        loc = torch.arange(self.n_loc, device=self.S.device)
+        vals = torch.ones(self.n_loc, dtype=torch.float64, device=self.S.device)
+        if guess == "jacobi":
+            lo, hi = self.ranges[0]
+            diag = self.A[self.own_t, self.own_t]
+            inc = (self.own_t < lo) | (self.own_t >= hi)
+            vals = torch.where(inc, 1.0 / diag, vals)
+        elif guess != "identity":
+            raise NotImplementedError(f"guess {guess!r} on the sharded path")
+        self.S[loc, self.own_t] = vals
+
+    # ------------------------------------------------------------ one block update
+    def block_update(self, k: int):
+        torch, be, pl = self.torch, self.be, self.plan[k]
+        lo, hi, b, a0, a1, n_cl = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"], pl["n_cl"]
+        p = self.p
+        segs = [(0, 0, lo), (hi, hi, p - hi)]
+        Mbuf = be.zeros(b, max(n_cl, 1))
+        if n_cl > 0:
+            # 1. Mbuf = −W Σ[c_own, c]ᵀ ; mirror: Σ_loc[c_own row][lo + m] = −M
+            be.gemm(GemmSpec(x=self.W[k], xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl, segs=segs,
+                             c=Mbuf, cm=0, cn=0, mirror=True, c2=self.S, c2m=lo, c2n=(a0, 0, a1),
+                             alpha=-1.0, tma_safe=True, xrows=b, xcols=p, yrows=self.n_loc, ycols=p))
+        # 2. partial top = −Mbuf · W[:, c_own]ᵀ (local columns), all-reduce
+        top = be.zeros(b, b)
+        if n_cl > 0:
+            be.gemm(GemmSpec(x=Mbuf, xm=0, y=self._w_loc(k), yn=0, m=b, n=b,
+                             segs=[(0, 0, a0), (a0, a1, self.n_loc - a1)], c=top, alpha=-1.0,
+                             tma_safe=(a0 % 16 == 0), xrows=b, xcols=n_cl, yrows=b, ycols=self.n_loc))
+        self.comm.all_reduce(top)
+        if a1 > a0:
+            t = self.ainv[k] + top
+            rel = pl["my_rows_rel"]
+            self.S[a0:a1, lo:hi] = 0.5 * (t.index_select(0, rel) + t.t().index_select(0, rel))
+        # 3. exchange: rows of −M for the owners of I
+        if self.world > 1:
+            send = Mbuf[:, :n_cl].index_select(0, pl["send_perm"]).contiguous().reshape(-1)
+            in_splits = [pl["n_I"][h] * n_cl for h in range(self.world)]
+            my_I = pl["n_I"][self.rank]
+            out_splits = [my_I * pl["n_cl_all"][h] for h in range(self.world)]
+            recv = be.zeros(sum(out_splits))
+            self.comm.all_to_all(recv, send, out_splits, in_splits)
+            off = 0
+            rows = self.S[a0:a1]
+            for h in range(self.world):
+                n = out_splits[h]
+                if n:
+                    blk = recv[off:off + n].view(my_I, pl["n_cl_all"][h])
+                    rows.index_copy_(1, pl["cols_c"][h], blk)
+                off += n
+        elif a1 > a0 and n_cl > 0:
+            # single rank: the owner rows are all of I
+            self.S[a0:a1].index_copy_(1, pl["cols_c"][0], Mbuf[:, :n_cl])
+
+    # ------------------------------------------------------------ estimate
+    def error_estimate(self, k: int, rtol: float = 1e-9, max_iters: int = 5000):
+        """‖Σ_II A_Ic + Σ_Ic A_cc‖₂ (solver.py:147-155), same value on every rank."""
+        torch, be, pl = self.torch, self.be, self.plan[k]
+        lo, hi, b, a0, a1 = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"]
+        p, c = self.p, self.p - b
+        Bloc = be.zeros(max(a1 - a0, 1), c)[: a1 - a0]
+        if a1 > a0:
+            be.gemm(GemmSpec(x=self.S, xm=a0, y=self.A, yn=(lo, 0, hi), m=a1 - a0, n=c, segs=[(0, 0, p)],
+                             c=Bloc, tma_safe=True, xrows=self.n_loc, xcols=p, yrows=p, ycols=p))
+        parts = self.comm.all_gather_rows(Bloc, pl["n_I"])
+        order = np.argsort(np.concatenate(pl["rows_I"]), kind="stable")
+        B = parts.index_select(0, be.index_tensor(order)).contiguous()
+        return be.two_norm(B, rtol, max_iters)
+
+    def sweep(self, rtol: float = 1e-9, max_iters: int = 5000):
+        for k in range(len(self.ranges)):
+            self.block_update(k)
+        return self.error_estimate(len(self.ranges) - 1, rtol, max_iters)
+
+    # ------------------------------------------------------------ residual / result
+    def frobenius(self) -> float:
+        """‖I − AΣ‖_F = ‖I − ΣA‖_F from local rows of ΣA, then all-reduce."""
+        torch = self.torch
+        part = torch.zeros(1, dtype=torch.float64, device=self.S.device)
+        if self.n_loc:
+            v = self.be.gemm(GemmSpec(x=self.S, xm=0, y=self.A, yn=0, m=self.n_loc, n=self.p,
+                                      segs=[(0, 0, self.p)], cidx=self.own_t, frob=True, tma_safe=True,
+                                      xrows=self.n_loc, xcols=self.p, yrows=self.p, ycols=self.p))
+            part[0] = v
+        self.comm.all_reduce(part)
+        return float(torch.sqrt(part)[0])
+
+    def gather_sigma(self):
+        """Full Σ (host numpy) on every rank, original index order."""
+        torch = self.torch
+        counts = [len(r) for r in self.layout.rows]
+        allrows = self.comm.all_gather_rows(self.S[: self.n_loc, : self.p], counts)
+        order = np.concatenate(self.layout.rows)
+        full = np.empty((self.p, self.p))
+        full[order] = allrows.cpu().numpy()
+        if self.perm is not None:
+            inv = np.argsort(self.perm)
+            full = full[np.ix_(inv, inv)]
+        return full
+
+    def close(self):
+        self.be.close()

@@ -1,0 +1,81 @@
+"""Sharded sweep (paper_2502_06377_b200.distributed) on CPU with gloo.
+
+world_size 2 and 3, block-cyclic panels of 8 rows, the torch CPU emulation of
+the GEMM backend (tests/torch_backend.py).  Every rank must end with the
+oracle's Σ (relative Frobenius ≤ 1e-12), error trace and ‖I − AΣ‖_F.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, case, out):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from torch_backend import TorchCPUBackend
+
+        from paper_2502_06377_b200 import contiguous_partition, red_black_partition
+        from paper_2502_06377_b200.distributed import ShardedSolver
+
+        p, k, f, sweeps, guess = case
+        m = np.random.default_rng(p + k).standard_normal((p, p))
+        a = m.T @ m + p * np.eye(p)
+        part = red_black_partition(p) if k == 0 else contiguous_partition(p, k, f)
+        ss = ShardedSolver(a, part, panel=8, backend=TorchCPUBackend())
+        ss.init_sigma(guess)
+        errs = [ss.sweep()[0] for _ in range(sweeps)]
+        sig = ss.gather_sigma()
+        fr = ss.frobenius()
+        out.put((rank, errs, sig, fr))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", [(96, 3, 0.1, 4, "identity"), (80, 2, 0.0, 3, "jacobi"), (64, 0, 0.0, 3, "identity"),
+                                  (100, 4, 0.2, 3, "identity")])
+def test_sharded_matches_oracle(world, case):
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import contiguous_partition, red_black_partition
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p, k, f, sweeps, guess = case
+    m = np.random.default_rng(p + k).standard_normal((p, p))
+    a = m.T @ m + p * np.eye(p)
+    part = red_black_partition(p) if k == 0 else contiguous_partition(p, k, f)
+    o = orc.solve(a, part.sets, tol=1e-300, max_iterations=sweeps, guess=guess)
+    for rank, errs, sig, fr in res:
+        assert np.linalg.norm(sig - o["result"]) <= 1e-12 * np.linalg.norm(o["result"]), rank
+        np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-14)
+        assert abs(fr - orc.frobenius_residual(a, o["result"])) <= 1e-9 * max(1.0, fr)

@@ -1,0 +1,73 @@
+"""CPU emulation of the sharded solver's compute backend — TEST DOUBLE ONLY.
+
+Implements the GemmSpec semantics of paper_2502_06377_b200.distributed (and
+include/ibmi_b200.h::ibmi_gemm) with torch CPU float64 ops, so the
+multi-process exchange logic can be exercised with the gloo backend on hosts
+without a GPU.  The product never imports this module.
+"""
+
+import numpy as np
+import torch
+
+from oracle import ibmi_oracle as orc
+from paper_2502_06377_b200.distributed import GemmSpec, map_indices
+
+
+class TorchCPUBackend:
+    def __init__(self):
+        self.device = torch.device("cpu")
+
+    def setup(self, a, ranges):
+        a = np.asarray(a, dtype=np.float64)
+        p = a.shape[0]
+        A = torch.as_tensor(a.copy())
+        W, ainv = [], []
+        for lo, hi in ranges:
+            inv = orc.spd_inverse(a[lo:hi, lo:hi])
+            w = inv @ a[lo:hi, :]
+            w[:, lo:hi] = 0.0
+            W.append(torch.as_tensor(w))
+            ainv.append(torch.as_tensor(inv))
+        return A, W, ainv
+
+    def zeros(self, *shape):
+        return torch.zeros(shape, dtype=torch.float64)
+
+    def index_tensor(self, idx):
+        return torch.as_tensor(np.asarray(idx, dtype=np.int64))
+
+    def gemm(self, s: GemmSpec):
+        rx = torch.as_tensor(map_indices(s.xm, s.m))
+        ry = torch.as_tensor(map_indices(s.yn, s.n))
+        acc = torch.zeros((s.m, s.n), dtype=torch.float64)
+        for x0, y0, ln in s.segs:
+            if ln > 0:
+                acc += s.x[rx, x0:x0 + ln] @ s.y[ry, y0:y0 + ln].T
+        crow = s.cidx if s.cidx is not None else torch.as_tensor(map_indices(s.cm, s.m))
+        ccol = torch.as_tensor(map_indices(s.cn, s.n))
+        if s.frob:
+            delta = (crow[:, None] == ccol[None, :]).to(torch.float64)
+            return ((delta - acc) ** 2).sum()
+        v = s.alpha * acc
+        if s.beta != 0.0:
+            v = v + s.beta * s.d[torch.as_tensor(map_indices(s.dm, s.m))][:, torch.as_tensor(map_indices(s.dn, s.n))]
+        keep = torch.ones_like(v, dtype=torch.bool)
+        if s.lower:
+            keep = torch.tril(keep)
+        if s.direct:
+            mi, ni = torch.nonzero(keep, as_tuple=True)
+            s.c[crow[mi], ccol[ni]] = v[mi, ni]
+        if s.mirror:
+            c2 = s.c2 if s.c2 is not None else s.c
+            c2m = torch.as_tensor(map_indices(s.c2m if s.c2 is not None else s.cm, s.m))
+            c2n = torch.as_tensor(map_indices(s.c2n if s.c2 is not None else s.cn, s.n))
+            mi, ni = torch.nonzero(keep, as_tuple=True)
+            c2[c2n[ni], c2m[mi]] = v[mi, ni]
+        return None
+
+    def two_norm(self, b, rtol, max_iters):
+        s, conv, it = orc.power_sigma_max(b.numpy(), rtol, max_iters)
+        return s, it, conv
+
+    def close(self):
+        pass
