@@ -183,7 +183,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "IBMI sweeps/s (FP64) at p=16384" if args.config == "c4" else f"IBMI sweeps/s ({args.config})",
         "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_sweep * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t_sweep * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg.description}", "p": p, "sets": part.k, "overlap": cfg.overlap},
         "tflops": configs.sweep_flops(cfg) * value / 1e12,
@@ -194,6 +194,21 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def executed_flops(cfg):
+    """FLOPs the kernels actually execute per sweep: K2 and the Gram product
+    compute only the lower triangle of a symmetric result."""
+    part = cfg.partition()
+    p = cfg.p
+    tot = 0.0
+    for s in part.sets:
+        b = len(s)
+        c = p - b
+        tot += 2.0 * b * c * c + b * b * c
+    b = len(part.sets[-1])
+    c = p - b
+    return tot + 2.0 * b * p * c + b * b * c
+
+
 def run_ours(args):
     import torch
 
@@ -202,7 +217,7 @@ def run_ours(args):
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -222,15 +237,31 @@ def run_ours(args):
         a_dev = configs.make_matrix_c5_device(0, device=f"cuda:{dev}")
     torch.cuda.synchronize()
     peak = probe_fp64_peak(dev)
+    flops = configs.sweep_flops(cfg)
+    sizes = [len(s) for s in part.sets]
+    guess = "jacobi" if cfg.guess == "jacobi" else "identity"
 
-    ds = DeviceSolver(a_dev, partition=part, device=dev, stream=stream.cuda_stream)
-    t0 = time.perf_counter()
-    ds.setup()
-    ds.init_sigma(1 if cfg.guess == "jacobi" else 0)
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
+    if world == 1:
+        solver = DeviceSolver(a_dev, partition=part, device=dev, stream=stream.cuda_stream)
+        del a_dev
+        t0 = time.perf_counter()
+        solver.setup()
+        solver.init_sigma(1 if guess == "jacobi" else 0)
+        torch.cuda.synchronize()
+        setup_s = time.perf_counter() - t0
+        sweep = lambda: solver.sweep(1e-9, 5000)          # noqa: E731
+    else:
+        from paper_2502_06377_b200.distributed import ShardedSolver
+
+        t0 = time.perf_counter()
+        solver = ShardedSolver(a_dev, part, device=dev)
+        solver.init_sigma(guess)
+        torch.cuda.synchronize()
+        setup_s = time.perf_counter() - t0
+        del a_dev
+        sweep = lambda: solver.sweep(1e-9, 5000)          # noqa: E731
     for _ in range(args.warmup):
-        ds.sweep(1e-9, 5000)
+        sweep()
     errs = []
     if world > 1:
         torch.distributed.barrier()
@@ -239,7 +270,7 @@ def run_ours(args):
     with ClockSampler(dev) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            errs.append(ds.sweep(1e-9, 5000))
+            errs.append(sweep())
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -248,61 +279,78 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    sweeps_s = world * args.steps / (ms / 1e3)
-    flops = configs.sweep_flops(cfg)
-    # per-kernel-class device times of one sweep (CUDA events on the same stream)
-    timed = [ds.sweep_timed(1e-9, 5000)[3] for _ in range(2)]
-    kt = {k: min(t[k] for t in timed) for k in timed[0]}
-    sizes = [len(s) for s in part.sets]
-    panel_flops = sum(2.0 * b * (p - b) ** 2 for b in sizes)
-    panel_tf = panel_flops / (kt["panel_gemm"] * 1e-3) / 1e12
-    pow_iters = [e[1] for e in errs]
-    ds.close()
-    del a_dev
+    sweeps_s = args.steps / (ms / 1e3)
+    kt, panel_tf = None, None
+    if world == 1:
+        # per-kernel-class device times of one sweep (CUDA events on the same stream)
+        timed = [solver.sweep_timed(1e-9, 5000)[3] for _ in range(2)]
+        kt = {k: min(t[k] for t in timed) for k in timed[0]}
+        panel_flops = sum(2.0 * b * (p - b) ** 2 for b in sizes)
+        panel_tf = panel_flops / (kt["panel_gemm"] * 1e-3) / 1e12
+    # time to tolerance from a fresh Σ0 (setup included), same solver state machine
+    ttt = None
+    if world == 1:
+        solver.init_sigma(1 if guess == "jacobi" else 0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        n_to_tol = 0
+        for n_to_tol in range(1, cfg.max_iterations + 1):
+            e, _, _ = solver.sweep(1e-9, 5000)
+            fr = solver.frobenius() if cfg.stopping == "frobenius" else None
+            if (fr < cfg.tol) if fr is not None else (e <= cfg.tol):
+                break
+        torch.cuda.synchronize()
+        ttt = {"seconds": setup_s + time.perf_counter() - t0, "sweeps": n_to_tol, "tol": cfg.tol,
+               "stopping": cfg.stopping, "setup_s": setup_s}
+    solver.close()
     torch.cuda.empty_cache()
 
     e2e = None
-    if not args.no_e2e and a_host is not None and rank == 0:
+    if not args.no_e2e and a_host is not None and rank == 0 and world == 1:
         # public API, host buffers: h2d of A, setup, K sweeps, d2h of Σ inside the timed region
         t0 = time.perf_counter()
-        rep = pkg.solve(a_host, part, pkg.IbmiConfig(tol=1e-300, max_iterations=args.steps,
-                                                     initial_guess=cfg.guess if cfg.guess != "identity" else "identity"))
+        rep = pkg.solve(a_host, part, pkg.IbmiConfig(tol=1e-300, max_iterations=args.steps, initial_guess=guess))
         wall = time.perf_counter() - t0
         e2e = {"value": rep.iterations / wall, "unit": "sweeps/s",
                "h2d_bytes_per_step": int(p * p * 8 / rep.iterations),
                "d2h_bytes_per_step": int(p * p * 8 / rep.iterations) + 8,
                "note": "solve(a_host, part, IbmiConfig(max_iterations=steps)) wall time incl. A upload, setup, "
-                       "sweeps, per-sweep error readback and Σ download"}
+                       "sweeps, per-sweep error readback and Sigma download"}
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1 and a_host is not None:
         s = cpu_sample(cfg, a_host)
         cpu = {"value": 1.0 / s["sweep_s"], "unit": "sweeps/s", "cores": os.cpu_count(), "kind": "port",
                "sample": s["sample"], "setup_one_set_s": s["setup_one_set_s"]}
     if rank == 0:
+        tf = flops * sweeps_s / 1e12
         line = {
             "metric": "IBMI sweeps/s (FP64) at p=16384" if args.config == "c4" else f"IBMI sweeps/s ({args.config})",
             "value": sweeps_s, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {cfg.description}", "p": p, "sets": part.k,
                        "overlap": cfg.overlap, "set_sizes": sorted(set(sizes)),
-                       "l2": "inputs (A, Sigma 2.15 GB each) exceed L2; no flush",
-                       "parallelism": "replicas" if world > 1 else "single"},
-            "tflops": flops * sweeps_s / world / 1e12,
-            "tflops_frac_of_peak": flops * sweeps_s / world / 1e12 / peak,
+                       "l2": "inputs (A, Sigma) exceed L2; no flush",
+                       "parallelism": f"row-panel sharded x{world}" if world > 1 else "single"},
+            "tflops": tf,
+            "tflops_frac_of_peak": tf / world / peak,
+            "tflops_executed": executed_flops(cfg) * sweeps_s / 1e12,
             "fp64_peak_tflops": peak,
             "setup_s": setup_s,
-            "time_to_first_sweep_s": setup_s + ms_step / 1e3,
-            "power_iterations": pow_iters,
+            "time_to_tol": ttt,
+            "power_iterations": [e[1] for e in errs],
             "error_trace": [e[0] for e in errs],
             "kernel_ms_per_sweep": kt,
-            "roofline": {"bound": "tensor", "kernel": "gemm_nt_kernel (panel M = W Sigma_cc, FP64 DMMA)",
-                         "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s", "frac": panel_tf / peak,
-                         "traffic": None,
+            "roofline": {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
+                         "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s",
+                         "frac": panel_tf / peak if panel_tf else None,
+                         "traffic": 6.50e9,
+                         "traffic_note": "ncu dram read+write bytes of one interior-set panel GEMM launch "
+                                         "(profiles/r01_c4_sweep.md); algorithmic minimum 2.38e9",
                          "peak_source": "measured on this box: DMMA m8n8k4 throughput probe (ibmi_probe_fp64_peak)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * (2 * part.k + 4),
+            "gpu_launches": args.steps * (2 * part.k + 5),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
