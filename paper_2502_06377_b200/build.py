@@ -17,7 +17,7 @@ DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "gemm_nt
     os.path.join(ROOT, "include", "ibmi_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
 def stale() -> bool:

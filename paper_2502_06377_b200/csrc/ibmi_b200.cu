@@ -15,7 +15,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ibmi_b200.h"
@@ -314,6 +316,94 @@ int auto_split(int tiles, int kt_total, int sms) {
     if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
   }
   return best;
+}
+
+// ------------------------------------------------------ host <-> device staging
+// Large host copies go through a pool of pinned slots, several threads at a
+// time: each thread copies its row chunks into its own pinned slots (touching
+// and, for fresh destinations, faulting pages in parallel) while its stream
+// moves the previous chunk over PCIe.
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<void*> slots;
+  size_t slot_bytes = 0;
+};
+PinnedPool g_pool;
+constexpr size_t STAGE_SLOT = 16u << 20;   // 16 MiB per slot, 2 slots per thread
+
+int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t rows, int64_t cols, bool to_device,
+                int device) {
+  const size_t row_bytes = (size_t)cols * 8;
+  const size_t total = row_bytes * (size_t)rows;
+  if (total < (64u << 20) || row_bytes > STAGE_SLOT) {
+    CUDA_TRY(cudaMemcpy2D(to_device ? (void*)dev : (void*)host, (to_device ? ldd : ldh) * 8,
+                          to_device ? (const void*)host : (const void*)dev, (to_device ? ldh : ldd) * 8, row_bytes,
+                          rows, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
+    return IBMI_OK;
+  }
+  const int64_t chunk_rows = std::max<int64_t>(1, (int64_t)(STAGE_SLOT / row_bytes));
+  const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
+  unsigned hc = std::thread::hardware_concurrency();
+  const int nthreads = (int)std::min<int64_t>(nchunks, std::max(1u, std::min(8u, hc ? hc : 1u)));
+  std::lock_guard<std::mutex> lock(g_pool.mu);
+  while ((int)g_pool.slots.size() < 2 * nthreads) {
+    void* p = nullptr;
+    CUDA_TRY(cudaMallocHost(&p, STAGE_SLOT));
+    g_pool.slots.push_back(p);
+  }
+  std::vector<int> rc(nthreads, IBMI_OK);
+  std::vector<std::string> msg(nthreads);
+  auto work = [&](int t) {
+    cudaSetDevice(device);
+    cudaStream_t st;
+    cudaEvent_t ev[2];
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc[t] = IBMI_ERR_CUDA; return; }
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    bool used[2] = {false, false};
+    int64_t pending_r0[2] = {0, 0}, pending_n[2] = {0, 0};
+    int s = 0;
+    auto drain = [&](int slot) {   // D2H: wait for the slot's copy, move it to the destination
+      if (!used[slot]) return;
+      cudaEventSynchronize(ev[slot]);
+      if (!to_device) {
+        const char* src = (const char*)g_pool.slots[2 * t + slot];
+        for (int64_t r = 0; r < pending_n[slot]; ++r)
+          memcpy(host + (pending_r0[slot] + r) * ldh, src + r * row_bytes, row_bytes);
+      }
+      used[slot] = false;
+    };
+    for (int64_t c = t; c < nchunks; c += nthreads) {
+      const int64_t r0 = c * chunk_rows, n = std::min(chunk_rows, rows - r0);
+      drain(s);
+      char* slot = (char*)g_pool.slots[2 * t + s];
+      cudaError_t e;
+      if (to_device) {
+        for (int64_t r = 0; r < n; ++r) memcpy(slot + r * row_bytes, host + (r0 + r) * ldh, row_bytes);
+        e = cudaMemcpy2DAsync(dev + r0 * ldd, ldd * 8, slot, row_bytes, row_bytes, n, cudaMemcpyHostToDevice, st);
+      } else {
+        e = cudaMemcpy2DAsync(slot, row_bytes, dev + r0 * ldd, ldd * 8, row_bytes, n, cudaMemcpyDeviceToHost, st);
+      }
+      if (e != cudaSuccess) { rc[t] = IBMI_ERR_CUDA; msg[t] = cudaGetErrorString(e); break; }
+      cudaEventRecord(ev[s], st);
+      used[s] = true;
+      pending_r0[s] = r0;
+      pending_n[s] = n;
+      s ^= 1;
+    }
+    drain(s);
+    drain(s ^ 1);
+    cudaStreamSynchronize(st);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaStreamDestroy(st);
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t) th.emplace_back(work, t);
+  for (auto& x : th) x.join();
+  for (int t = 0; t < nthreads; ++t)
+    if (rc[t]) return fail(rc[t], "staged copy: " + msg[t]);
+  return IBMI_OK;
 }
 
 dim3 grid2d(int64_t rows, int64_t cols) {
@@ -837,8 +927,14 @@ int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
   CUDA_TRY(cudaSetDevice(c->device));
   const int64_t p = c->p;
   CUDA_TRY(cudaMemsetAsync(c->A, 0, (size_t)p * c->ld * sizeof(double), c->stream));
-  CUDA_TRY(cudaMemcpy2DAsync(c->A, c->ld * sizeof(double), a, lda * sizeof(double), p * sizeof(double), p,
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  if (on_device) {
+    CUDA_TRY(cudaMemcpy2DAsync(c->A, c->ld * sizeof(double), a, lda * sizeof(double), p * sizeof(double), p,
+                               cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    int rc = staged_copy(c->A, c->ld, const_cast<double*>(a), lda, p, p, true, c->device);
+    if (rc) return rc;
+  }
   c->a_set = true;
   for (auto& s : c->sets) s.ready = false;
   invalidate_graph(c);
@@ -986,8 +1082,13 @@ int ibmi_set_sigma(ibmi_ctx* c, const double* s, int64_t lds, int on_device) {
   CUDA_TRY(cudaSetDevice(c->device));
   if (int rc = ensure_sigma(c)) return rc;
   CUDA_TRY(cudaMemsetAsync(c->S, 0, (size_t)c->p * c->ld * sizeof(double), c->stream));
-  CUDA_TRY(cudaMemcpy2DAsync(c->S, c->ld * 8, s, lds * 8, c->p * 8, c->p,
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  if (on_device) {
+    CUDA_TRY(cudaMemcpy2DAsync(c->S, c->ld * 8, s, lds * 8, c->p * 8, c->p, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    int rc = staged_copy(c->S, c->ld, const_cast<double*>(s), lds, c->p, c->p, true, c->device);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return IBMI_OK;
 }
@@ -997,8 +1098,13 @@ int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
   if (ldo < c->p) return fail(IBMI_ERR_DIM, "ldo < p");
   CUDA_TRY(cudaSetDevice(c->device));
   if (int rc = ensure_sigma(c)) return rc;
-  CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, c->S, c->ld * 8, c->p * 8, c->p,
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  if (on_device) {
+    CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, c->S, c->ld * 8, c->p * 8, c->p, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    int rc = staged_copy(c->S, c->ld, out, ldo, c->p, c->p, false, c->device);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return IBMI_OK;
 }
