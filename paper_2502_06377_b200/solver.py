@@ -15,6 +15,8 @@ Extensions (all optional, defaults reproduce the reference):
 
 from __future__ import annotations
 
+import os
+import sys
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -151,8 +153,12 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
     if cfg.initial_guess not in _GUESS_KIND:
         raise NotImplementedError(f"initial guess {cfg.initial_guess!r} is not available on the B200 path yet")
 
+    prof = os.environ.get("IBMI_PROFILE") is not None
+    t_enter = time.perf_counter()
     with DeviceSolver(a, partition=part, device=device) as ds:
         t0 = time.perf_counter()
+        if prof:
+            print(f"[ibmi] context+upload {t0 - t_enter:.3f}s", file=sys.stderr)
         ds.setup()
         ds.init_sigma(_GUESS_KIND[cfg.initial_guess])
         setup_s = time.perf_counter() - t0
@@ -177,7 +183,13 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
             if (fr < cfg.tol) if fr is not None else (err <= cfg.tol):
                 converged = True
                 break
+        t1 = time.perf_counter()
         result = ds.sigma(on_device=result_on_device)
+        if prof:
+            print(f"[ibmi] setup {setup_s:.3f}s sweeps {sum(walls):.3f}s download {time.perf_counter() - t1:.3f}s",
+                  file=sys.stderr)
+    if prof:
+        print(f"[ibmi] solve total {time.perf_counter() - t_enter:.3f}s", file=sys.stderr)
     return SolveReport(iterations=it, converged=converged, error_trace=errs, wall_times=walls, result=result,
                        power_iterations=pits, residual_trace=resid, setup_seconds=setup_s)
 

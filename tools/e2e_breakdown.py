@@ -37,3 +37,9 @@ for rep in range(2):
 t = time.perf_counter()
 rep = pkg.solve(a, part, pkg.IbmiConfig(tol=1e-300, max_iterations=10))
 print("solve() 10 sweeps:", round(time.perf_counter() - t, 3))
+os.environ["IBMI_PROFILE"] = "1"
+for _ in range(2):
+    t = time.perf_counter()
+    rep = pkg.solve(a, part, pkg.IbmiConfig(tol=1e-300, max_iterations=10))
+    print("solve() 10 sweeps:", round(time.perf_counter() - t, 3), flush=True)
+    del rep
