@@ -70,6 +70,12 @@ int ibmi_set_matrix(ibmi_ctx* ctx, const double* a, int64_t lda, int on_device);
  * validation of partition.py:102-121 stays on the host). */
 int ibmi_set_partition(ibmi_ctx* ctx, int k, const int64_t* lo, const int64_t* hi);
 
+/* General partition: set j is set_idx[set_ptr[j] .. set_ptr[j+1]) (ascending,
+ * any index sets, overlapping or not — reference partition.py:124-141).  Runs
+ * use the contiguous kernels; other sets use device index lists and a K loop
+ * over all p columns (W is exactly zero on I). */
+int ibmi_set_partition_general(ibmi_ctx* ctx, int k, const int64_t* set_ptr, const int64_t* set_idx);
+
 /* Per set: symmetry check of A_II, Cholesky (dpotrf, linalg.py:104), inverse
  * (dpotrs against I + symmetrise, linalg.py:119,130) and W = A_II⁻¹ A_Ic
  * (solver.py:119-120).  On IBMI_ERR_NOT_SPD, *fail_set / *fail_pivot hold the
@@ -137,10 +143,12 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
 
 /* ---- composable pieces for the sharded (multi-GPU) sweep ---- */
 
-/* One-gap index map: logical i -> (i < split ? off0 + i : off1 + (i - split)).
- * A contiguous run starting at o is {INT64_MAX, o, 0}. */
+/* One-gap index map: logical i -> (i < split ? off0 + i : off1 + (i - split)),
+ * or, when idx != NULL, logical i -> idx[i] (device array, rows only on the
+ * cp.async path).  A contiguous run starting at o is {INT64_MAX, o, 0, NULL}. */
 typedef struct {
   int64_t split, off0, off1;
+  const int64_t* idx;
 } ibmi_map;
 
 /* General NT GEMM on device pointers (the kernels behind every call above):

@@ -32,6 +32,7 @@ SIGNATURES = [
     ("ibmi_destroy", C.c_int, [_P]),
     ("ibmi_set_matrix", C.c_int, [_P, _P, _I64, C.c_int]),
     ("ibmi_set_partition", C.c_int, [_P, C.c_int, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("ibmi_set_partition_general", C.c_int, [_P, C.c_int, C.POINTER(_I64), C.POINTER(_I64)]),
     ("ibmi_setup", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(_I64)]),
     ("ibmi_init_sigma", C.c_int, [_P, C.c_int, _P, _I64, C.c_int]),
     ("ibmi_set_sigma", C.c_int, [_P, _P, _I64, C.c_int]),
@@ -125,15 +126,15 @@ RUN = 2 ** 62   # "no gap" split value of an ibmi_map
 
 class Map(C.Structure):
     """``ibmi_map``: logical i -> i < split ? off0 + i : off1 + (i - split)."""
-    _fields_ = [("split", C.c_int64), ("off0", C.c_int64), ("off1", C.c_int64)]
+    _fields_ = [("split", C.c_int64), ("off0", C.c_int64), ("off1", C.c_int64), ("idx", C.c_void_p)]
 
     @classmethod
     def run(cls, off=0):
-        return cls(RUN, int(off), 0)
+        return cls(RUN, int(off), 0, None)
 
     @classmethod
     def gap(cls, split, off0, off1):
-        return cls(int(split), int(off0), int(off1))
+        return cls(int(split), int(off0), int(off1), None)
 
 
 class GemmDesc(C.Structure):

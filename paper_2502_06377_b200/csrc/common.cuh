@@ -11,20 +11,26 @@ namespace ibmi {
 // complement index i maps to i (< lo) or i + (hi - lo) (>= lo).  This is how
 // every kernel addresses Σ[c, c] without gathering it (the reference gathers
 // with np.ix_, linalg.py:186-191).
+// A general (non-contiguous) index set uses an explicit device index list
+// instead (`idx`, sorted ascending), e.g. the sets of a custom overlapping
+// partition (reference partition.py:124-141).
 struct RowMap {
   int split;      // i < split -> off0 + i ; else off1 + (i - split)
   int64_t off0;
   int64_t off1;
+  const int64_t* idx;   // non-null: i -> idx[i]
 };
 
 __host__ __device__ __forceinline__ int64_t map_idx(const RowMap& m, int i) {
+  if (m.idx) return m.idx[i];
   return i < m.split ? m.off0 + i : m.off1 + (int64_t)(i - m.split);
 }
 
-inline RowMap contig_map(int64_t off) { return RowMap{INT_MAX, off, 0}; }
+inline RowMap contig_map(int64_t off) { return RowMap{INT_MAX, off, 0, nullptr}; }
+inline RowMap list_map(const int64_t* idx) { return RowMap{INT_MAX, 0, 0, idx}; }
 // complement of [lo, hi): logical [0, lo) -> [0, lo), [lo, ..) -> [hi, ..)
 inline RowMap complement_map(int64_t lo, int64_t hi) {
-  return RowMap{(int)lo, 0, hi};
+  return RowMap{(int)lo, 0, hi, nullptr};
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {

@@ -257,7 +257,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
   bool use_tma = nn && op.tma_ok && g_use_tma && g_variant != 2 && tma_encoder() && aligned16(op.X) &&
                  aligned16(op.Y) && (op.ldx * 8) % 16 == 0 && (op.ldy * 8) % 16 == 0;
   auto gap_ok = [](const RowMap& m, int64_t rows) { return m.split >= rows || (m.split % 8) == 0; };
-  use_tma = use_tma && gap_ok(op.xm, op.M) && gap_ok(op.yn, op.N);
+  use_tma = use_tma && gap_ok(op.xm, op.M) && gap_ok(op.yn, op.N) && !op.xm.idx && !op.yn.idx;
   // the innermost TMA coordinate must be 16-byte aligned: even K starts only
   for (int i = 0; i < op.nseg; ++i) use_tma = use_tma && (op.seg[i].x0 % 2 == 0) && (op.seg[i].y0 % 2 == 0);
   if (use_tma) {
@@ -542,6 +542,11 @@ int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t
 struct SetDev {
   int64_t lo = 0, hi = 0;
   int b = 0;
+  bool general = false;          // non-contiguous set: index lists below
+  int64_t* idx = nullptr;        // device, b entries (ascending)
+  int64_t* comp = nullptr;       // device, p - b entries (ascending complement)
+  RowMap rows() const { return general ? list_map(idx) : contig_map(lo); }
+  RowMap cmap() const { return general ? list_map(comp) : complement_map(lo, hi); }
   double* W = nullptr;      // b × ld
   double* ainv = nullptr;   // b × ldb
   int64_t ldb = 0;
@@ -600,11 +605,11 @@ void invalidate_graph(ibmi_ctx* c) {
   c->graph_ok = false;
 }
 
-int symcheck(ibmi_ctx* c, int64_t off, int64_t n, const char* what) {
+int symcheck(ibmi_ctx* c, RowMap map, int64_t n, const char* what) {
   unsigned long long* d = reinterpret_cast<unsigned long long*>(c->dscal + 8);
   CUDA_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), c->stream));
   const int nt = (int)((n + 31) / 32);
-  symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, c->stream>>>(c->A, c->ld, off, (int)n, d);
+  symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, c->stream>>>(c->A, c->ld, map, (int)n, d);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(c->hpin + 8, c->dscal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -635,6 +640,33 @@ int plan_split(const ibmi_ctx* c, const GemmOp& op, int forced, int64_t* ws_need
 int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   const SetDev& s = c->sets[k];
   const int64_t p = c->p, lo = s.lo, hi = s.hi, b = s.b, cc = p - b;
+  if (s.general) {
+    // K loop over all p columns: W is exactly zero on I, so the extra b
+    // columns contribute nothing (p/c more flops, no gather of Σ_cc).
+    GemmOp k1;
+    k1.X = s.W; k1.ldx = c->ld;
+    k1.Y = c->S; k1.ldy = c->ld; k1.yn = s.cmap();
+    k1.M = b; k1.N = cc;
+    k1.add_seg(0, 0, p);
+    k1.C = c->S; k1.ldc = c->ld; k1.cm = s.rows(); k1.cn = s.cmap();
+    k1.alpha = -1.0; k1.mirror = true;
+    CUDA_TRY(launch_gemm(k1, c->stream));
+    if (mid) CUDA_TRY(cudaEventRecord(mid, c->stream));
+    GemmOp k2;
+    k2.X = c->S; k2.ldx = c->ld; k2.xm = s.rows();
+    k2.Y = s.W; k2.ldy = c->ld;
+    k2.M = b; k2.N = b;
+    k2.add_seg(0, 0, p);
+    k2.C = c->S; k2.ldc = c->ld; k2.cm = s.rows(); k2.cn = s.rows();
+    k2.alpha = -1.0; k2.beta = 1.0; k2.D = s.ainv; k2.ldd = s.ldb;
+    k2.lower = true; k2.mirror = true;
+    int64_t need = 0;
+    k2.splits = plan_split(c, k2, g_split_diag, &need);
+    if (need > c->splitws_cap) k2.splits = 1;
+    k2.ws = c->splitws;
+    CUDA_TRY(launch_gemm(k2, c->stream));
+    return IBMI_OK;
+  }
   // K1: Σ[I, c] = −W Σ[c, c];  Σ[c, I] = its transpose (mirror store)
   GemmOp k1;
   k1.X = s.W; k1.ldx = c->ld; k1.xm = contig_map(0);
@@ -688,8 +720,12 @@ int plan_workspace(ibmi_ctx* c) {
   for (const SetDev& s : c->sets) {
     GemmOp k2;
     k2.M = s.b; k2.N = s.b; k2.lower = true;
-    k2.add_seg(0, 0, s.lo);
-    k2.add_seg(s.hi, s.hi, c->p - s.hi);
+    if (s.general) {
+      k2.add_seg(0, 0, c->p);
+    } else {
+      k2.add_seg(0, 0, s.lo);
+      k2.add_seg(s.hi, s.hi, c->p - s.hi);
+    }
     int64_t w = 0;
     plan_split(c, k2, g_split_diag, &w);
     need = std::max(need, w);
@@ -810,7 +846,7 @@ void power_launch_shape(int device, int* blocks, int* threads, size_t* smem_cap)
 // ev (optional): [0] after the B GEMM, [1] after the Gram GEMM.
 int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaEvent_t* ev = nullptr) {
   const SetDev& s = c->sets[k];
-  const int64_t p = c->p, lo = s.lo, hi = s.hi, b = s.b, cc = p - b;
+  const int64_t p = c->p, b = s.b, cc = p - b;
   if (cc <= 0) return fail(IBMI_ERR_DIM, "set covers every index: empty complement");
   int rc = ensure_estimate_buffers(c, b, cc);
   if (rc) return rc;
@@ -819,8 +855,8 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   }
   // B[m][n] = Σ_k Σ[I_m][k] A[c_n][k]   (A symmetric: A[k][c_n] = A[c_n][k])
   GemmOp gb;
-  gb.X = c->S; gb.ldx = c->ld; gb.xm = contig_map(lo);
-  gb.Y = c->A; gb.ldy = c->ld; gb.yn = complement_map(lo, hi);
+  gb.X = c->S; gb.ldx = c->ld; gb.xm = s.rows();
+  gb.Y = c->A; gb.ldy = c->ld; gb.yn = s.cmap();
   gb.M = b; gb.N = cc;
   gb.add_seg(0, 0, p);
   gb.C = c->Bm; gb.ldc = c->ldB;
@@ -911,6 +947,8 @@ int ibmi_destroy(ibmi_ctx* c) {
   for (auto& s : c->sets) {
     if (s.W) cudaFree(s.W);
     if (s.ainv) cudaFree(s.ainv);
+    if (s.idx) cudaFree(s.idx);
+    if (s.comp) cudaFree(s.comp);
   }
   c->cs.release();
   for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal, c->splitws})
@@ -938,7 +976,7 @@ int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
   c->a_set = true;
   for (auto& s : c->sets) s.ready = false;
   invalidate_graph(c);
-  int rc = symcheck(c, 0, p, "matrix");
+  int rc = symcheck(c, contig_map(0), p, "matrix");
   if (rc) { c->a_set = false; return rc; }
   return IBMI_OK;
 }
@@ -955,7 +993,9 @@ int ibmi_set_partition(ibmi_ctx* c, int k, const int64_t* lo, const int64_t* hi)
   for (auto& s : c->sets) {
     if (s.W) cudaFree(s.W);
     if (s.ainv) cudaFree(s.ainv);
-    c->bytes -= (size_t)s.b * c->ld * 8 + (size_t)s.b * s.ldb * 8;
+    if (s.idx) cudaFree(s.idx);
+    if (s.comp) cudaFree(s.comp);
+    if (s.W) c->bytes -= (size_t)s.b * c->ld * 8 + (size_t)s.b * s.ldb * 8;
   }
   c->sets.assign(k, SetDev());
   for (int j = 0; j < k; ++j) {
@@ -965,6 +1005,52 @@ int ibmi_set_partition(ibmi_ctx* c, int k, const int64_t* lo, const int64_t* hi)
     c->sets[j].ldb = round_up(c->sets[j].b, 32);
   }
   invalidate_graph(c);
+  return IBMI_OK;
+}
+
+int ibmi_set_partition_general(ibmi_ctx* c, int k, const int64_t* set_ptr, const int64_t* set_idx) {
+  if (!c || !set_ptr || !set_idx) return fail(IBMI_ERR_INVALID, "null argument");
+  if (k < 1) return fail(IBMI_ERR_INVALID, "need at least one set");
+  const int64_t p = c->p;
+  std::vector<int64_t> lo(k), hi(k);
+  std::vector<bool> run(k);
+  for (int j = 0; j < k; ++j) {
+    const int64_t n = set_ptr[j + 1] - set_ptr[j];
+    if (n < 1) return fail(IBMI_ERR_INVALID, "set " + std::to_string(j) + " is empty");
+    const int64_t* s = set_idx + set_ptr[j];
+    bool r = true;
+    for (int64_t i = 0; i < n; ++i) {
+      if (s[i] < 0 || s[i] >= p) return fail(IBMI_ERR_INDEX, "set " + std::to_string(j) + " has indices outside [0, p)");
+      if (i && s[i] <= s[i - 1]) return fail(IBMI_ERR_INVALID, "set " + std::to_string(j) + " must be strictly ascending");
+      if (s[i] != s[0] + i) r = false;
+    }
+    lo[j] = s[0];
+    hi[j] = s[n - 1] + 1;
+    run[j] = r;
+  }
+  int rc = ibmi_set_partition(c, k, lo.data(), hi.data());
+  if (rc) return rc;
+  for (int j = 0; j < k; ++j) {
+    if (run[j]) continue;
+    SetDev& sd = c->sets[j];
+    const int64_t n = set_ptr[j + 1] - set_ptr[j];
+    const int64_t* s = set_idx + set_ptr[j];
+    std::vector<int64_t> comp;
+    comp.reserve(p - n);
+    for (int64_t i = 0, q = 0; i < p; ++i) {
+      if (q < n && s[q] == i) { ++q; continue; }
+      comp.push_back(i);
+    }
+    sd.general = true;
+    sd.b = (int)n;
+    sd.ldb = round_up(n, 32);
+    CUDA_TRY(cudaMalloc(&sd.idx, n * sizeof(int64_t)));
+    CUDA_TRY(cudaMemcpy(sd.idx, s, n * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (!comp.empty()) {
+      CUDA_TRY(cudaMalloc(&sd.comp, comp.size() * sizeof(int64_t)));
+      CUDA_TRY(cudaMemcpy(sd.comp, comp.data(), comp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
+  }
   return IBMI_OK;
 }
 
@@ -983,7 +1069,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   for (int k = first; k < first + count; ++k) {
     SetDev& s = c->sets[k];
     const int64_t b = s.b, lo = s.lo, hi = s.hi, p = c->p;
-    rc = symcheck(c, lo, b, "matrix");
+    rc = symcheck(c, s.rows(), b, "matrix");
     if (rc) { if (fail_set) *fail_set = k; return rc; }
     if (!s.W) {
       CUDA_TRY(cudaMalloc(&s.W, (size_t)b * c->ld * sizeof(double)));
@@ -995,7 +1081,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
     if (rc) return rc;
     c->bytes += c->cs.bytes - before;
     // A_II (lower) -> scratch
-    copy2d_kernel<<<grid2d(b, b), 256, 0, st>>>(c->A, c->ld, contig_map(lo), contig_map(lo), c->cs.ws, c->cs.ldw,
+    copy2d_kernel<<<grid2d(b, b), 256, 0, st>>>(c->A, c->ld, s.rows(), s.rows(), c->cs.ws, c->cs.ldw,
                                                (int)b, (int)b, 1);
     CUDA_TRY(cudaGetLastError());
     int64_t piv = -1;
@@ -1009,6 +1095,30 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
     if (rc) return rc;
     // W = A_II⁻¹ A[I, c]  written at global columns, zero on I
     CUDA_TRY(cudaMemsetAsync(s.W, 0, (size_t)b * c->ld * sizeof(double), st));
+    if (s.general) {
+      // A_I = A[I, :] gathered (b × p), W = ainv · A_I (transposed-Y GEMM), then zero W[:, I]
+      double* ai = nullptr;
+      CUDA_TRY(cudaMalloc(&ai, (size_t)b * c->ld * sizeof(double)));
+      copy2d_kernel<<<grid2d(b, c->ld), 256, 0, st>>>(c->A, c->ld, s.rows(), contig_map(0), ai, c->ld, (int)b,
+                                                     (int)c->ld, 0);
+      GemmOp gw;
+      gw.X = s.ainv; gw.ldx = s.ldb;
+      gw.Y = ai; gw.ldy = c->ld; gw.yt = true;
+      gw.M = b; gw.N = p;
+      gw.add_seg(0, 0, b);
+      gw.C = s.W; gw.ldc = c->ld;
+      cudaError_t e = launch_gemm(gw, st);
+      if (e == cudaSuccess) {
+        zero_cols_kernel<<<dim3((unsigned)((b + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0, st>>>(
+            s.W, c->ld, (int)b, s.rows(), (int)b);
+        e = cudaGetLastError();
+      }
+      cudaStreamSynchronize(st);
+      cudaFree(ai);
+      if (e != cudaSuccess) return fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+      s.ready = true;
+      continue;
+    }
     GemmOp gw;
     gw.X = s.ainv; gw.ldx = s.ldb;
     gw.Y = c->A; gw.ldy = c->ld; gw.yn = complement_map(lo, hi);
@@ -1033,7 +1143,7 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
   fill2d_kernel<<<grid2d(p, c->ld), 256, 0, st>>>(c->S, c->ld, (int)p, (int)c->ld, 0.0, 1.0);
   CUDA_TRY(cudaGetLastError());
   if (c0 == 0) return IBMI_OK;
-  const RowMap cmap = complement_map(s0.lo, s0.hi);
+  const RowMap cmap = s0.cmap();
   if (kind == IBMI_GUESS_IDENTITY) {
   } else if (kind == IBMI_GUESS_JACOBI) {
     jacobi_diag_kernel<<<(int)((c0 + 255) / 256), 256, 0, st>>>(c->A, c->ld, c->S, c->ld, cmap, (int)c0);
@@ -1341,6 +1451,7 @@ static RowMap to_map(const ibmi_map& m) {
   r.split = (m.split < 0 || m.split > INT_MAX) ? INT_MAX : (int)m.split;
   r.off0 = m.off0;
   r.off1 = m.off1;
+  r.idx = m.idx;
   return r;
 }
 

@@ -101,9 +101,9 @@ __global__ void jacobi_diag_kernel(const double* __restrict__ a, int64_t lda, do
   s[g * lds + g] = 1.0 / a[g * lda + g];
 }
 
-// max|a| and max|a - aᵀ| over the n×n block starting at (off, off).
+// max|a| and max|a - aᵀ| over the n×n block A[map(i)][map(j)].
 // Non-negative doubles order like their bit patterns, so atomicMax on u64.
-__global__ void symcheck_kernel(const double* __restrict__ a, int64_t lda, int64_t off, int n,
+__global__ void symcheck_kernel(const double* __restrict__ a, int64_t lda, RowMap map, int n,
                                 unsigned long long* out) {
   __shared__ double tile[32][33];
   const int bi = blockIdx.y, bj = blockIdx.x;
@@ -112,13 +112,13 @@ __global__ void symcheck_kernel(const double* __restrict__ a, int64_t lda, int64
   double mabs = 0.0, mskew = 0.0;
   for (int r = ty; r < 32; r += blockDim.y) {
     const int i = bj * 32 + r, j = bi * 32 + tx;
-    tile[r][tx] = (i < n && j < n) ? a[(off + i) * lda + off + j] : 0.0;
+    tile[r][tx] = (i < n && j < n) ? a[map_idx(map, i) * lda + map_idx(map, j)] : 0.0;
   }
   __syncthreads();
   for (int r = ty; r < 32; r += blockDim.y) {
     const int i = bi * 32 + r, j = bj * 32 + tx;
     if (i < n && j < n) {
-      const double v = a[(off + i) * lda + off + j];
+      const double v = a[map_idx(map, i) * lda + map_idx(map, j)];
       mabs = fmax(mabs, fabs(v));
       mskew = fmax(mskew, fabs(v - tile[tx][r]));
       if (v != v) mskew = __longlong_as_double(0x7ff8000000000000ll);
@@ -130,6 +130,14 @@ __global__ void symcheck_kernel(const double* __restrict__ a, int64_t lda, int64
     atomicMax(out, (unsigned long long)__double_as_longlong(mabs));
     atomicMax(out + 1, (unsigned long long)__double_as_longlong(mskew));
   }
+}
+
+// dst[i][map(j)] = 0 for j < n (zero the I columns of a global-coordinate W)
+__global__ void zero_cols_kernel(double* __restrict__ dst, int64_t ldd, int rows, RowMap cols, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t c = map_idx(cols, j);
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) dst[(int64_t)i * ldd + c] = 0.0;
 }
 
 // y[r] = sum_j B[r][j] * v   (power-iteration start y1 = B·(1/√c)·1, linalg.py:230,235)

@@ -44,19 +44,22 @@ class DeviceSolver:
         self._L = L
         self.device = int(device)
         self.perm = None
+        self.general = None        # list of ascending index arrays (overlapping non-contiguous sets)
         if partition is not None:
             ranges = contiguous_ranges(partition)
             if ranges is None:
                 bp = block_permutation(partition)
-                if bp is None:
-                    raise NotImplementedError(
-                        "overlapping non-contiguous partitions are not supported on the B200 path yet")
-                self.perm, ranges = bp
+                if bp is not None:
+                    self.perm, ranges = bp          # disjoint sets: relabel into runs
+                else:
+                    self.general = [np.unique(np.asarray(s, dtype=np.int64)) for s in partition.sets]
+                    ranges = [(int(s[0]), int(s[-1]) + 1) for s in self.general]
         elif perm is not None:
             self.perm = np.asarray(perm, dtype=np.int64)
         if ranges is None:
             raise ValueError("need ranges or partition")
         self.ranges = [(int(lo), int(hi)) for lo, hi in ranges]
+        self.sizes = [len(s) for s in self.general] if self.general else [hi - lo for lo, hi in self.ranges]
         on_dev = _is_cuda_tensor(a)
         if on_dev:
             import torch
@@ -83,11 +86,18 @@ class DeviceSolver:
         try:
             _abi.check(L.ibmi_set_matrix(h, C.c_void_p(_abi.dptr(a)), lda, int(on_dev)), "set_matrix")
             k = len(self.ranges)
-            lo = (C.c_int64 * k)(*[r[0] for r in self.ranges])
-            hi = (C.c_int64 * k)(*[r[1] for r in self.ranges])
-            _abi.check(L.ibmi_set_partition(h, k, lo, hi), "set_partition")
+            if self.general:
+                ptr = np.zeros(k + 1, dtype=np.int64)
+                ptr[1:] = np.cumsum([len(s) for s in self.general])
+                idx = np.ascontiguousarray(np.concatenate(self.general))
+                _abi.check(L.ibmi_set_partition_general(h, k, ptr.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                        idx.ctypes.data_as(C.POINTER(C.c_int64))), "set_partition")
+            else:
+                lo = (C.c_int64 * k)(*[r[0] for r in self.ranges])
+                hi = (C.c_int64 * k)(*[r[1] for r in self.ranges])
+                _abi.check(L.ibmi_set_partition(h, k, lo, hi), "set_partition")
             self._restart_n = None
-            self._set_restart(self.p - (self.ranges[-1][1] - self.ranges[-1][0]))
+            self._set_restart(self.p - self.sizes[-1])
         except BaseException:
             self.close()
             raise
@@ -132,7 +142,7 @@ class DeviceSolver:
         else:
             _abi.check(self._L.ibmi_init_sigma(self._h, kind, None, 0, 0), "init_sigma")
 
-    def _permute_guess(self, g):
+    def _permute_guess(self, g):  # noqa: D401
         # guess is over the ascending original complement of set 0; the
         # device complement of set 0 is perm[[0,lo) ∪ [hi,p)] in that order.
         lo, hi = self.ranges[0]
@@ -181,16 +191,14 @@ class DeviceSolver:
         _abi.check(self._L.ibmi_block_update(self._h, int(k)), "block_update")
 
     def error_estimate(self, k: int, rtol: float, max_iters: int):
-        lo, hi = self.ranges[k]
-        self._set_restart(self.p - (hi - lo))
+        self._set_restart(self.p - self.sizes[k])
         e, it, cv = C.c_double(), C.c_int(), C.c_int()
         _abi.check(self._L.ibmi_error_estimate(self._h, int(k), float(rtol), int(max_iters), C.byref(e),
                                                C.byref(it), C.byref(cv)), "error_estimate")
         return e.value, it.value, bool(cv.value)
 
     def sweep(self, rtol: float, max_iters: int):
-        lo, hi = self.ranges[-1]
-        self._set_restart(self.p - (hi - lo))
+        self._set_restart(self.p - self.sizes[-1])
         e, it, cv = C.c_double(), C.c_int(), C.c_int()
         _abi.check(self._L.ibmi_sweep(self._h, float(rtol), int(max_iters), C.byref(e), C.byref(it), C.byref(cv)),
                    "sweep")
@@ -198,8 +206,7 @@ class DeviceSolver:
 
     def sweep_timed(self, rtol: float, max_iters: int):
         """Sweep without the graph, returning per-kernel-class device ms."""
-        lo, hi = self.ranges[-1]
-        self._set_restart(self.p - (hi - lo))
+        self._set_restart(self.p - self.sizes[-1])
         e, it, cv = C.c_double(), C.c_int(), C.c_int()
         t = (C.c_float * 6)()
         _abi.check(self._L.ibmi_sweep_timed(self._h, float(rtol), int(max_iters), C.byref(e), C.byref(it),

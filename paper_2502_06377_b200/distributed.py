@@ -105,6 +105,10 @@ def _map3(m):
     return tuple(int(v) for v in m)
 
 
+def _cmap(m):
+    return _abi.Map(*_map3(m), None)
+
+
 def map_indices(m, n: int) -> np.ndarray:
     """Materialise a map over logical indices 0..n-1 (used by emulation backends)."""
     split, off0, off1 = _map3(m)
@@ -158,9 +162,9 @@ class CudaBackend:
     def gemm(self, s: GemmSpec):
         torch = self.torch
         d = _abi.GemmDesc()
-        d.x, d.ldx, d.xm = s.x.data_ptr(), s.x.stride(0), _abi.Map(*_map3(s.xm))
+        d.x, d.ldx, d.xm = s.x.data_ptr(), s.x.stride(0), _cmap(s.xm)
         d.xrows, d.xcols = s.xrows or s.x.shape[0], s.xcols or s.x.shape[1]
-        d.y, d.ldy, d.yn = s.y.data_ptr(), s.y.stride(0), _abi.Map(*_map3(s.yn))
+        d.y, d.ldy, d.yn = s.y.data_ptr(), s.y.stride(0), _cmap(s.yn)
         d.yrows, d.ycols = s.yrows or s.y.shape[0], s.ycols or s.y.shape[1]
         d.m, d.n = int(s.m), int(s.n)
         segs = [g for g in s.segs if g[2] > 0]
@@ -169,18 +173,18 @@ class CudaBackend:
             d.seg_x0[i], d.seg_y0[i], d.seg_len[i] = int(x0), int(y0), int(ln)
         if s.c is not None:
             d.c, d.ldc = s.c.data_ptr(), s.c.stride(0)
-        d.cm, d.cn = _abi.Map(*_map3(s.cm)), _abi.Map(*_map3(s.cn))
+        d.cm, d.cn = _cmap(s.cm), _cmap(s.cn)
         d.cidx = s.cidx.data_ptr() if s.cidx is not None else None
         d.direct = int(bool(s.direct) and not s.frob)
         if s.mirror:
             d.mirror = 1
             if s.c2 is not None:
                 d.c2, d.ldc2 = s.c2.data_ptr(), s.c2.stride(0)
-                d.c2m, d.c2n = _abi.Map(*_map3(s.c2m)), _abi.Map(*_map3(s.c2n))
+                d.c2m, d.c2n = _cmap(s.c2m), _cmap(s.c2n)
         d.alpha, d.beta = float(s.alpha), float(s.beta)
         if s.d is not None:
             d.d, d.ldd = s.d.data_ptr(), s.d.stride(0)
-            d.dm, d.dn = _abi.Map(*_map3(s.dm)), _abi.Map(*_map3(s.dn))
+            d.dm, d.dn = _cmap(s.dm), _cmap(s.dn)
         d.lower, d.tma_safe, d.splits = int(s.lower), int(s.tma_safe), 1
         out = None
         if s.frob:

@@ -345,3 +345,39 @@ def test_c4_first_sweeps_match_reference_and_converge():
         for _ in range(10):
             err, _, _ = ds.sweep(1e-9, 5000)
         assert err < 2e-6
+
+
+def test_solve_overlapping_noncontiguous_matches_oracle():
+    """Custom JSON partition with overlapping, non-contiguous sets (reference
+    partition.py:124-141) runs on the general index-list path."""
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+
+    p = 300
+    a = random_spd(p, 21)
+    rng = np.random.default_rng(4)
+    perm = rng.permutation(p)
+    sets = [np.sort(perm[:140]), np.sort(perm[110:230]), np.sort(perm[200:])]   # overlapping, scattered
+    part = pkg.load_partition_json({"p": p, "sets": [s.tolist() for s in sets]})
+    rep = pkg.solve(a, part, pkg.IbmiConfig(tol=1e-11))
+    o = orc.solve(a, part.sets, tol=1e-11)
+    assert rep.converged
+    assert rel_fro(rep.result, o["result"]) < 1e-10
+    check_trace(rep.error_trace, o["error_trace"], 1e-11)
+
+
+def test_solve_mixed_runs_and_lists_local_guess():
+    """Some sets are runs, some scattered; 'local' initial guess on the GPU."""
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+
+    p = 256
+    a = random_spd(p, 22)
+    s0 = np.arange(0, 100)
+    s1 = np.concatenate([np.arange(90, 180), np.arange(200, 220)])
+    s2 = np.concatenate([np.arange(170, 200), np.arange(210, 256)])
+    part = pkg.load_partition_json({"p": p, "sets": [s0.tolist(), s1.tolist(), s2.tolist()]})
+    rep = pkg.solve(a, part, pkg.IbmiConfig(tol=1e-11, initial_guess="local"))
+    o = orc.solve(a, part.sets, tol=1e-11, guess="local")
+    assert rel_fro(rep.result, o["result"]) < 1e-10
+    check_trace(rep.error_trace, o["error_trace"], 1e-11)
