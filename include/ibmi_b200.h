@@ -44,7 +44,9 @@ typedef enum {
   IBMI_GUESS_IDENTITY = 0,     /* solver.py:158-159                                         */
   IBMI_GUESS_JACOBI = 1,       /* BASELINE c1/c2: Σ0[c1,c1] = diag(1/A_ii) (not in reference) */
   IBMI_GUESS_MATRIX = 2,       /* caller-supplied c1×c1 block (any host-side guess)         */
-  IBMI_GUESS_LOCAL = 3         /* solver.py:162-164: spd_inverse(A[c1,c1]) on the device     */
+  IBMI_GUESS_LOCAL = 3,        /* solver.py:162-164: spd_inverse(A[c1,c1]) on the device     */
+  IBMI_GUESS_MC = 4,           /* solver.py:167-181: guess = p x ldg standard-normal draws      */
+  IBMI_GUESS_TAKAHASHI = 5     /* solver.py:184-212: (A^-1)[c1,c1] = S_c^-1 (needs ibmi_setup)  */
 } ibmi_guess;
 
 typedef struct ibmi_ctx ibmi_ctx;
@@ -134,6 +136,12 @@ int ibmi_dgemm_nt(int64_t m, int64_t n, int64_t k, double alpha, const double* x
  * (linalg.py:122-130).  On IBMI_ERR_NOT_SPD *fail_pivot = elimination step. */
 int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
                      void* stream);
+
+/* Monte Carlo guess block (solver.py:167-181) for any ordering: A (device, p×p),
+ * w (host, p×n standard-normal draws of default_rng(mc_seed)), comp (host, c
+ * ascending indices); out (device, c×c) = (L⁻ᵀw)_c (L⁻ᵀw)_cᵀ / n. */
+int ibmi_mc_guess(int64_t p, const double* a, int64_t lda, const double* w, int64_t n, const int64_t* comp,
+                  int64_t c, double* out, int64_t ldo, void* stream);
 
 /* ‖B‖₂ of a device matrix (rows×cols, ldb) by power iteration with the
  * reference's stopping rule; replaces two_norm (linalg.py:256-274).

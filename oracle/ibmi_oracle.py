@@ -138,7 +138,50 @@ def complement(p: int, idx) -> np.ndarray:
     return np.nonzero(keep)[0].astype(np.intp)
 
 
-def initial_sigma(a, comp0, guess: str = "identity", sigma0=None) -> np.ndarray:
+def guess_monte_carlo(a, comp, n_samples: int = 100, seed: int = 0) -> np.ndarray:
+    """solver.py:167-181 — cov of L⁻ᵀw restricted to comp (dpotrf + dtrsm, same calls)."""
+    a = np.asarray(a, dtype=np.float64)
+    l, info = dpotrf(a, lower=1, clean=1, overwrite_a=0)
+    if info > 0:
+        raise NotPositiveDefinite(info - 1)
+    w = np.random.default_rng(seed).standard_normal((a.shape[0], n_samples))
+    z = sla.solve_triangular(l, w, lower=True, trans="T", check_finite=False)
+    zc = z[np.asarray(comp, dtype=np.intp)]
+    return (zc @ zc.T) / n_samples
+
+
+def guess_takahashi(a, comp) -> np.ndarray:
+    """solver.py:184-212 — unpivoted LDLᵀ of A reordered [rest, comp], then the
+    backward recurrence h[i,j] = δ_ij/d_i − Σ_{k>i} l_ki h_kj over the comp corner."""
+    a = np.asarray(a, dtype=np.float64)
+    comp = np.asarray(comp, dtype=np.intp)
+    p = a.shape[0]
+    keep = np.ones(p, dtype=bool)
+    keep[comp] = False
+    order = np.concatenate([np.nonzero(keep)[0], comp])
+    w = a[np.ix_(order, order)].copy()
+    lower = np.eye(p)
+    d = np.zeros(p)
+    for j in range(p):                       # right-looking unblocked LDLᵀ
+        d[j] = w[j, j]
+        col = w[j + 1:, j] / d[j]
+        lower[j + 1:, j] = col
+        w[j + 1:, j + 1:] -= d[j] * np.outer(col, col)
+    c = comp.size
+    off = p - c
+    h = np.zeros((c, c))
+    for i in range(p - 1, off - 1, -1):
+        ii = i - off
+        lcol = lower[i + 1:, i]
+        row = -(lcol @ h[ii + 1:, ii + 1:])
+        h[ii, ii + 1:] = row
+        h[ii + 1:, ii] = row
+        h[ii, ii] = 1.0 / d[i] - lcol @ row
+    return 0.5 * (h + h.T)
+
+
+def initial_sigma(a, comp0, guess: str = "identity", sigma0=None, mc_samples: int = 100,
+                  mc_seed: int = 0) -> np.ndarray:
     """solver.py:244-251 (identity) plus the BASELINE ``jacobi`` seed."""
     p = a.shape[0]
     sigma = np.eye(p)
@@ -152,6 +195,10 @@ def initial_sigma(a, comp0, guess: str = "identity", sigma0=None) -> np.ndarray:
         g = np.diag(1.0 / np.diag(a)[comp0])
     elif guess == "local":
         g = spd_inverse(a[np.ix_(comp0, comp0)])
+    elif guess == "mc":
+        g = guess_monte_carlo(a, comp0, mc_samples, mc_seed)
+    elif guess == "takahashi":
+        g = guess_takahashi(a, comp0)
     else:
         raise ValueError(f"oracle has no guess {guess!r}")
     if g.shape != (comp0.size, comp0.size):
@@ -162,7 +209,7 @@ def initial_sigma(a, comp0, guess: str = "identity", sigma0=None) -> np.ndarray:
 
 def solve(a, sets, *, tol=1e-8, max_iterations=500, guess="identity", sigma0=None,
           stopping="estimate", norm_rtol=POWER_RTOL, norm_max_iters=POWER_MAX_ITERS,
-          record_frobenius=False, callback=None):
+          record_frobenius=False, callback=None, mc_samples=100, mc_seed=0):
     """solver.py:225-278 with the stopping-rule and Σ₀ extensions.
 
     ``stopping="estimate"``: stop when the reference estimate ≤ tol
@@ -177,7 +224,7 @@ def solve(a, sets, *, tol=1e-8, max_iterations=500, guess="identity", sigma0=Non
     t0 = time.perf_counter()
     ops = [BlockOp(a, s, c) for s, c in zip(sets, comps)]
     setup_s = time.perf_counter() - t0
-    sigma = initial_sigma(a, comps[0], guess, sigma0)
+    sigma = initial_sigma(a, comps[0], guess, sigma0, mc_samples, mc_seed)
     err_trace, walls, pits, frob = [], [], [], []
     converged, it = False, 0
     while it < max_iterations:

@@ -39,6 +39,8 @@ from .solver import (  # noqa: F401
     error_estimate,
     initial_guess_identity,
     initial_guess_local_inverse,
+    initial_guess_monte_carlo,
+    initial_guess_takahashi,
     make_initial_guess,
     solve,
 )

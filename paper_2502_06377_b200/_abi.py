@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libibmi_b200.so")
 
 OK, ERR_INVALID, ERR_DIM, ERR_INDEX, ERR_NOT_SPD, ERR_NOT_SYMMETRIC, ERR_CUDA, ERR_OOM, ERR_STATE, ERR_UNSUPPORTED = range(10)
-GUESS_IDENTITY, GUESS_JACOBI, GUESS_MATRIX, GUESS_LOCAL = range(4)
+GUESS_IDENTITY, GUESS_JACOBI, GUESS_MATRIX, GUESS_LOCAL, GUESS_MC, GUESS_TAKAHASHI = range(6)
 
 # (name, restype, argtypes) — the full exported surface of include/ibmi_b200.h
 _P = C.c_void_p
@@ -47,6 +47,7 @@ SIGNATURES = [
     ("ibmi_device_bytes", C.c_int, [_P, C.POINTER(_I64)]),
     ("ibmi_dgemm_nt", C.c_int, [_I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, C.c_double, _P, _I64, _P]),
     ("ibmi_spd_inverse", C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(_I64), _P]),
+    ("ibmi_mc_guess", C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     ("ibmi_two_norm", C.c_int, [_I64, _I64, _P, _I64, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), _P]),
     ("ibmi_gemm", C.c_int, [_P, _P]),

@@ -492,7 +492,7 @@ int potrf_blocked(CholScratch& cs, int n, cudaStream_t s, int64_t* pivot) {
 // In-place L -> L⁻¹ (LAPACK dtrtri lower, blocked right-to-left), then
 // out = L⁻ᵀ L⁻¹ (lower tiles, mirrored: exactly symmetric, like the
 // reference's 0.5(inv + invᵀ), linalg.py:130).
-int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t s) {
+int trtri_blocked(CholScratch& cs, int n, cudaStream_t s) {
   double* a = cs.ws;
   const int64_t ld = cs.ldw;
   const int nblk = (n + CHOL_NB - 1) / CHOL_NB;
@@ -524,6 +524,14 @@ int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t
                                                  a + (int64_t)j0 * ld + j0, ld, jb, jb, 0);
     CUDA_TRY(cudaGetLastError());
   }
+  return IBMI_OK;
+}
+
+int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t s) {
+  int rc = trtri_blocked(cs, n, s);
+  if (rc) return rc;
+  double* a = cs.ws;
+  const int64_t ld = cs.ldw;
   GemmOp la;   // out[m][n] = Σ_k X[k][m] X[k][n]
   la.X = a; la.ldx = ld; la.xt = true;
   la.Y = a; la.ldy = ld; la.yt = true;
@@ -535,6 +543,51 @@ int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t
   return IBMI_OK;
 }
 
+
+
+// Monte Carlo guess (solver.py:167-181): A = L Lᵀ (blocked Cholesky), Z = L⁻ᵀ w,
+// out[orow(m)][ocol(n)] = (1/n) Σ_s Z[cmap(m)][s] Z[cmap(n)][s] for m, n < c0.
+int mc_guess_into(const double* A, int64_t lda, int64_t p, const double* w_src, int on_device, int64_t n,
+                  RowMap cmap, int64_t c0, double* out, int64_t ldo, RowMap orow, RowMap ocol, cudaStream_t st) {
+  CholScratch cs;
+  int rc = ensure_scratch(cs, (int)p);
+  if (rc) { cs.release(); return rc; }
+  double *w = nullptr, *z = nullptr;
+  cudaError_t e = cudaMalloc(&w, (size_t)p * n * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&z, (size_t)p * n * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(w, w_src, (size_t)p * n * sizeof(double),
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) { cs.release(); cudaFree(w); cudaFree(z); return fail(IBMI_ERR_OOM, cudaGetErrorString(e)); }
+  copy2d_kernel<<<grid2d(p, p), 256, 0, st>>>(A, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)p, (int)p, 1);
+  int64_t piv = -1;
+  rc = potrf_blocked(cs, (int)p, st, &piv);
+  if (!rc) rc = trtri_blocked(cs, (int)p, st);
+  if (!rc) {
+    GemmOp gz;   // Z[i][s] = Σ_k L⁻¹[k][i] w[k][s]   (both operands transposed)
+    gz.X = cs.ws; gz.ldx = cs.ldw; gz.xt = true;
+    gz.Y = w; gz.ldy = n; gz.yt = true;
+    gz.M = p; gz.N = n;
+    gz.add_seg(0, 0, p);
+    gz.C = z; gz.ldc = n;
+    e = launch_gemm(gz, st);
+    GemmOp gg;   // out = Z_c Z_cᵀ / n  (lower tiles, mirrored)
+    gg.X = z; gg.ldx = n; gg.xm = cmap;
+    gg.Y = z; gg.ldy = n; gg.yn = cmap;
+    gg.M = c0; gg.N = c0;
+    gg.add_seg(0, 0, n);
+    gg.C = out; gg.ldc = ldo; gg.cm = orow; gg.cn = ocol;
+    gg.alpha = 1.0 / (double)n;
+    gg.lower = true; gg.mirror = true;
+    if (e == cudaSuccess) e = launch_gemm(gg, st);
+    if (e != cudaSuccess) rc = fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaStreamSynchronize(st);
+  cs.release();
+  cudaFree(w);
+  cudaFree(z);
+  return rc;
+}
 
 }  // namespace
 
@@ -1179,6 +1232,54 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
     cudaFree(inv);
     cs.release();
     if (rc) return rc;
+  } else if (kind == IBMI_GUESS_MC) {
+    // Σ0[c,c] = Z_c Z_cᵀ / n, Z = L⁻ᵀ w, A = L Lᵀ (reference solver.py:167-181); w = p × ldg draws.
+    if (!guess || ldg < 1) return fail(IBMI_ERR_INVALID, "mc guess needs the p x n sample matrix");
+    rc = mc_guess_into(c->A, c->ld, p, guess, on_device, ldg, cmap, c0, c->S, c->ld, cmap, cmap, st);
+    if (rc) return rc;
+  } else if (kind == IBMI_GUESS_TAKAHASHI) {
+    // (A⁻¹)[c,c] = S_c⁻¹, S_c = A_cc − A_cI W (W = A_II⁻¹ A_Ic of set 0): the block the
+    // reference's LDLᵀ backward recurrence reproduces (solver.py:184-212).  Needs set 0 set up.
+    if (!s0.ready) return fail(IBMI_ERR_STATE, "takahashi guess needs set 0 set up (call ibmi_setup first)");
+    const int64_t b0 = s0.b;
+    CholScratch cs;
+    rc = ensure_scratch(cs, (int)c0);
+    if (rc) { cs.release(); return rc; }
+    double *aci = nullptr, *wc = nullptr, *inv = nullptr;
+    const int64_t ldb0 = round_up(b0, 32), ldc0 = round_up(c0, 32);
+    cudaError_t e = cudaMalloc(&aci, (size_t)c0 * ldb0 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&wc, (size_t)b0 * ldc0 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&inv, (size_t)c0 * cs.ldw * sizeof(double));
+    if (e != cudaSuccess) {
+      cs.release(); cudaFree(aci); cudaFree(wc); cudaFree(inv);
+      return fail(IBMI_ERR_OOM, cudaGetErrorString(e));
+    }
+    const RowMap imap = s0.rows();
+    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 0);
+    copy2d_kernel<<<grid2d(c0, b0), 256, 0, st>>>(c->A, c->ld, cmap, imap, aci, ldb0, (int)c0, (int)b0, 0);
+    copy2d_kernel<<<grid2d(b0, c0), 256, 0, st>>>(s0.W, c->ld, contig_map(0), cmap, wc, ldc0, (int)b0, (int)c0, 0);
+    GemmOp gs;   // S_c[m][n] = A_cc[m][n] − Σ_k A_cI[m][k] W_c[k][n]
+    gs.X = aci; gs.ldx = ldb0;
+    gs.Y = wc; gs.ldy = ldc0; gs.yt = true;
+    gs.M = c0; gs.N = c0;
+    gs.add_seg(0, 0, b0);
+    gs.C = cs.ws; gs.ldc = cs.ldw;
+    gs.alpha = -1.0; gs.beta = 1.0; gs.D = cs.ws; gs.ldd = cs.ldw;
+    gs.lower = true;
+    e = launch_gemm(gs, st);
+    if (e != cudaSuccess) rc = fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+    int64_t piv = -1;
+    if (!rc) rc = potrf_blocked(cs, (int)c0, st, &piv);
+    if (!rc) rc = potri_blocked(cs, (int)c0, inv, cs.ldw, st);
+    if (!rc) {
+      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(inv, cs.ldw, c->S, c->ld, cmap, cmap, (int)c0, (int)c0);
+      cudaStreamSynchronize(st);
+    }
+    cs.release();
+    cudaFree(aci);
+    cudaFree(wc);
+    cudaFree(inv);
+    if (rc) return rc;
   } else {
     return fail(IBMI_ERR_INVALID, "unknown guess kind " + std::to_string(kind));
   }
@@ -1554,6 +1655,19 @@ int ibmi_tune(int key, int value) {
   }
   ++g_tune_gen;
   return IBMI_OK;
+}
+
+int ibmi_mc_guess(int64_t p, const double* a, int64_t lda, const double* w, int64_t n, const int64_t* comp,
+                  int64_t c, double* out, int64_t ldo, void* stream) {
+  if (p < 1 || n < 1 || c < 1) return fail(IBMI_ERR_DIM, "bad sizes");
+  if (!a || !w || !comp || !out) return fail(IBMI_ERR_INVALID, "null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* dcomp = nullptr;
+  CUDA_TRY(cudaMalloc(&dcomp, c * sizeof(int64_t)));
+  CUDA_TRY(cudaMemcpy(dcomp, comp, c * sizeof(int64_t), cudaMemcpyHostToDevice));
+  int rc = mc_guess_into(a, lda, p, w, 0, n, list_map(dcomp), c, out, ldo, contig_map(0), contig_map(0), st);
+  cudaFree(dcomp);
+  return rc;
 }
 
 int ibmi_probe_fp64_peak(int device, double* tflops) {

@@ -134,6 +134,14 @@ class DeviceSolver:
         _abi.check(rc, "setup", fail_set=fs.value, fail_pivot=fp.value)
 
     def init_sigma(self, kind: int = _abi.GUESS_IDENTITY, guess: np.ndarray | None = None):
+        """Σ = I, Σ[c₁,c₁] = guess block.  GUESS_MATRIX: ``guess`` is that block (ascending
+        complement order); GUESS_MC: ``guess`` is the p × n matrix of standard-normal draws."""
+        if kind == _abi.GUESS_MC:
+            w = np.ascontiguousarray(np.asarray(guess, dtype=np.float64))
+            if self.perm is not None:
+                raise ValueError("GUESS_MC needs the original ordering; pass the block via GUESS_MATRIX")
+            _abi.check(self._L.ibmi_init_sigma(self._h, kind, C.c_void_p(w.ctypes.data), w.shape[1], 0), "init_sigma")
+            return
         if kind == _abi.GUESS_MATRIX:
             g = np.ascontiguousarray(np.asarray(guess, dtype=np.float64))
             if self.perm is not None:

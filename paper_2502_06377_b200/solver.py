@@ -36,6 +36,8 @@ __all__ = [
     "error_estimate",
     "initial_guess_identity",
     "initial_guess_local_inverse",
+    "initial_guess_monte_carlo",
+    "initial_guess_takahashi",
     "make_initial_guess",
     "solve",
 ]
@@ -111,20 +113,71 @@ def initial_guess_local_inverse(a, comp) -> np.ndarray:
     return spd_inverse(a[np.ix_(comp, comp)])
 
 
+def _mc_draws(p: int, n_samples: int, seed: int) -> np.ndarray:
+    """The reference's standard-normal draws (solver.py:178), so the GPU guess
+    matches it sample for sample."""
+    return np.random.default_rng(seed).standard_normal((p, n_samples))
+
+
+def initial_guess_monte_carlo(a, comp, n_samples: int, seed: int) -> np.ndarray:
+    """solver.py:167-181 — sample covariance of L⁻ᵀw on ``comp``; Cholesky,
+    triangular inverse and both products on the GPU (``ibmi_mc_guess``)."""
+    import ctypes as C
+
+    import torch
+
+    if n_samples < 1:
+        raise ValueError(f"n_samples must be >= 1, got {n_samples}")
+    comp = np.ascontiguousarray(np.asarray(comp, dtype=np.int64))
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        da = a.to(torch.float64).contiguous()
+    else:
+        da = torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float64)), device="cuda")
+    p = da.shape[0]
+    w = np.ascontiguousarray(_mc_draws(p, n_samples, seed))
+    out = torch.zeros((comp.size, comp.size), dtype=torch.float64, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _abi.check(_abi.lib().ibmi_mc_guess(p, C.c_void_p(da.data_ptr()), da.stride(0), C.c_void_p(w.ctypes.data), n_samples,
+                                        C.c_void_p(comp.ctypes.data), comp.size, C.c_void_p(out.data_ptr()),
+                                        comp.size, st), "mc_guess")
+    return out.cpu().numpy()
+
+
+def initial_guess_takahashi(a, comp) -> np.ndarray:
+    """solver.py:184-212 — the comp × comp block of A⁻¹, which the reference's
+    LDLᵀ backward recurrence reproduces; on the GPU it is S_c⁻¹ with
+    S_c = A_cc − A_cI A_II⁻¹ A_Ic (``IBMI_GUESS_TAKAHASHI``)."""
+    a = np.asarray(a, dtype=np.float64)
+    comp = np.asarray(comp, dtype=np.int64)
+    p = a.shape[0]
+    keep = np.ones(p, dtype=bool)
+    keep[comp] = False
+    rest = np.nonzero(keep)[0]
+    perm = np.concatenate([rest, comp])
+    with DeviceSolver(a, [(0, rest.size), (rest.size, p)], perm=perm) as ds:
+        ds.setup(0, 1)
+        ds.init_sigma(_abi.GUESS_TAKAHASHI)
+        s = ds.sigma()
+    return s[np.ix_(comp, comp)]
+
+
 def make_initial_guess(a, comp, cfg: IbmiConfig) -> np.ndarray:
-    """solver.py:215-222 for the guesses available on the device path."""
+    """solver.py:215-222 (plus the BASELINE ``jacobi`` seed), all on the GPU."""
     if cfg.initial_guess == GUESS_IDENTITY:
         return initial_guess_identity(len(comp))
     if cfg.initial_guess == GUESS_LOCAL_INVERSE:
         return initial_guess_local_inverse(a, comp)
+    if cfg.initial_guess == GUESS_MONTE_CARLO:
+        return initial_guess_monte_carlo(a, comp, cfg.mc_samples, cfg.mc_seed)
     if cfg.initial_guess == GUESS_JACOBI:
         d = np.diag(np.asarray(a, dtype=np.float64))[np.asarray(comp, dtype=np.intp)]
         return np.diag(1.0 / d)
-    raise NotImplementedError(f"initial guess {cfg.initial_guess!r} is not available on the B200 path yet")
+    return initial_guess_takahashi(a, comp)
 
 
 _GUESS_KIND = {GUESS_IDENTITY: _abi.GUESS_IDENTITY, GUESS_JACOBI: _abi.GUESS_JACOBI,
-               GUESS_LOCAL_INVERSE: _abi.GUESS_LOCAL}
+               GUESS_LOCAL_INVERSE: _abi.GUESS_LOCAL, GUESS_TAKAHASHI: _abi.GUESS_TAKAHASHI,
+               GUESS_MONTE_CARLO: _abi.GUESS_MC}
 
 
 def _shape_of(a):
@@ -160,7 +213,15 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
         if prof:
             print(f"[ibmi] context+upload {t0 - t_enter:.3f}s", file=sys.stderr)
         ds.setup()
-        ds.init_sigma(_GUESS_KIND[cfg.initial_guess])
+        kind = _GUESS_KIND[cfg.initial_guess]
+        if kind == _abi.GUESS_MC:
+            if ds.perm is None:
+                ds.init_sigma(kind, _mc_draws(part.p, cfg.mc_samples, cfg.mc_seed))
+            else:   # relabelled partition: draw in the original order, insert the block
+                comp0 = complement(part, 0)
+                ds.init_sigma(_abi.GUESS_MATRIX, initial_guess_monte_carlo(a, comp0, cfg.mc_samples, cfg.mc_seed))
+        else:
+            ds.init_sigma(kind)
         setup_s = time.perf_counter() - t0
         errs, walls, pits, resid = [], [], [], []
         converged, it = False, 0

@@ -147,6 +147,16 @@ def pins():
     assert (s_ref, c_ref, it_ref) == (s_or, c_or, it_or)
     out["restart_b"] = m
     out["restart_out"] = np.array([s_ref, float(c_ref), float(it_ref)])
+    # initial guesses (solver.py:167-212) on a small SPD matrix
+    a = out["case1_a"]
+    part = ibmi.contiguous_partition(96, 3, 0.1)
+    comp = ibmi.complement(part, 0)
+    g_mc = rsol.initial_guess_monte_carlo(a, comp, 50, 7)
+    g_tk = rsol.initial_guess_takahashi(a, comp)
+    assert np.array_equal(orc.guess_monte_carlo(a, comp, 50, 7), g_mc)
+    assert np.abs(orc.guess_takahashi(a, comp) - g_tk).max() <= 1e-12 * np.abs(g_tk).max()
+    out["guess_mc"] = g_mc
+    out["guess_takahashi"] = g_tk
     np.savez_compressed(os.path.join(HERE, "pins.npz"), **out)
     print("pins OK:", len(cases), "cases")
 

@@ -381,3 +381,42 @@ def test_solve_mixed_runs_and_lists_local_guess():
     o = orc.solve(a, part.sets, tol=1e-11, guess="local")
     assert rel_fro(rep.result, o["result"]) < 1e-10
     check_trace(rep.error_trace, o["error_trace"], 1e-11)
+
+
+def test_initial_guesses_match_reference():
+    """GPU mc / takahashi / local guesses against the reference's own values."""
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+
+    pins = golden("pins.npz")
+    a = pins["case1_a"]
+    part = pkg.contiguous_partition(96, 3, 0.1)
+    comp = pkg.complement(part, 0)
+    g = pkg.initial_guess_monte_carlo(a, comp, 50, 7)
+    assert rel_fro(g, pins["guess_mc"]) < 1e-12
+    g = pkg.initial_guess_takahashi(a, comp)
+    assert rel_fro(g, pins["guess_takahashi"]) < 1e-12
+    g = pkg.initial_guess_local_inverse(a, comp)
+    assert rel_fro(g, orc.spd_inverse(a[np.ix_(comp, comp)])) < 1e-12
+
+
+@pytest.mark.parametrize("guess", ["mc", "takahashi"])
+@pytest.mark.parametrize("kind", ["contiguous", "red-black", "general"])
+def test_solve_with_guess_matches_oracle(guess, kind):
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+
+    p = 192
+    a = random_spd(p, 31)
+    if kind == "contiguous":
+        part = pkg.contiguous_partition(p, 3, 0.1)
+    elif kind == "red-black":
+        part = pkg.red_black_partition(p)
+    else:
+        perm = np.random.default_rng(5).permutation(p)
+        part = pkg.load_partition_json({"p": p, "sets": [np.sort(perm[:110]).tolist(), np.sort(perm[90:]).tolist()]})
+    cfg = pkg.IbmiConfig(tol=1e-11, initial_guess=guess, mc_samples=40, mc_seed=3)
+    rep = pkg.solve(a, part, cfg)
+    o = orc.solve(a, part.sets, tol=1e-11, guess=guess, mc_samples=40, mc_seed=3)
+    assert rep.converged and abs(rep.iterations - o["iterations"]) <= 1
+    assert rel_fro(rep.result, o["result"]) < 1e-10

@@ -54,3 +54,13 @@ def test_oracle_c2_first_sweeps():
     o = orc.solve(a, cfg.partition().sets, tol=cfg.tol, max_iterations=2, guess="jacobi", stopping="frobenius")
     assert np.array_equal(np.array(o["error_trace"]), g["error_trace"][:2])
     np.testing.assert_allclose(o["frobenius_trace"], g["frobenius_trace"][:2], rtol=1e-12)
+
+
+def test_oracle_initial_guesses_against_reference():
+    pins = golden("pins.npz")
+    a = pins["case1_a"]
+    part = contiguous_partition(96, 3, 0.1)
+    comp = orc.complement(96, part.sets[0])
+    assert np.array_equal(orc.guess_monte_carlo(a, comp, 50, 7), pins["guess_mc"])
+    g = pins["guess_takahashi"]
+    assert np.abs(orc.guess_takahashi(a, comp) - g).max() <= 1e-12 * np.abs(g).max()
