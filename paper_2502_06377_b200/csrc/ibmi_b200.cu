@@ -1255,7 +1255,7 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
       return fail(IBMI_ERR_OOM, cudaGetErrorString(e));
     }
     const RowMap imap = s0.rows();
-    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 0);
+    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 1);
     copy2d_kernel<<<grid2d(c0, b0), 256, 0, st>>>(c->A, c->ld, cmap, imap, aci, ldb0, (int)c0, (int)b0, 0);
     copy2d_kernel<<<grid2d(b0, c0), 256, 0, st>>>(s0.W, c->ld, contig_map(0), cmap, wc, ldc0, (int)b0, (int)c0, 0);
     GemmOp gs;   // S_c[m][n] = A_cc[m][n] − Σ_k A_cI[m][k] W_c[k][n]

@@ -392,6 +392,10 @@ def test_initial_guesses_match_reference():
     a = pins["case1_a"]
     part = pkg.contiguous_partition(96, 3, 0.1)
     comp = pkg.complement(part, 0)
+    # multi-block factorisations (c > 64) of the Schur complement as well
+    big = random_spd(300, 8)
+    cbig = np.arange(40, 300)
+    assert rel_fro(pkg.initial_guess_takahashi(big, cbig), np.linalg.inv(big)[np.ix_(cbig, cbig)]) < 1e-12
     g = pkg.initial_guess_monte_carlo(a, comp, 50, 7)
     assert rel_fro(g, pins["guess_mc"]) < 1e-12
     g = pkg.initial_guess_takahashi(a, comp)
