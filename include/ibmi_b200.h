@@ -180,6 +180,15 @@ typedef struct {
   int lower, tma_safe, splits;
   double* frob_out;
   double* ws; int64_t ws_len;
+  /* fused exchange (sharded sweep): when peers != NULL the direct store of
+   * (m, n) goes to peers[h][lr][gc] with r = cm(m) (global row), h = (r/T)%G,
+   * lr = (r/(T*G))*T + r%T, l = cn(n) (local row of bc_rank), gc = ((l/T)*G +
+   * bc_rank)*T + l%T, T = bc_panel, G = bc_world — i.e. straight into the row
+   * panel of the owner through NVLink peer pointers (IPC-mapped). */
+  double* const* peers; int64_t bc_panel; int bc_world, bc_rank;
+  /* transposed operands: X(m, k) = x[(x0 + k) * ldx + xm.off0 + m] (likewise Y);
+   * contiguous maps only, cp.async kernel. */
+  int xt, yt;
 } ibmi_gemm_desc;
 
 int ibmi_gemm(const ibmi_gemm_desc* desc, void* stream);
@@ -188,6 +197,14 @@ int ibmi_gemm_workspace(const ibmi_gemm_desc* desc, int64_t* doubles);
 /* Device pointer, shape and leading dimension of a context buffer:
  * which = 0 A, 1 Σ, 2 W_k (b_k × ld, global columns), 3 A_II⁻¹ of set k. */
 int ibmi_export(ibmi_ctx* ctx, int which, int k, double** ptr, int64_t* rows, int64_t* cols, int64_t* ld);
+
+/* Device memory for peer-visible buffers and its CUDA IPC handle (64 bytes),
+ * opened by the other ranks of the node for the fused exchange. */
+int ibmi_device_alloc(int device, int64_t bytes, void** ptr);
+int ibmi_device_free(void* ptr);
+int ibmi_ipc_handle(void* ptr, void* handle64);
+int ibmi_ipc_open(int device, const void* handle64, void** ptr);
+int ibmi_ipc_close(void* ptr);
 
 /* Tuning knobs (process-wide; contexts re-capture their sweep graph):
  * key 0: GEMM configuration of the hot NT kernels (0: 8 warps 64x32, BK16;

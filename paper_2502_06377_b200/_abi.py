@@ -54,6 +54,11 @@ SIGNATURES = [
     ("ibmi_gemm_workspace", C.c_int, [_P, C.POINTER(_I64)]),
     ("ibmi_export", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(_I64), C.POINTER(_I64),
                               C.POINTER(_I64)]),
+    ("ibmi_device_alloc", C.c_int, [C.c_int, _I64, C.POINTER(_P)]),
+    ("ibmi_device_free", C.c_int, [_P]),
+    ("ibmi_ipc_handle", C.c_int, [_P, C.c_char_p]),
+    ("ibmi_ipc_open", C.c_int, [C.c_int, C.c_char_p, C.POINTER(_P)]),
+    ("ibmi_ipc_close", C.c_int, [_P]),
     ("ibmi_tune", C.c_int, [C.c_int, C.c_int]),
     ("ibmi_probe_fp64_peak", C.c_int, [C.c_int, _D]),
 ]
@@ -152,4 +157,6 @@ class GemmDesc(C.Structure):
         ("lower", C.c_int), ("tma_safe", C.c_int), ("splits", C.c_int),
         ("frob_out", C.c_void_p),
         ("ws", C.c_void_p), ("ws_len", C.c_int64),
+        ("peers", C.c_void_p), ("bc_panel", C.c_int64), ("bc_world", C.c_int), ("bc_rank", C.c_int),
+        ("xt", C.c_int), ("yt", C.c_int),
     ]

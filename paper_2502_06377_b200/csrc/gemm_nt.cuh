@@ -73,10 +73,29 @@ struct GemmParams {
   double* C2; int64_t ldc2; RowMap c2m, c2n;   // mirror target (defaults to C, cm, cn)
   const int64_t* cidx;                       // optional: direct-store / δ row = cidx[m] instead of cm(m)
   int direct;                                // write the direct store C[cm(m)][cn(n)] (default 1)
+  // peer mode (sharded sweep, fused exchange): the direct store goes to the
+  // row-panel owner's Σ through NVLink peer pointers.  cm(m) is the global
+  // row r, cn(n) this rank's local row l; block-cyclic panels of bc_panel rows.
+  double* const* peers;
+  int64_t bc_panel;
+  int bc_world, bc_rank;
   int lower;                                 // only tiles tm >= tn; in diagonal tiles only m >= n
   int tiles_m, tiles_n;
   double* partial;                           // EPI_FROB: one partial sum per CTA; EPI_PARTIAL: split tiles
 };
+
+// Direct-store address of element (m, n) (rowc = cidx/cm row already mapped).
+__device__ __forceinline__ double* direct_addr(const GemmParams& P, int64_t rowc, int n) {
+  if (P.peers) {
+    const int64_t T = P.bc_panel, G = P.bc_world;
+    const int h = (int)((rowc / T) % G);
+    const int64_t lr = (rowc / (T * G)) * T + rowc % T;
+    const int64_t l = map_idx(P.cn, n);
+    const int64_t gc = ((l / T) * G + P.bc_rank) * T + l % T;
+    return P.peers[h] + lr * P.ldc + gc;
+  }
+  return P.C + rowc * P.ldc + map_idx(P.cn, n);
+}
 
 template <int BK>
 __device__ __forceinline__ int swz(int r, int k) {   // non-transposed tile element (r, k)
@@ -296,11 +315,12 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
           if (diag_tile && m < n) continue;
           double v = P.alpha * acc[i][j][e];
           if (P.beta != 0.0) v += P.beta * P.D[rowd * P.ldd + map_idx(P.dn, n)];
-          if (P.direct) P.C[rowc * P.ldc + map_idx(P.cn, n)] = v;
+          if (P.direct) *direct_addr(P, rowc, n) = v;
           if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + mcol2] = v;
         }
       }
     }
+    if (P.peers) __threadfence_system();   // peer stores visible before the exchange barrier
   } else if (EPI == EPI_PARTIAL) {
     // raw partial tile [128][128] of (tile, split), reduced later in fixed split order
     double* dst = P.partial + ((size_t)blockIdx.x) * GB_M * GB_N;
@@ -371,7 +391,7 @@ __global__ void splitk_reduce_kernel(const GemmParams P) {
     double v = P.alpha * acc;
     const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
     if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + map_idx(P.dn, n)];
-    if (P.direct) P.C[rowc * P.ldc + map_idx(P.cn, n)] = v;
+    if (P.direct) *direct_addr(P, rowc, n) = v;
     if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + map_idx(P.c2m, m)] = v;
   }
 }

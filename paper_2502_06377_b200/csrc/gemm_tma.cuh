@@ -219,11 +219,12 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
           if (diag_tile && m < n) continue;
           double v = P.alpha * acc[i][j][e];
           if (P.beta != 0.0) v += P.beta * P.D[rowd * P.ldd + map_idx(P.dn, n)];
-          if (P.direct) P.C[rowc * P.ldc + map_idx(P.cn, n)] = v;
+          if (P.direct) *direct_addr(P, rowc, n) = v;
           if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + mcol2] = v;
         }
       }
     }
+    if (P.peers) __threadfence_system();
   } else if (EPI == EPI_PARTIAL) {
     double* dst = P.partial + ((size_t)blockIdx.x) * GB_M * GB_N;
 #pragma unroll

@@ -62,6 +62,7 @@ struct GemmOp {
   bool c2_set = false;           // false: mirror into C with (cm, cn)
   const int64_t* cidx = nullptr; // optional row index array for the direct store / δ
   bool direct = true;
+  double* const* peers = nullptr; int64_t bc_panel = 0; int bc_world = 1, bc_rank = 0;  // fused exchange
   double* partial = nullptr;     // non-null -> Frobenius epilogue
   int splits = 1;                // split-K factor (needs ws: tiles*splits*128*128 doubles)
   double* ws = nullptr;
@@ -233,6 +234,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
   else { P.C2 = op.C; P.ldc2 = op.ldc; P.c2m = op.cm; P.c2n = op.cn; }
   P.cidx = op.cidx;
   P.direct = op.direct ? 1 : 0;
+  P.peers = op.peers; P.bc_panel = op.bc_panel; P.bc_world = op.bc_world; P.bc_rank = op.bc_rank;
   P.tiles_m = (P.M + GB_M - 1) / GB_M;
   P.tiles_n = (P.N + GB_N - 1) / GB_N;
   const int tiles = gemm_tiles(op);
@@ -1582,6 +1584,17 @@ static int desc_to_op(const ibmi_gemm_desc* d, GemmOp& op) {
   op.tma_ok = d->tma_safe != 0;
   op.xrows = d->xrows; op.xcols = d->xcols; op.yrows = d->yrows; op.ycols = d->ycols;
   op.splits = d->splits > 1 ? d->splits : 1;
+  op.xt = d->xt != 0;
+  op.yt = d->yt != 0;
+  if ((op.xt && (op.xm.idx || op.xm.split != INT_MAX)) || (op.yt && (op.yn.idx || op.yn.split != INT_MAX)))
+    return fail(IBMI_ERR_INVALID, "transposed operands take contiguous maps only");
+  if (op.xt || op.yt) { op.tma_ok = false; op.splits = 1; }
+  if (d->peers) {
+    if (d->bc_panel < 1 || d->bc_world < 1 || d->bc_rank < 0 || d->bc_rank >= d->bc_world || op.cidx)
+      return fail(IBMI_ERR_INVALID, "bad peer-store layout");
+    op.peers = d->peers; op.bc_panel = d->bc_panel; op.bc_world = d->bc_world; op.bc_rank = d->bc_rank;
+    op.splits = 1;
+  }
   return IBMI_OK;
 }
 
@@ -1631,6 +1644,41 @@ int ibmi_export(ibmi_ctx* c, int which, int k, double** ptr, int64_t* rows, int6
   if (which == 2) { *ptr = s.W; if (rows) *rows = s.b; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK; }
   if (which == 3) { *ptr = s.ainv; if (rows) *rows = s.b; if (cols) *cols = s.b; if (ld) *ld = s.ldb; return IBMI_OK; }
   return fail(IBMI_ERR_INVALID, "unknown buffer");
+}
+
+int ibmi_device_alloc(int device, int64_t bytes, void** ptr) {
+  if (!ptr || bytes < 0) return fail(IBMI_ERR_INVALID, "bad argument");
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaMalloc(ptr, bytes > 0 ? bytes : 8));
+  CUDA_TRY(cudaMemset(*ptr, 0, bytes > 0 ? bytes : 8));
+  return IBMI_OK;
+}
+
+int ibmi_device_free(void* ptr) {
+  if (ptr) CUDA_TRY(cudaFree(ptr));
+  return IBMI_OK;
+}
+
+int ibmi_ipc_handle(void* ptr, void* handle) {
+  if (!ptr || !handle) return fail(IBMI_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, ptr));
+  memcpy(handle, &h, sizeof(h));
+  return IBMI_OK;
+}
+
+int ibmi_ipc_open(int device, const void* handle, void** ptr) {
+  if (!ptr || !handle) return fail(IBMI_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return IBMI_OK;
+}
+
+int ibmi_ipc_close(void* ptr) {
+  if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return IBMI_OK;
 }
 
 int ibmi_tune(int key, int value) {

@@ -96,6 +96,11 @@ class GemmSpec:
     xcols: int = 0
     yrows: int = 0
     ycols: int = 0
+    xt: bool = False                 # X given transposed: X(m, k) = x[seg.x0 + k][xm.off0 + m]
+    peers: object = None             # int64 tensor of per-rank Σ panel pointers (fused exchange)
+    bc_panel: int = 0
+    bc_world: int = 1
+    bc_rank: int = 0
     extra: dict = field(default_factory=dict)
 
 
@@ -186,6 +191,9 @@ class CudaBackend:
             d.d, d.ldd = s.d.data_ptr(), s.d.stride(0)
             d.dm, d.dn = _cmap(s.dm), _cmap(s.dn)
         d.lower, d.tma_safe, d.splits = int(s.lower), int(s.tma_safe), 1
+        d.xt = int(s.xt)
+        if s.peers is not None:
+            d.peers, d.bc_panel, d.bc_world, d.bc_rank = s.peers.data_ptr(), s.bc_panel, s.bc_world, s.bc_rank
         out = None
         if s.frob:
             out = torch.zeros(2, dtype=torch.float64, device=self.device)
@@ -200,6 +208,27 @@ class CudaBackend:
         _abi.check(self.L.ibmi_gemm(C.byref(d), stream), "gemm")
         return out[1] if s.frob else None
 
+    def gemm_xt(self, x, x_col0, y, m, n, segs, c, alpha=1.0):
+        """C = alpha · X · Yᵀ with X(m, k) = x[x0 + k][x_col0 + m] (x read transposed)."""
+        self.gemm(GemmSpec(x=x, xm=x_col0, y=y, yn=0, m=m, n=n, segs=segs, c=c, alpha=alpha, xt=True,
+                           xrows=x.shape[0], xcols=x.shape[1], yrows=y.shape[0], ycols=y.shape[1]))
+
+    # peer-visible Σ panels for the fused exchange
+    def alloc_shared(self, rows, cols):
+        ptr = C.c_void_p()
+        _abi.check(self.L.ibmi_device_alloc(self.device.index, int(rows) * int(cols) * 8, C.byref(ptr)), "device_alloc")
+        self._shared = getattr(self, "_shared", []) + [ptr.value]
+        t = self.torch.as_tensor(_CudaArray(ptr.value, rows, cols, cols), device=self.device)
+        h = C.create_string_buffer(64)
+        _abi.check(self.L.ibmi_ipc_handle(C.c_void_p(ptr.value), h), "ipc_handle")
+        return t, bytes(h.raw)
+
+    def open_peer(self, handle: bytes) -> int:
+        ptr = C.c_void_p()
+        _abi.check(self.L.ibmi_ipc_open(self.device.index, handle, C.byref(ptr)), "ipc_open")
+        self._opened = getattr(self, "_opened", []) + [ptr.value]
+        return ptr.value
+
     def two_norm(self, b, rtol, max_iters):
         torch = self.torch
         v = restart_vector(b.shape[1])
@@ -211,6 +240,13 @@ class CudaBackend:
         return sig.value, it.value, bool(cv.value)
 
     def close(self):
+        self.torch.cuda.synchronize(self.device)
+        for ptr in getattr(self, "_opened", []):
+            self.L.ibmi_ipc_close(C.c_void_p(ptr))
+        self._opened = []
+        for ptr in getattr(self, "_shared", []):
+            self.L.ibmi_device_free(C.c_void_p(ptr))
+        self._shared = []
         if self._ctx is not None:
             self._ctx.close()
             self._ctx = None
@@ -282,7 +318,7 @@ class ShardedSolver:
     """
 
     def __init__(self, a, partition: Partition | None = None, ranges=None, *, group=None, panel: int = 128,
-                 backend=None, device: int | None = None):
+                 backend=None, device: int | None = None, exchange: str = "nccl"):
         import torch
         import torch.distributed as dist
 
@@ -310,7 +346,18 @@ class ShardedSolver:
         self.n_loc = len(self.own)
         self.A, self.W, self.ainv = backend.setup(a, self.ranges)
         self.ld = self.A.stride(0)
-        self.S = backend.zeros(max(self.n_loc, 1), self.ld)
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        self.exchange = exchange
+        if exchange == "p2p":
+            # Σ panels live in IPC-exportable memory; every rank maps every peer's panel
+            self.S, handle = backend.alloc_shared(max(self.n_loc, 1), self.ld)
+            handles = [None] * self.world
+            self.torch.distributed.all_gather_object(handles, handle, group=self.comm.group)
+            ptrs = [self.S.data_ptr() if h == self.rank else backend.open_peer(handles[h]) for h in range(self.world)]
+            self.peers = backend.index_tensor(np.asarray(ptrs, dtype=np.uint64).view(np.int64))
+        else:
+            self.S = backend.zeros(max(self.n_loc, 1), self.ld)
         self.own_t = backend.index_tensor(self.own)
         self.plan = [self._plan_set(lo, hi) for (lo, hi) in self.ranges]
 
@@ -365,6 +412,8 @@ class ShardedSolver:
         lo, hi, b, a0, a1, n_cl = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"], pl["n_cl"]
         p = self.p
         segs = [(0, 0, lo), (hi, hi, p - hi)]
+        if self.exchange == "p2p":
+            return self._block_update_p2p(k)
         Mbuf = be.zeros(b, max(n_cl, 1))
         if n_cl > 0:
             # 1. Mbuf = −W Σ[c_own, c]ᵀ ; mirror: Σ_loc[c_own row][lo + m] = −M
@@ -401,6 +450,30 @@ class ShardedSolver:
         elif a1 > a0 and n_cl > 0:
             # single rank: the owner rows are all of I
             self.S[a0:a1].index_copy_(1, pl["cols_c"][0], Mbuf[:, :n_cl])
+
+    def _block_update_p2p(self, k: int):
+        """Fused exchange: the panel GEMM's epilogue stores −M rows straight into
+        the owners' Σ panels over NVLink (peer pointers), and mirrors −Mᵀ into the
+        local panel, from which the Σ_II partial is read back (no all_to_all)."""
+        be, pl = self.be, self.plan[k]
+        lo, hi, b, a0, a1, n_cl = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"], pl["n_cl"]
+        p = self.p
+        if n_cl > 0:
+            be.gemm(GemmSpec(x=self.W[k], xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl,
+                             segs=[(0, 0, lo), (hi, hi, p - hi)], c=self.S, cm=lo, cn=(a0, 0, a1),
+                             mirror=True, c2=self.S, c2m=lo, c2n=(a0, 0, a1), alpha=-1.0, tma_safe=True,
+                             xrows=b, xcols=p, yrows=self.n_loc, ycols=p, peers=self.peers,
+                             bc_panel=self.layout.panel, bc_world=self.world, bc_rank=self.rank))
+        top = be.zeros(b, b)
+        if n_cl > 0:
+            # top = −(−M)·W_cᵀ with −M read from the mirrored local panel Σ[c_own, I]
+            be.gemm_xt(x=self.S, x_col0=lo, y=self._w_loc(k), m=b, n=b,
+                       segs=[(0, 0, a0), (a1, a1, self.n_loc - a1)], c=top, alpha=-1.0)
+        self.comm.all_reduce(top)     # also the barrier after which the peers' stores have landed
+        if a1 > a0:
+            t = self.ainv[k] + top
+            rel = pl["my_rows_rel"]
+            self.S[a0:a1, lo:hi] = 0.5 * (t.index_select(0, rel) + t.t().index_select(0, rel))
 
     # ------------------------------------------------------------ estimate
     def error_estimate(self, k: int, rtol: float = 1e-9, max_iters: int = 5000):

@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, backend, case, out):
+def _worker(rank, world, port, backend, case, out, exchange="nccl"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -45,7 +45,7 @@ def _worker(rank, world, port, backend, case, out):
             p, k, f = name
             m = np.random.default_rng(p).standard_normal((p, p))
             a, part, guess = m.T @ m + p * np.eye(p), contiguous_partition(p, k, f), "identity"
-        ss = ShardedSolver(a, part, panel=panel, device=0)
+        ss = ShardedSolver(a, part, panel=panel, device=0, exchange=exchange)
         ss.init_sigma(guess)
         errs = [ss.sweep()[0] for _ in range(sweeps)]
         sig = ss.gather_sigma()
@@ -56,11 +56,11 @@ def _worker(rank, world, port, backend, case, out):
         dist.destroy_process_group()
 
 
-def _run(world, backend, case):
+def _run(world, backend, case, exchange="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, case, q, exchange)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -70,10 +70,11 @@ def _run(world, backend, case):
     return res
 
 
-@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
-def test_sharded_c1_matches_reference(world, backend):
+@pytest.mark.parametrize("world,backend,exchange", [(1, "nccl", "nccl"), (2, "gloo", "nccl"), (1, "nccl", "p2p"),
+                                                     (2, "gloo", "p2p")])
+def test_sharded_c1_matches_reference(world, backend, exchange):
     g = golden("c1.npz")
-    res = _run(world, backend, ("c1", int(g["iterations"][0]), 128))
+    res = _run(world, backend, ("c1", int(g["iterations"][0]), 128), exchange)
     for rank, errs, sig, fr in res:
         assert np.linalg.norm(sig - g["sigma"]) <= 1e-10 * np.linalg.norm(g["sigma"])
         ref = g["error_trace"]
@@ -81,13 +82,14 @@ def test_sharded_c1_matches_reference(world, backend):
         assert fr < 1e-9
 
 
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
 @pytest.mark.parametrize("case", [((1024, 4, 0.125), 6, 128), ((520, 3, 0.1), 5, 64)])
-def test_sharded_two_ranks_match_oracle(case):
+def test_sharded_two_ranks_match_oracle(case, exchange):
     from oracle import ibmi_oracle as orc
     from paper_2502_06377_b200 import contiguous_partition
 
     (p, k, f), sweeps, panel = case
-    res = _run(2, "gloo", case)
+    res = _run(2, "gloo", case, exchange)
     m = np.random.default_rng(p).standard_normal((p, p))
     a = m.T @ m + p * np.eye(p)
     o = orc.solve(a, contiguous_partition(p, k, f).sets, tol=1e-300, max_iterations=sweeps)

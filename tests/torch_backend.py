@@ -65,6 +65,13 @@ class TorchCPUBackend:
             c2[c2n[ni], c2m[mi]] = v[mi, ni]
         return None
 
+    def gemm_xt(self, x, x_col0, y, m, n, segs, c, alpha=1.0):
+        acc = torch.zeros((m, n), dtype=torch.float64)
+        for x0, y0, ln in segs:
+            if ln > 0:
+                acc += x[x0:x0 + ln, x_col0:x_col0 + m].T @ y[:n, y0:y0 + ln].T
+        c[:m, :n] = alpha * acc
+
     def two_norm(self, b, rtol, max_iters):
         s, conv, it = orc.power_sigma_max(b.numpy(), rtol, max_iters)
         return s, it, conv
