@@ -280,6 +280,15 @@ class _Comm:
             self.dist.all_reduce(t, group=self.group)
         return t
 
+    def barrier(self):
+        """Stream-ordered barrier (a one-element all-reduce)."""
+        if self.world == 1:
+            return
+        if getattr(self, "_tok", None) is None:
+            self._tok = self.torch.zeros(1, dtype=self.torch.float64,
+                                         device="cpu" if self.backend == "gloo" else "cuda")
+        self.all_reduce(self._tok)
+
     def all_to_all(self, out, inp, out_splits, in_splits):
         if self.world == 1:
             out.copy_(inp)
@@ -474,6 +483,9 @@ class ShardedSolver:
             t = self.ainv[k] + top
             rel = pl["my_rows_rel"]
             self.S[a0:a1, lo:hi] = 0.5 * (t.index_select(0, rel) + t.t().index_select(0, rel))
+        # With overlapping sets the next step's peer stores hit rows of I_k ∩ I_{k+1}
+        # that this Σ_II write also touches: every rank must finish it first.
+        self.comm.barrier()
 
     # ------------------------------------------------------------ estimate
     def error_estimate(self, k: int, rtol: float = 1e-9, max_iters: int = 5000):
