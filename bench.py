@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1 (diagnostic)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"])
     return ap.parse_args()
 
 
@@ -241,7 +243,13 @@ def run_ours(args):
     sizes = [len(s) for s in part.sets]
     guess = "jacobi" if cfg.guess == "jacobi" else "identity"
 
-    if world == 1:
+    if args.sharded and world == 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(f"cuda:{dev}"))
+    if world == 1 and not args.sharded:
         solver = DeviceSolver(a_dev, partition=part, device=dev, stream=stream.cuda_stream)
         del a_dev
         t0 = time.perf_counter()
@@ -254,7 +262,7 @@ def run_ours(args):
         from paper_2502_06377_b200.distributed import ShardedSolver
 
         t0 = time.perf_counter()
-        solver = ShardedSolver(a_dev, part, device=dev)
+        solver = ShardedSolver(a_dev, part, device=dev, exchange=args.exchange)
         solver.init_sigma(guess)
         torch.cuda.synchronize()
         setup_s = time.perf_counter() - t0
@@ -263,7 +271,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         sweep()
     errs = []
-    if world > 1:
+    if world > 1 or args.sharded:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -281,7 +289,7 @@ def run_ours(args):
     ms_step = ms / args.steps
     sweeps_s = args.steps / (ms / 1e3)
     kt, panel_tf = None, None
-    if world == 1:
+    if world == 1 and not args.sharded:
         # per-kernel-class device times of one sweep (CUDA events on the same stream)
         timed = [solver.sweep_timed(1e-9, 5000)[3] for _ in range(2)]
         kt = {k: min(t[k] for t in timed) for k in timed[0]}
@@ -289,7 +297,7 @@ def run_ours(args):
         panel_tf = panel_flops / (kt["panel_gemm"] * 1e-3) / 1e12
     # time to tolerance from a fresh Σ0 (setup included), same solver state machine
     ttt = None
-    if world == 1:
+    if world == 1 and not args.sharded:
         solver.init_sigma(1 if guess == "jacobi" else 0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -359,7 +367,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.sharded:
         torch.distributed.destroy_process_group()
 
 

@@ -327,7 +327,7 @@ class ShardedSolver:
     """
 
     def __init__(self, a, partition: Partition | None = None, ranges=None, *, group=None, panel: int = 128,
-                 backend=None, device: int | None = None, exchange: str = "nccl"):
+                 backend=None, device: int | None = None, exchange: str = "auto"):
         import torch
         import torch.distributed as dist
 
@@ -355,6 +355,13 @@ class ShardedSolver:
         self.n_loc = len(self.own)
         self.A, self.W, self.ainv = backend.setup(a, self.ranges)
         self.ld = self.A.stride(0)
+        if exchange == "auto":
+            # fused peer-memory exchange when every rank is on this node (NVLink/NVSwitch)
+            import socket
+
+            names = [None] * self.world
+            self.torch.distributed.all_gather_object(names, socket.gethostname(), group=self.comm.group)
+            exchange = "p2p" if isinstance(backend, CudaBackend) and len(set(names)) == 1 else "nccl"
         if exchange not in ("nccl", "p2p"):
             raise ValueError(f"unknown exchange {exchange!r}")
         self.exchange = exchange
