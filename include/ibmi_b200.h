@@ -180,11 +180,11 @@ typedef struct {
   int lower, tma_safe, splits;
   double* frob_out;
   double* ws; int64_t ws_len;
-  /* fused exchange (sharded sweep): when peers != NULL the direct store of
-   * (m, n) goes to peers[h][lr][gc] with r = cm(m) (global row), h = (r/T)%G,
-   * lr = (r/(T*G))*T + r%T, l = cn(n) (local row of bc_rank), gc = ((l/T)*G +
-   * bc_rank)*T + l%T, T = bc_panel, G = bc_world — i.e. straight into the row
-   * panel of the owner through NVLink peer pointers (IPC-mapped). */
+  /* fused exchange (sharded sweep): when peers != NULL every element (m, n) is
+   * also stored to peers[h][lr * ldc2 + gc] with r = c2m(m) (global row),
+   * h = (r/T)%G, lr = (r/(T*G))*T + r%T, l = c2n(n) (local row of bc_rank),
+   * gc = ((l/T)*G + bc_rank)*T + l%T, T = bc_panel, G = bc_world — straight
+   * into the owner's row panel through NVLink peer pointers (IPC-mapped). */
   double* const* peers; int64_t bc_panel; int bc_world, bc_rank;
   /* transposed operands: X(m, k) = x[(x0 + k) * ldx + xm.off0 + m] (likewise Y);
    * contiguous maps only, cp.async kernel. */

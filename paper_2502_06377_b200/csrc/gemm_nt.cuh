@@ -86,15 +86,20 @@ struct GemmParams {
 
 // Direct-store address of element (m, n) (rowc = cidx/cm row already mapped).
 __device__ __forceinline__ double* direct_addr(const GemmParams& P, int64_t rowc, int n) {
-  if (P.peers) {
-    const int64_t T = P.bc_panel, G = P.bc_world;
-    const int h = (int)((rowc / T) % G);
-    const int64_t lr = (rowc / (T * G)) * T + rowc % T;
-    const int64_t l = map_idx(P.cn, n);
-    const int64_t gc = ((l / T) * G + P.bc_rank) * T + l % T;
-    return P.peers[h] + lr * P.ldc + gc;
-  }
   return P.C + rowc * P.ldc + map_idx(P.cn, n);
+}
+
+// Peer store (fused exchange): element (m, n) of the panel GEMM is Σ[r][gc]
+// with r = c2m(m) the global row and gc the global column of this rank's
+// local row l = c2n(n); it goes to the owner of row r (block-cyclic panels).
+__device__ __forceinline__ void peer_store(const GemmParams& P, int m, int n, double v) {
+  const int64_t r = map_idx(P.c2m, m);
+  const int64_t T = P.bc_panel, G = P.bc_world;
+  const int h = (int)((r / T) % G);
+  const int64_t lr = (r / (T * G)) * T + r % T;
+  const int64_t l = map_idx(P.c2n, n);
+  const int64_t gc = ((l / T) * G + P.bc_rank) * T + l % T;
+  P.peers[h][lr * P.ldc2 + gc] = v;
 }
 
 template <int BK>
@@ -317,6 +322,7 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
           if (P.beta != 0.0) v += P.beta * P.D[rowd * P.ldd + map_idx(P.dn, n)];
           if (P.direct) *direct_addr(P, rowc, n) = v;
           if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + mcol2] = v;
+          if (P.peers) peer_store(P, m, n, v);
         }
       }
     }
@@ -393,6 +399,7 @@ __global__ void splitk_reduce_kernel(const GemmParams P) {
     if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + map_idx(P.dn, n)];
     if (P.direct) *direct_addr(P, rowc, n) = v;
     if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + map_idx(P.c2m, m)] = v;
+    if (P.peers) peer_store(P, m, n, v);
   }
 }
 

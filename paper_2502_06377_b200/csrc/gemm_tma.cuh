@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
           if (P.beta != 0.0) v += P.beta * P.D[rowd * P.ldd + map_idx(P.dn, n)];
           if (P.direct) *direct_addr(P, rowc, n) = v;
           if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + mcol2] = v;
+          if (P.peers) peer_store(P, m, n, v);
         }
       }
     }

@@ -424,30 +424,45 @@ class ShardedSolver:
 
     # ------------------------------------------------------------ one block update
     def block_update(self, k: int):
-        torch, be, pl = self.torch, self.be, self.plan[k]
+        """One block step (solver.py:122-129) on the row panels.
+
+        K1 (panel GEMM) writes Mbuf = −M (local columns), mirrors −Mᵀ into the
+        local panel and — in the fused ``p2p`` mode — also stores −M straight
+        into the owners' panels over NVLink.  K2 sums lower-triangle partials
+        of M·Wᵀ (their sum is the lower triangle of the symmetric total)."""
+        be, pl = self.be, self.plan[k]
         lo, hi, b, a0, a1, n_cl = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"], pl["n_cl"]
         p = self.p
-        segs = [(0, 0, lo), (hi, hi, p - hi)]
-        if self.exchange == "p2p":
-            return self._block_update_p2p(k)
-        Mbuf = be.zeros(b, max(n_cl, 1))
+        p2p = self.exchange == "p2p"
+        Mbuf = self._mbuf(b, n_cl)
         if n_cl > 0:
-            # 1. Mbuf = −W Σ[c_own, c]ᵀ ; mirror: Σ_loc[c_own row][lo + m] = −M
-            be.gemm(GemmSpec(x=self.W[k], xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl, segs=segs,
-                             c=Mbuf, cm=0, cn=0, mirror=True, c2=self.S, c2m=lo, c2n=(a0, 0, a1),
-                             alpha=-1.0, tma_safe=True, xrows=b, xcols=p, yrows=self.n_loc, ycols=p))
-        # 2. partial top = −Mbuf · W[:, c_own]ᵀ (local columns), all-reduce
-        top = be.zeros(b, b)
+            spec = GemmSpec(x=self.W[k], xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl,
+                            segs=[(0, 0, lo), (hi, hi, p - hi)], c=Mbuf, cm=0, cn=0, mirror=True, c2=self.S,
+                            c2m=lo, c2n=(a0, 0, a1), alpha=-1.0, tma_safe=True, xrows=b, xcols=p,
+                            yrows=self.n_loc, ycols=p)
+            if p2p:
+                spec.peers, spec.bc_panel, spec.bc_world, spec.bc_rank = (self.peers, self.layout.panel,
+                                                                          self.world, self.rank)
+            be.gemm(spec)
+        top = self._top(b)
+        top.zero_()
         if n_cl > 0:
             be.gemm(GemmSpec(x=Mbuf, xm=0, y=self._w_loc(k), yn=0, m=b, n=b,
-                             segs=[(0, 0, a0), (a0, a1, self.n_loc - a1)], c=top, alpha=-1.0,
+                             segs=[(0, 0, a0), (a0, a1, self.n_loc - a1)], c=top, alpha=-1.0, lower=True,
                              tma_safe=(a0 % 16 == 0), xrows=b, xcols=n_cl, yrows=b, ycols=self.n_loc))
-        self.comm.all_reduce(top)
+        self.comm.all_reduce(top)     # in p2p mode also the barrier after which the peer stores have landed
         if a1 > a0:
-            t = self.ainv[k] + top
             rel = pl["my_rows_rel"]
-            self.S[a0:a1, lo:hi] = 0.5 * (t.index_select(0, rel) + t.t().index_select(0, rel))
-        # 3. exchange: rows of −M for the owners of I
+            # Σ_II rows = ainv + (lower sum mirrored); the diagonal appears in both halves once
+            t = self.ainv[k].index_select(0, rel) + top.index_select(0, rel) + top.t().index_select(0, rel)
+            ar = self.torch.arange(a1 - a0, device=top.device)
+            t[ar, rel] -= top[rel, rel]
+            self.S[a0:a1, lo:hi] = t
+        if p2p:
+            # with overlapping sets the next step's peer stores hit rows of I_k ∩ I_{k+1}
+            # that the Σ_II write above also touches: every rank must finish it first
+            self.comm.barrier()
+            return
         if self.world > 1:
             send = Mbuf[:, :n_cl].index_select(0, pl["send_perm"]).contiguous().reshape(-1)
             in_splits = [pl["n_I"][h] * n_cl for h in range(self.world)]
@@ -464,35 +479,20 @@ class ShardedSolver:
                     rows.index_copy_(1, pl["cols_c"][h], blk)
                 off += n
         elif a1 > a0 and n_cl > 0:
-            # single rank: the owner rows are all of I
             self.S[a0:a1].index_copy_(1, pl["cols_c"][0], Mbuf[:, :n_cl])
 
-    def _block_update_p2p(self, k: int):
-        """Fused exchange: the panel GEMM's epilogue stores −M rows straight into
-        the owners' Σ panels over NVLink (peer pointers), and mirrors −Mᵀ into the
-        local panel, from which the Σ_II partial is read back (no all_to_all)."""
-        be, pl = self.be, self.plan[k]
-        lo, hi, b, a0, a1, n_cl = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"], pl["n_cl"]
-        p = self.p
-        if n_cl > 0:
-            be.gemm(GemmSpec(x=self.W[k], xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl,
-                             segs=[(0, 0, lo), (hi, hi, p - hi)], c=self.S, cm=lo, cn=(a0, 0, a1),
-                             mirror=True, c2=self.S, c2m=lo, c2n=(a0, 0, a1), alpha=-1.0, tma_safe=True,
-                             xrows=b, xcols=p, yrows=self.n_loc, ycols=p, peers=self.peers,
-                             bc_panel=self.layout.panel, bc_world=self.world, bc_rank=self.rank))
-        top = be.zeros(b, b)
-        if n_cl > 0:
-            # top = −(−M)·W_cᵀ with −M read from the mirrored local panel Σ[c_own, I]
-            be.gemm_xt(x=self.S, x_col0=lo, y=self._w_loc(k), m=b, n=b,
-                       segs=[(0, 0, a0), (a1, a1, self.n_loc - a1)], c=top, alpha=-1.0)
-        self.comm.all_reduce(top)     # also the barrier after which the peers' stores have landed
-        if a1 > a0:
-            t = self.ainv[k] + top
-            rel = pl["my_rows_rel"]
-            self.S[a0:a1, lo:hi] = 0.5 * (t.index_select(0, rel) + t.t().index_select(0, rel))
-        # With overlapping sets the next step's peer stores hit rows of I_k ∩ I_{k+1}
-        # that this Σ_II write also touches: every rank must finish it first.
-        self.comm.barrier()
+    def _mbuf(self, b, n_cl):
+        buf = getattr(self, "_mb", None)
+        need = b * max(n_cl, 1)
+        if buf is None or buf.numel() < need:
+            self._mb = buf = self.be.zeros(need)
+        return buf[:need].view(b, max(n_cl, 1))
+
+    def _top(self, b):
+        buf = getattr(self, "_tb", None)
+        if buf is None or buf.numel() < b * b:
+            self._tb = buf = self.be.zeros(b * b)
+        return buf[: b * b].view(b, b)
 
     # ------------------------------------------------------------ estimate
     def error_estimate(self, k: int, rtol: float = 1e-9, max_iters: int = 5000):
