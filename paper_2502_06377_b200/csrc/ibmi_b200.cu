@@ -869,24 +869,6 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
   return IBMI_OK;
 }
 
-int alloc_norm_bufs(NormBufs& nb, int64_t b, int64_t cc, int blocks, int threads, size_t smem_cap) {
-  const int64_t n = std::min(b, cc);
-  nb.ldG = round_up(n, 32);
-  nb.G = nb.vec = nb.part = nb.out = nullptr;
-  nb.blocks = blocks; nb.threads = threads; nb.smem_cap = smem_cap;
-  nb.ws = nullptr; nb.ws_cap = 0; nb.sms = 148;
-  CUDA_TRY(cudaMalloc(&nb.G, (size_t)n * nb.ldG * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&nb.vec, (size_t)2 * std::max(b, cc) * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&nb.part, (size_t)4 * blocks * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&nb.out, 4 * sizeof(double)));
-  return IBMI_OK;
-}
-
-void free_norm_bufs(NormBufs& nb) {
-  for (double* q : {nb.G, nb.vec, nb.part, nb.out})
-    if (q) cudaFree(q);
-}
-
 void power_launch_shape(int device, int* blocks, int* threads, size_t* smem_cap) {
   int sms = 148, maxb = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1562,6 +1544,163 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
   if (iters) *iters = (int)nc.host[2];
   return IBMI_OK;
 }
+
+static RowMap to_map(const ibmi_map& m) {
+  RowMap r;
+  r.split = (m.split < 0 || m.split > INT_MAX) ? INT_MAX : (int)m.split;
+  r.off0 = m.off0;
+  r.off1 = m.off1;
+  r.idx = m.idx;
+  return r;
+}
+
+static int desc_to_op(const ibmi_gemm_desc* d, GemmOp& op) {
+  if (!d) return fail(IBMI_ERR_INVALID, "null descriptor");
+  if (d->m < 0 || d->n < 0 || d->m > INT_MAX || d->n > INT_MAX) return fail(IBMI_ERR_DIM, "bad m/n");
+  if (d->nseg < 0 || d->nseg > 2) return fail(IBMI_ERR_INVALID, "nseg must be 0, 1 or 2");
+  if (!d->x || !d->y) return fail(IBMI_ERR_INVALID, "null operand");
+  if (!d->frob_out && !d->c && d->direct) return fail(IBMI_ERR_INVALID, "null output");
+  if (d->lower && d->m != d->n) return fail(IBMI_ERR_DIM, "lower requires m == n");
+  op.X = d->x; op.ldx = d->ldx; op.xm = to_map(d->xm);
+  op.Y = d->y; op.ldy = d->ldy; op.yn = to_map(d->yn);
+  op.M = d->m; op.N = d->n;
+  for (int i = 0; i < d->nseg; ++i) {
+    if (d->seg_len[i] < 0 || d->seg_len[i] > INT_MAX) return fail(IBMI_ERR_DIM, "bad segment length");
+    op.add_seg(d->seg_x0[i], d->seg_y0[i], d->seg_len[i]);
+  }
+  op.C = d->c; op.ldc = d->ldc; op.cm = to_map(d->cm); op.cn = to_map(d->cn);
+  op.cidx = d->cidx; op.direct = d->direct != 0;
+  if (d->mirror) {
+    op.mirror = true;
+    if (d->c2) { op.c2_set = true; op.C2 = d->c2; op.ldc2 = d->ldc2; op.c2m = to_map(d->c2m); op.c2n = to_map(d->c2n); }
+  }
+  op.alpha = d->alpha; op.beta = d->beta;
+  op.D = d->d; op.ldd = d->ldd; op.dm = to_map(d->dm); op.dn = to_map(d->dn);
+  op.lower = d->lower != 0;
+  op.tma_ok = d->tma_safe != 0;
+  op.xrows = d->xrows; op.xcols = d->xcols; op.yrows = d->yrows; op.ycols = d->ycols;
+  op.splits = d->splits > 1 ? d->splits : 1;
+  op.xt = d->xt != 0;
+  op.yt = d->yt != 0;
+  if ((op.xt && (op.xm.idx || op.xm.split != INT_MAX)) || (op.yt && (op.yn.idx || op.yn.split != INT_MAX)))
+    return fail(IBMI_ERR_INVALID, "transposed operands take contiguous maps only");
+  if (op.xt || op.yt) { op.tma_ok = false; op.splits = 1; }
+  if (d->peers) {
+    if (d->bc_panel < 1 || d->bc_world < 1 || d->bc_rank < 0 || d->bc_rank >= d->bc_world || op.cidx)
+      return fail(IBMI_ERR_INVALID, "bad peer-store layout");
+    op.peers = d->peers; op.bc_panel = d->bc_panel; op.bc_world = d->bc_world; op.bc_rank = d->bc_rank;
+    op.splits = 1;
+  }
+  return IBMI_OK;
+}
+
+int ibmi_gemm_workspace(const ibmi_gemm_desc* d, int64_t* doubles) {
+  GemmOp op;
+  int rc = desc_to_op(d, op);
+  if (rc) return rc;
+  const int64_t tiles = gemm_tiles(op);
+  int64_t need = 0;
+  if (d->frob_out) need = tiles;
+  else if (op.splits > 1) need = tiles * op.splits * GB_M * GB_N;
+  if (doubles) *doubles = need;
+  return IBMI_OK;
+}
+
+int ibmi_gemm(const ibmi_gemm_desc* d, void* stream) {
+  GemmOp op;
+  int rc = desc_to_op(d, op);
+  if (rc) return rc;
+  int64_t need = 0;
+  ibmi_gemm_workspace(d, &need);
+  if (need > 0 && (!d->ws || d->ws_len < need)) return fail(IBMI_ERR_INVALID, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d->frob_out) {
+    op.partial = d->ws;
+    CUDA_TRY(launch_gemm(op, st));
+    reduce_partials_kernel<<<1, 1024, 0, st>>>(d->ws, (int)need, d->frob_out);
+    CUDA_TRY(cudaGetLastError());
+    return IBMI_OK;
+  }
+  if (op.splits > 1) op.ws = d->ws;
+  CUDA_TRY(launch_gemm(op, st));
+  return IBMI_OK;
+}
+
+int ibmi_export(ibmi_ctx* c, int which, int k, double** ptr, int64_t* rows, int64_t* cols, int64_t* ld) {
+  if (!c || !ptr) return fail(IBMI_ERR_INVALID, "null argument");
+  if (which == 0) { *ptr = c->A; if (rows) *rows = c->p; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK; }
+  if (which == 1) {
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (int rc = ensure_sigma(c)) return rc;
+    *ptr = c->S; if (rows) *rows = c->p; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK;
+  }
+  if (k < 0 || k >= (int)c->sets.size()) return fail(IBMI_ERR_INVALID, "set index out of range");
+  const SetDev& s = c->sets[k];
+  if (!s.ready) return fail(IBMI_ERR_STATE, "set not set up");
+  if (which == 2) { *ptr = s.W; if (rows) *rows = s.b; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK; }
+  if (which == 3) { *ptr = s.ainv; if (rows) *rows = s.b; if (cols) *cols = s.b; if (ld) *ld = s.ldb; return IBMI_OK; }
+  return fail(IBMI_ERR_INVALID, "unknown buffer");
+}
+
+int ibmi_device_alloc(int device, int64_t bytes, void** ptr) {
+  if (!ptr || bytes < 0) return fail(IBMI_ERR_INVALID, "bad argument");
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaMalloc(ptr, bytes > 0 ? bytes : 8));
+  CUDA_TRY(cudaMemset(*ptr, 0, bytes > 0 ? bytes : 8));
+  return IBMI_OK;
+}
+
+int ibmi_device_free(void* ptr) {
+  if (ptr) CUDA_TRY(cudaFree(ptr));
+  return IBMI_OK;
+}
+
+int ibmi_ipc_handle(void* ptr, void* handle) {
+  if (!ptr || !handle) return fail(IBMI_ERR_INVALID, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, ptr));
+  memcpy(handle, &h, sizeof(h));
+  return IBMI_OK;
+}
+
+int ibmi_ipc_open(int device, const void* handle, void** ptr) {
+  if (!ptr || !handle) return fail(IBMI_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return IBMI_OK;
+}
+
+int ibmi_ipc_close(void* ptr) {
+  if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return IBMI_OK;
+}
+
+int ibmi_tune(int key, int value) {
+  switch (key) {
+    case 0:
+      if (value < 0 || value > 2) return fail(IBMI_ERR_INVALID, "gemm variant must be 0, 1 or 2");
+      g_variant = value;
+      break;
+    case 1:
+      if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
+      g_split_diag = value;
+      break;
+    case 2:
+      if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
+      g_split_gram = value;
+      break;
+    case 3:
+      g_use_tma = value ? 1 : 0;
+      break;
+    default:
+      return fail(IBMI_ERR_INVALID, "unknown tuning key");
+  }
+  ++g_tune_gen;
+  return IBMI_OK;
+}
+
 
 int ibmi_mc_guess(int64_t p, const double* a, int64_t lda, const double* w, int64_t n, const int64_t* comp,
                   int64_t c, double* out, int64_t ldo, void* stream) {

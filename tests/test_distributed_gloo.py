@@ -66,7 +66,19 @@ def test_sharded_matches_oracle(world, case):
     procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    res = [q.get(timeout=120) for _ in range(world)]
+    import queue
+    import time as _time
+
+    res, deadline = [], _time.time() + 240
+    while len(res) < len(procs):
+        try:
+            res.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [pr.exitcode for pr in procs if pr.exitcode not in (None, 0)]
+            if dead or _time.time() > deadline:
+                for pr in procs:
+                    pr.kill()
+                raise AssertionError(f"worker failed (exit codes {[pr.exitcode for pr in procs]})")
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
