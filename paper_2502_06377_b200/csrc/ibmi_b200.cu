@@ -334,13 +334,16 @@ PinnedPool g_pool;
 constexpr size_t STAGE_SLOT = 16u << 20;   // 16 MiB per slot, 2 slots per thread
 
 int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t rows, int64_t cols, bool to_device,
-                int device) {
+                int device, cudaStream_t stream) {
   const size_t row_bytes = (size_t)cols * 8;
   const size_t total = row_bytes * (size_t)rows;
   if (total < (64u << 20) || row_bytes > STAGE_SLOT) {
-    CUDA_TRY(cudaMemcpy2D(to_device ? (void*)dev : (void*)host, (to_device ? ldd : ldh) * 8,
-                          to_device ? (const void*)host : (const void*)dev, (to_device ? ldh : ldd) * 8, row_bytes,
-                          rows, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
+    // async on the caller's stream + sync: a pageable cudaMemcpy may return
+    // before its DMA lands, and the context stream does not wait for stream 0
+    CUDA_TRY(cudaMemcpy2DAsync(to_device ? (void*)dev : (void*)host, (to_device ? ldd : ldh) * 8,
+                               to_device ? (const void*)host : (const void*)dev, (to_device ? ldh : ldd) * 8,
+                               row_bytes, rows, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
     return IBMI_OK;
   }
   const int64_t chunk_rows = std::max<int64_t>(1, (int64_t)(STAGE_SLOT / row_bytes));
@@ -1007,7 +1010,7 @@ int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
                                cudaMemcpyDeviceToDevice, c->stream));
   } else {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    int rc = staged_copy(c->A, c->ld, const_cast<double*>(a), lda, p, p, true, c->device);
+    int rc = staged_copy(c->A, c->ld, const_cast<double*>(a), lda, p, p, true, c->device, c->stream);
     if (rc) return rc;
   }
   c->a_set = true;
@@ -1082,11 +1085,13 @@ int ibmi_set_partition_general(ibmi_ctx* c, int k, const int64_t* set_ptr, const
     sd.b = (int)n;
     sd.ldb = round_up(n, 32);
     CUDA_TRY(cudaMalloc(&sd.idx, n * sizeof(int64_t)));
-    CUDA_TRY(cudaMemcpy(sd.idx, s, n * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpyAsync(sd.idx, s, n * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
     if (!comp.empty()) {
       CUDA_TRY(cudaMalloc(&sd.comp, comp.size() * sizeof(int64_t)));
-      CUDA_TRY(cudaMemcpy(sd.comp, comp.data(), comp.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpyAsync(sd.comp, comp.data(), comp.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                               c->stream));
     }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
   return IBMI_OK;
 }
@@ -1281,7 +1286,7 @@ int ibmi_set_sigma(ibmi_ctx* c, const double* s, int64_t lds, int on_device) {
     CUDA_TRY(cudaMemcpy2DAsync(c->S, c->ld * 8, s, lds * 8, c->p * 8, c->p, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    int rc = staged_copy(c->S, c->ld, const_cast<double*>(s), lds, c->p, c->p, true, c->device);
+    int rc = staged_copy(c->S, c->ld, const_cast<double*>(s), lds, c->p, c->p, true, c->device, c->stream);
     if (rc) return rc;
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1297,7 +1302,7 @@ int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
     CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, c->S, c->ld * 8, c->p * 8, c->p, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    int rc = staged_copy(c->S, c->ld, out, ldo, c->p, c->p, false, c->device);
+    int rc = staged_copy(c->S, c->ld, out, ldo, c->p, c->p, false, c->device, c->stream);
     if (rc) return rc;
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1709,7 +1714,7 @@ int ibmi_mc_guess(int64_t p, const double* a, int64_t lda, const double* w, int6
   cudaStream_t st = (cudaStream_t)stream;
   int64_t* dcomp = nullptr;
   CUDA_TRY(cudaMalloc(&dcomp, c * sizeof(int64_t)));
-  CUDA_TRY(cudaMemcpy(dcomp, comp, c * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpyAsync(dcomp, comp, c * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   int rc = mc_guess_into(a, lda, p, w, 0, n, list_map(dcomp), c, out, ldo, contig_map(0), contig_map(0), st);
   cudaFree(dcomp);
   return rc;
