@@ -304,7 +304,10 @@ def run_ours(args):
         n_to_tol = 0
         for n_to_tol in range(1, cfg.max_iterations + 1):
             e, _, _ = solver.sweep(1e-9, 5000)
-            fr = solver.frobenius() if cfg.stopping == "frobenius" else None
+            # exact skip: ‖I − AΣ‖_F ≥ err, so the residual is needed only once err < tol
+            fr = solver.frobenius() if cfg.stopping == "frobenius" and e < 1.01 * cfg.tol else None
+            if cfg.stopping == "frobenius" and fr is None:
+                continue
             if (fr < cfg.tol) if fr is not None else (e <= cfg.tol):
                 break
         torch.cuda.synchronize()

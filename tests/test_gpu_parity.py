@@ -280,7 +280,13 @@ def test_c2_full_solve_frobenius_stop():
     cfg = configs.get_config("c2")
     a = configs.make_matrix("c2")
     rep = pkg.solve(a, cfg.partition(), pkg.IbmiConfig(tol=cfg.tol, max_iterations=cfg.max_iterations,
-                                                       initial_guess="jacobi", stopping="frobenius"))
+                                                       initial_guess="jacobi", stopping="frobenius",
+                                                       residual_every_sweep=True))
+    # the bound-based skip of the residual must stop at the same sweep
+    rep2 = pkg.solve(a, cfg.partition(), pkg.IbmiConfig(tol=cfg.tol, max_iterations=cfg.max_iterations,
+                                                        initial_guess="jacobi", stopping="frobenius"))
+    assert rep2.iterations == rep.iterations
+    assert np.array_equal(rep2.result, rep.result)
     ref_fro = g["frobenius_trace"]
     n = min(len(rep.residual_trace), len(ref_fro))
     fr = np.asarray(rep.residual_trace[:n])
