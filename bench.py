@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1 (diagnostic)")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance run")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"])
     return ap.parse_args()
 
@@ -297,7 +298,7 @@ def run_ours(args):
         panel_tf = panel_flops / (kt["panel_gemm"] * 1e-3) / 1e12
     # time to tolerance from a fresh Σ0 (setup included), same solver state machine
     ttt = None
-    if world == 1 and not args.sharded:
+    if world == 1 and not args.sharded and not args.no_ttt:
         solver.init_sigma(1 if guess == "jacobi" else 0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
