@@ -37,7 +37,8 @@ typedef enum {
   IBMI_ERR_CUDA = 6,           /* CUDA runtime failure              -> DeviceError           */
   IBMI_ERR_OOM = 7,            /* device allocation failed          -> OutOfMemoryBudget     */
   IBMI_ERR_STATE = 8,          /* call out of order (e.g. sweep before setup)                */
-  IBMI_ERR_UNSUPPORTED = 9     /* not implemented on this path                               */
+  IBMI_ERR_UNSUPPORTED = 9,    /* not implemented on this path                               */
+  IBMI_ERR_IO = 10             /* file unreadable / malformed       -> IoError               */
 } ibmi_status;
 
 typedef enum {
@@ -66,6 +67,13 @@ int ibmi_destroy(ibmi_ctx* ctx);
  * whole matrix with the reference's tolerance (linalg.py:68-77).
  * Replaces np.asarray(a, float64) at solver.py:234. */
 int ibmi_set_matrix(ibmi_ctx* ctx, const double* a, int64_t lda, int on_device);
+
+/* A straight from an IBMI1 file (reference matio.py:3-47 layout) into HBM:
+ * parallel pread into pinned slots, async copies; same checks as set_matrix.
+ * Replaces matio.load_matrix (matio.py:74-77) on the `invert` path (cli.py:146). */
+int ibmi_load_ibmi1(ibmi_ctx* ctx, const char* path);
+/* Σ from HBM straight to an IBMI1 file (replaces matio.save_matrix, cli.py:150). */
+int ibmi_save_sigma_ibmi1(ibmi_ctx* ctx, const char* path);
 
 /* K contiguous sets [lo[j], hi[j]); complement of set j is [0,lo) ∪ [hi,p).
  * Replaces the comps/ops construction at solver.py:241-242 (the index

@@ -13,12 +13,14 @@ import threading
 
 import numpy as np
 
-from .exceptions import DeviceError, DimensionMismatch, IndexOutOfRange, NotPositiveDefinite, OutOfMemoryBudget
+from .exceptions import (DeviceError, DimensionMismatch, IndexOutOfRange, IoError, NotPositiveDefinite,
+                         OutOfMemoryBudget)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libibmi_b200.so")
 
-OK, ERR_INVALID, ERR_DIM, ERR_INDEX, ERR_NOT_SPD, ERR_NOT_SYMMETRIC, ERR_CUDA, ERR_OOM, ERR_STATE, ERR_UNSUPPORTED = range(10)
+(OK, ERR_INVALID, ERR_DIM, ERR_INDEX, ERR_NOT_SPD, ERR_NOT_SYMMETRIC, ERR_CUDA, ERR_OOM, ERR_STATE, ERR_UNSUPPORTED,
+ ERR_IO) = range(11)
 GUESS_IDENTITY, GUESS_JACOBI, GUESS_MATRIX, GUESS_LOCAL, GUESS_MC, GUESS_TAKAHASHI = range(6)
 
 # (name, restype, argtypes) — the full exported surface of include/ibmi_b200.h
@@ -31,6 +33,8 @@ SIGNATURES = [
     ("ibmi_create", C.c_int, [C.POINTER(_P), C.c_int, _I64, _P]),
     ("ibmi_destroy", C.c_int, [_P]),
     ("ibmi_set_matrix", C.c_int, [_P, _P, _I64, C.c_int]),
+    ("ibmi_load_ibmi1", C.c_int, [_P, C.c_char_p]),
+    ("ibmi_save_sigma_ibmi1", C.c_int, [_P, C.c_char_p]),
     ("ibmi_set_partition", C.c_int, [_P, C.c_int, C.POINTER(_I64), C.POINTER(_I64)]),
     ("ibmi_set_partition_general", C.c_int, [_P, C.c_int, C.POINTER(_I64), C.POINTER(_I64)]),
     ("ibmi_setup", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(_I64)]),
@@ -113,6 +117,8 @@ def check(rc: int, what: str = "", *, fail_set: int | None = None, fail_pivot: i
         raise OutOfMemoryBudget(msg)
     if rc == ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == ERR_IO:
+        raise IoError(msg)
     raise DeviceError(msg)
 
 

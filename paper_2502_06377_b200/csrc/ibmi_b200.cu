@@ -11,6 +11,8 @@
 //   B        b_K × ldc     estimate matrix Σ_II A_Ic + Σ_Ic A_cc (solver.py:154)
 //   G        n × n         its Gram matrix (B·Bᵀ or Bᵀ·B, whichever is smaller)
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <unistd.h>
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -408,6 +410,74 @@ int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t row
   for (auto& x : th) x.join();
   for (int t = 0; t < nthreads; ++t)
     if (rc[t]) return fail(rc[t], "staged copy: " + msg[t]);
+  return IBMI_OK;
+}
+
+// ------------------------------------------------------ IBMI1 files <-> HBM
+// IBMI1 (reference matio.py:3-47): 8-byte magic "IBMI1\0\0\0", rows and cols as
+// u64 LE, then rows*cols f64 LE row-major.  Rows stream between the file and
+// device memory through the pinned slots, several threads doing pread/pwrite.
+const char kMagic[8] = {'I', 'B', 'M', 'I', '1', 0, 0, 0};
+
+int staged_file(double* dev, int64_t ldd, int fd, int64_t base, int64_t rows, int64_t cols, bool to_device,
+                int device) {
+  const size_t row_bytes = (size_t)cols * 8;
+  const int64_t chunk_rows = std::max<int64_t>(1, (int64_t)(STAGE_SLOT / std::max<size_t>(row_bytes, 1)));
+  if (row_bytes > STAGE_SLOT) return fail(IBMI_ERR_UNSUPPORTED, "row larger than a staging slot");
+  const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
+  unsigned hc = std::thread::hardware_concurrency();
+  const int nthreads = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, std::max(1u, std::min(8u, hc ? hc : 1u))));
+  std::lock_guard<std::mutex> lock(g_pool.mu);
+  while ((int)g_pool.slots.size() < 2 * nthreads) {
+    void* p = nullptr;
+    CUDA_TRY(cudaMallocHost(&p, STAGE_SLOT));
+    g_pool.slots.push_back(p);
+  }
+  std::vector<int> rc(nthreads, IBMI_OK);
+  std::vector<std::string> msg(nthreads);
+  auto work = [&](int t) {
+    cudaSetDevice(device);
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc[t] = IBMI_ERR_CUDA; return; }
+    char* slot = (char*)g_pool.slots[2 * t];
+    for (int64_t c = t; c < nchunks && rc[t] == IBMI_OK; c += nthreads) {
+      const int64_t r0 = c * chunk_rows, n = std::min(chunk_rows, rows - r0);
+      const size_t bytes = (size_t)n * row_bytes;
+      const off_t off = (off_t)(base + (int64_t)r0 * (int64_t)row_bytes);
+      if (to_device) {
+        size_t got = 0;
+        while (got < bytes) {
+          ssize_t k = pread(fd, slot + got, bytes - got, off + (off_t)got);
+          if (k <= 0) { rc[t] = IBMI_ERR_IO; msg[t] = "short read"; break; }
+          got += (size_t)k;
+        }
+        if (rc[t]) break;
+        if (cudaMemcpy2DAsync(dev + r0 * ldd, ldd * 8, slot, row_bytes, row_bytes, n, cudaMemcpyHostToDevice, st) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+          rc[t] = IBMI_ERR_CUDA; msg[t] = "copy"; break;
+        }
+      } else {
+        if (cudaMemcpy2DAsync(slot, row_bytes, dev + r0 * ldd, ldd * 8, row_bytes, n, cudaMemcpyDeviceToHost, st) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+          rc[t] = IBMI_ERR_CUDA; msg[t] = "copy"; break;
+        }
+        size_t put = 0;
+        while (put < bytes) {
+          ssize_t k = pwrite(fd, slot + put, bytes - put, off + (off_t)put);
+          if (k <= 0) { rc[t] = IBMI_ERR_IO; msg[t] = "short write"; break; }
+          put += (size_t)k;
+        }
+      }
+    }
+    cudaStreamDestroy(st);
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t) th.emplace_back(work, t);
+  for (auto& x : th) x.join();
+  for (int t = 0; t < nthreads; ++t)
+    if (rc[t]) return fail(rc[t], "IBMI1 transfer: " + msg[t]);
   return IBMI_OK;
 }
 
@@ -1680,6 +1750,58 @@ int ibmi_ipc_open(int device, const void* handle, void** ptr) {
 int ibmi_ipc_close(void* ptr) {
   if (ptr) CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return IBMI_OK;
+}
+
+int ibmi_load_ibmi1(ibmi_ctx* c, const char* path) {
+  if (!c || !path) return fail(IBMI_ERR_INVALID, "null argument");
+  int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(IBMI_ERR_IO, std::string(path) + ": cannot open");
+  char magic[8];
+  uint64_t hdr[2] = {0, 0};
+  if (pread(fd, magic, 8, 0) != 8 || memcmp(magic, kMagic, 8) != 0) {
+    close(fd);
+    return fail(IBMI_ERR_IO, std::string(path) + ": bad magic, expected IBMI1");
+  }
+  if (pread(fd, hdr, 16, 8) != 16) { close(fd); return fail(IBMI_ERR_IO, std::string(path) + ": truncated header"); }
+  const off_t size = lseek(fd, 0, SEEK_END);
+  if ((int64_t)hdr[0] != c->p || (int64_t)hdr[1] != c->p) {
+    close(fd);
+    return fail(IBMI_ERR_DIM, std::string(path) + ": matrix is " + std::to_string(hdr[0]) + "x" +
+                                  std::to_string(hdr[1]) + ", context expects " + std::to_string(c->p));
+  }
+  if ((int64_t)size - 24 != (int64_t)(hdr[0] * hdr[1] * 8)) {
+    close(fd);
+    return fail(IBMI_ERR_IO, std::string(path) + ": payload size does not match the header");
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemsetAsync(c->A, 0, (size_t)c->p * c->ld * sizeof(double), c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  int rc = staged_file(c->A, c->ld, fd, 24, c->p, c->p, true, c->device);
+  close(fd);
+  if (rc) return rc;
+  c->a_set = true;
+  for (auto& s : c->sets) s.ready = false;
+  invalidate_graph(c);
+  rc = symcheck(c, contig_map(0), c->p, "matrix");
+  if (rc) { c->a_set = false; return rc; }
+  return IBMI_OK;
+}
+
+int ibmi_save_sigma_ibmi1(ibmi_ctx* c, const char* path) {
+  if (!c || !path) return fail(IBMI_ERR_INVALID, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (int rc = ensure_sigma(c)) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  int fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0) return fail(IBMI_ERR_IO, std::string(path) + ": cannot create");
+  uint64_t hdr[2] = {(uint64_t)c->p, (uint64_t)c->p};
+  if (pwrite(fd, kMagic, 8, 0) != 8 || pwrite(fd, hdr, 16, 8) != 16) {
+    close(fd);
+    return fail(IBMI_ERR_IO, std::string(path) + ": write failed");
+  }
+  int rc = staged_file(c->S, c->ld, fd, 24, c->p, c->p, false, c->device);
+  if (close(fd) != 0 && !rc) rc = fail(IBMI_ERR_IO, std::string(path) + ": close failed");
+  return rc;
 }
 
 int ibmi_tune(int key, int value) {

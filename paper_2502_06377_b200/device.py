@@ -26,6 +26,14 @@ def restart_vector(n: int) -> np.ndarray:
     return np.ascontiguousarray(v / np.linalg.norm(v))
 
 
+class _FileMatrix:
+    """Marker: A comes from an IBMI1 file (read by the library, not by Python)."""
+
+    def __init__(self, path, p):
+        self.path, self.p = str(path), int(p)
+        self.shape = (self.p, self.p)
+
+
 def _is_cuda_tensor(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda", False))
 
@@ -37,6 +45,19 @@ class DeviceSolver:
     torch tensor (copied device→device).  ``ranges`` is a list of ``(lo, hi)``
     runs, or pass ``partition=`` to derive them (and a relabelling if needed).
     """
+
+    @classmethod
+    def from_ibmi1(cls, path: str, partition: Partition, *, device: int = 0, stream: int | None = None):
+        """Load A from an IBMI1 file straight into HBM (no host copy).  Only
+        partitions that need no relabelling (runs or index lists) qualify."""
+        from .matio import read_header
+
+        rows, cols = read_header(path)
+        if rows != cols or rows != partition.p:
+            from .exceptions import DimensionMismatch
+
+            raise DimensionMismatch(f"matrix shape ({rows}, {cols}) does not match partition over {partition.p}")
+        return cls(_FileMatrix(path, rows), partition=partition, device=device, stream=stream)
 
     def __init__(self, a, ranges=None, *, partition: Partition | None = None, device: int = 0,
                  stream: int | None = None, perm: np.ndarray | None = None):
@@ -61,7 +82,12 @@ class DeviceSolver:
         self.ranges = [(int(lo), int(hi)) for lo, hi in ranges]
         self.sizes = [len(s) for s in self.general] if self.general else [hi - lo for lo, hi in self.ranges]
         on_dev = _is_cuda_tensor(a)
-        if on_dev:
+        from_file = isinstance(a, _FileMatrix)
+        if from_file:
+            if self.perm is not None:
+                raise NotImplementedError("relabelled partitions need A in memory; load it with matio.load_matrix")
+            p, lda = a.p, a.p
+        elif on_dev:
             import torch
 
             if a.dtype != torch.float64:
@@ -84,7 +110,10 @@ class DeviceSolver:
         _abi.check(L.ibmi_create(C.byref(h), self.device, self.p, C.c_void_p(stream or 0)), "ibmi_create")
         self._h = h
         try:
-            _abi.check(L.ibmi_set_matrix(h, C.c_void_p(_abi.dptr(a)), lda, int(on_dev)), "set_matrix")
+            if from_file:
+                _abi.check(L.ibmi_load_ibmi1(h, a.path.encode()), "load_ibmi1")
+            else:
+                _abi.check(L.ibmi_set_matrix(h, C.c_void_p(_abi.dptr(a)), lda, int(on_dev)), "set_matrix")
             k = len(self.ranges)
             if self.general:
                 ptr = np.zeros(k + 1, dtype=np.int64)
@@ -226,6 +255,15 @@ class DeviceSolver:
         out = C.c_double()
         _abi.check(self._L.ibmi_frobenius_residual(self._h, C.byref(out)), "frobenius_residual")
         return out.value
+
+    def save_sigma_ibmi1(self, path: str):
+        """Σ from HBM straight to an IBMI1 file (original index order)."""
+        if self.perm is not None:
+            from .matio import save_ibmi
+
+            save_ibmi(path, self.sigma())
+            return
+        _abi.check(self._L.ibmi_save_sigma_ibmi1(self._h, str(path).encode()), "save_sigma_ibmi1")
 
     def device_bytes(self) -> int:
         b = C.c_int64()

@@ -16,7 +16,6 @@ Extensions (all optional, defaults reproduce the reference):
 from __future__ import annotations
 
 import os
-import sys
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -39,6 +38,7 @@ __all__ = [
     "initial_guess_monte_carlo",
     "initial_guess_takahashi",
     "make_initial_guess",
+    "run_solve",
     "solve",
 ]
 
@@ -207,59 +207,63 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
     if cfg.initial_guess not in _GUESS_KIND:
         raise NotImplementedError(f"initial guess {cfg.initial_guess!r} is not available on the B200 path yet")
 
-    prof = os.environ.get("IBMI_PROFILE") is not None
-    t_enter = time.perf_counter()
     with DeviceSolver(a, partition=part, device=device) as ds:
-        t0 = time.perf_counter()
-        if prof:
-            print(f"[ibmi] context+upload {t0 - t_enter:.3f}s", file=sys.stderr)
-        ds.setup()
-        kind = _GUESS_KIND[cfg.initial_guess]
-        if kind == _abi.GUESS_MC:
-            if ds.perm is None:
-                ds.init_sigma(kind, _mc_draws(part.p, cfg.mc_samples, cfg.mc_seed))
-            else:   # relabelled partition: draw in the original order, insert the block
-                comp0 = complement(part, 0)
-                ds.init_sigma(_abi.GUESS_MATRIX, initial_guess_monte_carlo(a, comp0, cfg.mc_samples, cfg.mc_seed))
-        else:
-            ds.init_sigma(kind)
-        setup_s = time.perf_counter() - t0
-        errs, walls, pits, resid = [], [], [], []
-        converged, it = False, 0
-        while it < cfg.max_iterations:
-            start = time.perf_counter()
-            it += 1
-            err, pit, pconv = ds.sweep(cfg.norm_rtol, cfg.norm_max_iters)
-            # ‖I − AΣ‖_F ≥ ‖(ΣA)_Ic‖_F = ‖B‖_F ≥ ‖B‖₂ ≥ err (the power iteration approaches ‖B‖₂
-            # from below), so while err ≥ tol (with a rounding margin) the residual cannot be
-            # < tol and its 2p³ evaluation is skipped without changing the stopping sweep.
-            fr = None
-            if stopping == "frobenius":
-                if getattr(cfg, "residual_every_sweep", False) or err < 1.01 * cfg.tol:
-                    fr = ds.frobenius()
-                else:
-                    fr = float("nan")
-            walls.append(time.perf_counter() - start)
-            if not pconv:
-                warnings.warn(
-                    f"two_norm: power iteration did not stabilize in {cfg.norm_max_iters} "
-                    f"iterations; returning last estimate {err:.6e}", NoConvergenceWarning, stacklevel=2)
-            errs.append(err)
-            pits.append(pit)
-            if fr is not None:
-                resid.append(fr)
-            if callback is not None:
-                callback(it, err, fr)
-            if (fr < cfg.tol) if fr is not None else (err <= cfg.tol):   # nan < tol is False
-                converged = True
-                break
-        t1 = time.perf_counter()
-        result = ds.sigma(on_device=result_on_device)
-        if prof:
-            print(f"[ibmi] setup {setup_s:.3f}s sweeps {sum(walls):.3f}s download {time.perf_counter() - t1:.3f}s",
-                  file=sys.stderr)
+        return run_solve(ds, part, cfg, a=a, result_on_device=result_on_device, callback=callback)
+
+
+def run_solve(ds: DeviceSolver, part: Partition, cfg: IbmiConfig, *, a=None, result_on_device: bool = False,
+              callback=None, fetch_result: bool = True) -> SolveReport:
+    """The sweep loop of ``solve`` (solver.py:241-278) on a prepared device state."""
+    prof = os.environ.get("IBMI_PROFILE") is not None
+    stopping = getattr(cfg, "stopping", "estimate")
+    t0 = time.perf_counter()
+    ds.setup()
+    kind = _GUESS_KIND[cfg.initial_guess]
+    if kind == _abi.GUESS_MC:
+        if ds.perm is None:
+            ds.init_sigma(kind, _mc_draws(part.p, cfg.mc_samples, cfg.mc_seed))
+        else:   # relabelled partition: draw in the original order, insert the block
+            comp0 = complement(part, 0)
+            ds.init_sigma(_abi.GUESS_MATRIX, initial_guess_monte_carlo(a, comp0, cfg.mc_samples, cfg.mc_seed))
+    else:
+        ds.init_sigma(kind)
+    setup_s = time.perf_counter() - t0
+    errs, walls, pits, resid = [], [], [], []
+    converged, it = False, 0
+    while it < cfg.max_iterations:
+        start = time.perf_counter()
+        it += 1
+        err, pit, pconv = ds.sweep(cfg.norm_rtol, cfg.norm_max_iters)
+        # ‖I − AΣ‖_F ≥ ‖(ΣA)_Ic‖_F = ‖B‖_F ≥ ‖B‖₂ ≥ err (the power iteration approaches ‖B‖₂
+        # from below), so while err ≥ tol (with a rounding margin) the residual cannot be
+        # < tol and its 2p³ evaluation is skipped without changing the stopping sweep.
+        fr = None
+        if stopping == "frobenius":
+            if getattr(cfg, "residual_every_sweep", False) or err < 1.01 * cfg.tol:
+                fr = ds.frobenius()
+            else:
+                fr = float("nan")
+        walls.append(time.perf_counter() - start)
+        if not pconv:
+            warnings.warn(
+                f"two_norm: power iteration did not stabilize in {cfg.norm_max_iters} "
+                f"iterations; returning last estimate {err:.6e}", NoConvergenceWarning, stacklevel=3)
+        errs.append(err)
+        pits.append(pit)
+        if fr is not None:
+            resid.append(fr)
+        if callback is not None:
+            callback(it, err, fr)
+        if (fr < cfg.tol) if fr is not None else (err <= cfg.tol):   # nan < tol is False
+            converged = True
+            break
+    t1 = time.perf_counter()
+    result = ds.sigma(on_device=result_on_device) if fetch_result else None
     if prof:
-        print(f"[ibmi] solve total {time.perf_counter() - t_enter:.3f}s", file=sys.stderr)
+        import sys
+
+        print(f"[ibmi] setup {setup_s:.3f}s sweeps {sum(walls):.3f}s download {time.perf_counter() - t1:.3f}s",
+              file=sys.stderr)
     return SolveReport(iterations=it, converged=converged, error_trace=errs, wall_times=walls, result=result,
                        power_iterations=pits, residual_trace=resid, setup_seconds=setup_s)
 

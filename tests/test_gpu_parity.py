@@ -430,3 +430,42 @@ def test_solve_with_guess_matches_oracle(guess, kind):
     o = orc.solve(a, part.sets, tol=1e-11, guess=guess, mc_samples=40, mc_seed=3)
     assert rep.converged and abs(rep.iterations - o["iterations"]) <= 1
     assert rel_fro(rep.result, o["result"]) < 1e-10
+
+
+def test_cli_invert_streams_ibmi1_and_matches_solve(tmp_path):
+    import json
+
+    import paper_2502_06377_b200 as pkg
+    from paper_2502_06377_b200 import matio
+    from paper_2502_06377_b200.cli import main
+
+    p = 640
+    a = random_spd(p, 41)
+    fin, fout, frep = tmp_path / "a.ibmi", tmp_path / "s.ibmi", tmp_path / "r.json"
+    matio.save_ibmi(fin, a)
+    assert main(["invert", "--in", str(fin), "--out", str(fout), "--blocks", "3", "--overlap", "0.1",
+                 "--tol", "1e-11", "--report", str(frep)]) == 0
+    rep = pkg.solve(a, pkg.contiguous_partition(p, 3, 0.1), pkg.IbmiConfig(tol=1e-11))
+    s = matio.load_ibmi(fout)
+    assert np.array_equal(s, rep.result)
+    meta = json.loads(frep.read_text())
+    assert meta["iterations"] == rep.iterations and meta["converged"]
+    # red-black goes through the host (relabelled), CSV output
+    fcsv = tmp_path / "s.csv"
+    assert main(["invert", "--in", str(fin), "--out", str(fcsv), "--ordering", "red-black", "--tol", "1e-11"]) == 0
+    rb = pkg.solve(a, pkg.red_black_partition(p), pkg.IbmiConfig(tol=1e-11))
+    assert np.array_equal(matio.load_csv(fcsv), rb.result)
+
+
+def test_cli_compare(tmp_path, capsys):
+    import json
+
+    from paper_2502_06377_b200 import matio
+    from paper_2502_06377_b200.cli import main
+
+    a = random_spd(300, 42)
+    f = tmp_path / "a.ibmi"
+    matio.save_ibmi(f, a)
+    assert main(["compare", "--in", str(f), "--blocks", "2", "--tol", "1e-12"]) == 0
+    out = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert out["converged"] and out["relative_error_2norm"] < 1e-10
