@@ -520,19 +520,36 @@ int ensure_scratch(CholScratch& cs, int n) {
   return IBMI_OK;
 }
 
+// Enqueue the blocked Cholesky of cs.ws on stream s; the first failing pivot
+// lands in *info (caller initialises it to INT_MAX).  No host sync.
+int potrf_enqueue(CholScratch& cs, int n, cudaStream_t s, int* info);
+
 // Factor the n×n SPD matrix whose LOWER triangle is in cs.ws (upper zero):
 // blocked right-looking Cholesky (LAPACK dpotrf lower, linalg.py:104).
 // Returns IBMI_ERR_NOT_SPD with *pivot = first failing elimination step.
 int potrf_blocked(CholScratch& cs, int n, cudaStream_t s, int64_t* pivot) {
   const int init = INT_MAX;
   CUDA_TRY(cudaMemcpyAsync(cs.info, &init, sizeof(int), cudaMemcpyHostToDevice, s));
+  int rc = potrf_enqueue(cs, n, s, cs.info);
+  if (rc) return rc;
+  int h = INT_MAX;
+  CUDA_TRY(cudaMemcpyAsync(&h, cs.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (h != INT_MAX) {
+    *pivot = h;
+    return fail(IBMI_ERR_NOT_SPD, "non-positive pivot at elimination step " + std::to_string(h));
+  }
+  return IBMI_OK;
+}
+
+int potrf_enqueue(CholScratch& cs, int n, cudaStream_t s, int* info) {
   double* a = cs.ws;
   const int64_t ld = cs.ldw;
   for (int j0 = 0, blk = 0; j0 < n; j0 += CHOL_NB, ++blk) {
     const int jb = std::min(CHOL_NB, n - j0);
     const int j1 = j0 + jb;
     double* dblk = cs.dinv + (size_t)blk * CHOL_NB * CHOL_NB;
-    potf2_trti2_kernel<<<1, 256, 0, s>>>(a + (int64_t)j0 * ld + j0, ld, jb, dblk, CHOL_NB, cs.info, j0);
+    potf2_trti2_kernel<<<1, 256, 0, s>>>(a + (int64_t)j0 * ld + j0, ld, jb, dblk, CHOL_NB, info, j0);
     CUDA_TRY(cudaGetLastError());
     if (j1 >= n) break;
     // panel: L[j1:, j0:j1] = A[j1:, j0:j1] · L_jj⁻ᵀ   (in place, one N tile)
@@ -553,13 +570,6 @@ int potrf_blocked(CholScratch& cs, int n, cudaStream_t s, int64_t* pivot) {
     tr.alpha = -1.0; tr.beta = 1.0; tr.D = a; tr.ldd = ld; tr.dm = contig_map(j1); tr.dn = contig_map(j1);
     tr.lower = true;
     CUDA_TRY(launch_gemm(tr, s));
-  }
-  int h = INT_MAX;
-  CUDA_TRY(cudaMemcpyAsync(&h, cs.info, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
-  if (h != INT_MAX) {
-    *pivot = h;
-    return fail(IBMI_ERR_NOT_SPD, "non-positive pivot at elimination step " + std::to_string(h));
   }
   return IBMI_OK;
 }
@@ -1171,47 +1181,98 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   if (!c->a_set) return fail(IBMI_ERR_STATE, "matrix not set");
   if (c->sets.empty()) return fail(IBMI_ERR_STATE, "partition not set");
   CUDA_TRY(cudaSetDevice(c->device));
-  int rc = IBMI_OK;
   if (fail_set) *fail_set = -1;
   if (fail_pivot) *fail_pivot = -1;
   const int K = (int)c->sets.size();
   if (count < 0) count = K - first;
   if (first < 0 || first + count > K) return fail(IBMI_ERR_INVALID, "set range out of bounds");
+  if (count == 0) return IBMI_OK;
+  const int64_t p = c->p;
   cudaStream_t st = c->stream;
-  for (int k = first; k < first + count; ++k) {
-    SetDev& s = c->sets[k];
-    const int64_t b = s.b, lo = s.lo, hi = s.hi, p = c->p;
-    rc = symcheck(c, s.rows(), b, "matrix");
-    if (rc) { if (fail_set) *fail_set = k; return rc; }
+
+  // 1. symmetry of every A_II (linalg.py:68-77), one sync for all sets
+  unsigned long long* dsym = nullptr;
+  CUDA_TRY(cudaMalloc(&dsym, (size_t)2 * count * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(dsym, 0, (size_t)2 * count * sizeof(unsigned long long), st));
+  for (int j = 0; j < count; ++j) {
+    const SetDev& s = c->sets[first + j];
+    const int nt = (s.b + 31) / 32;
+    symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(c->A, c->ld, s.rows(), s.b, dsym + 2 * j);
+  }
+  std::vector<unsigned long long> hsym(2 * count);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hsym.data(), dsym, hsym.size() * 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(dsym);
+  if (e != cudaSuccess) return fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+
+  // 2. factor / invert / W for all sets, up to 8 sets in flight on their own streams
+  for (int j = 0; j < count; ++j) {
+    SetDev& s = c->sets[first + j];
     if (!s.W) {
-      CUDA_TRY(cudaMalloc(&s.W, (size_t)b * c->ld * sizeof(double)));
-      CUDA_TRY(cudaMalloc(&s.ainv, (size_t)b * s.ldb * sizeof(double)));
-      c->bytes += (size_t)b * c->ld * 8 + (size_t)b * s.ldb * 8;
+      CUDA_TRY(cudaMalloc(&s.W, (size_t)s.b * c->ld * sizeof(double)));
+      CUDA_TRY(cudaMalloc(&s.ainv, (size_t)s.b * s.ldb * sizeof(double)));
+      c->bytes += (size_t)s.b * c->ld * 8 + (size_t)s.b * s.ldb * 8;
     }
-    size_t before = c->cs.bytes;
-    rc = ensure_scratch(c->cs, (int)b);
-    if (rc) return rc;
-    c->bytes += c->cs.bytes - before;
-    // A_II (lower) -> scratch
-    copy2d_kernel<<<grid2d(b, b), 256, 0, st>>>(c->A, c->ld, s.rows(), s.rows(), c->cs.ws, c->cs.ldw,
-                                               (int)b, (int)b, 1);
-    CUDA_TRY(cudaGetLastError());
-    int64_t piv = -1;
-    rc = potrf_blocked(c->cs, (int)b, st, &piv);
-    if (rc) {
-      if (fail_set) *fail_set = k;
-      if (fail_pivot) *fail_pivot = piv;
-      return rc;
+  }
+  const int S = std::min(count, 8);
+  std::vector<cudaStream_t> ss(S, nullptr);
+  std::vector<CholScratch> scr(S);
+  std::vector<double*> gather(S, nullptr);
+  std::vector<int> infos(count, INT_MAX);
+  int* dinfo = nullptr;
+  cudaEvent_t ready = nullptr;
+  int rc = IBMI_OK;
+  auto cleanup = [&]() {
+    for (int q = 0; q < S; ++q) {
+      if (ss[q]) { cudaStreamSynchronize(ss[q]); cudaStreamDestroy(ss[q]); }
+      scr[q].release();
+      if (gather[q]) cudaFree(gather[q]);
     }
-    rc = potri_blocked(c->cs, (int)b, s.ainv, s.ldb, st);
-    if (rc) return rc;
-    // W = A_II⁻¹ A[I, c]  written at global columns, zero on I
-    CUDA_TRY(cudaMemsetAsync(s.W, 0, (size_t)b * c->ld * sizeof(double), st));
+    if (dinfo) cudaFree(dinfo);
+    if (ready) cudaEventDestroy(ready);
+  };
+#define SETUP_TRY(expr)                                                             \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess) { cleanup(); return fail(e_ == cudaErrorMemoryAllocation \
+        ? IBMI_ERR_OOM : IBMI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); } \
+  } while (0)
+  SETUP_TRY(cudaMalloc(&dinfo, (size_t)count * sizeof(int)));
+  SETUP_TRY(cudaMemcpyAsync(dinfo, infos.data(), (size_t)count * sizeof(int), cudaMemcpyHostToDevice, st));
+  SETUP_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  SETUP_TRY(cudaEventRecord(ready, st));
+  for (int q = 0; q < S; ++q) {
+    SETUP_TRY(cudaStreamCreateWithFlags(&ss[q], cudaStreamNonBlocking));
+    SETUP_TRY(cudaStreamWaitEvent(ss[q], ready, 0));
+    int bmax = 0;
+    for (int j = q; j < count; j += S) bmax = std::max(bmax, c->sets[first + j].b);
+    rc = ensure_scratch(scr[q], bmax);
+    if (rc) { cleanup(); return rc; }
+  }
+  for (int j = 0; j < count; ++j) {
+    const int q = j % S;
+    SetDev& s = c->sets[first + j];
+    cudaStream_t sq = ss[q];
+    CholScratch& cs = scr[q];
+    const int64_t b = s.b, lo = s.lo, hi = s.hi;
+    int* info = dinfo + j;
+    copy2d_kernel<<<grid2d(b, b), 256, 0, sq>>>(c->A, c->ld, s.rows(), s.rows(), cs.ws, cs.ldw, (int)b, (int)b, 1);
+    SETUP_TRY(cudaGetLastError());
+    rc = potrf_enqueue(cs, (int)b, sq, info);
+    if (!rc) rc = potri_blocked(cs, (int)b, s.ainv, s.ldb, sq);
+    if (rc) { cleanup(); return rc; }
+    SETUP_TRY(cudaMemsetAsync(s.W, 0, (size_t)b * c->ld * sizeof(double), sq));
     if (s.general) {
       // A_I = A[I, :] gathered (b × p), W = ainv · A_I (transposed-Y GEMM), then zero W[:, I]
-      double* ai = nullptr;
-      CUDA_TRY(cudaMalloc(&ai, (size_t)b * c->ld * sizeof(double)));
-      copy2d_kernel<<<grid2d(b, c->ld), 256, 0, st>>>(c->A, c->ld, s.rows(), contig_map(0), ai, c->ld, (int)b,
+      if (!gather[q]) {
+        int64_t gmax = 0;
+        for (int jj = q; jj < count; jj += S)
+          if (c->sets[first + jj].general) gmax = std::max<int64_t>(gmax, c->sets[first + jj].b);
+        SETUP_TRY(cudaMalloc(&gather[q], (size_t)gmax * c->ld * sizeof(double)));
+      }
+      double* ai = gather[q];
+      copy2d_kernel<<<grid2d(b, c->ld), 256, 0, sq>>>(c->A, c->ld, s.rows(), contig_map(0), ai, c->ld, (int)b,
                                                      (int)c->ld, 0);
       GemmOp gw;
       gw.X = s.ainv; gw.ldx = s.ldb;
@@ -1219,28 +1280,43 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
       gw.M = b; gw.N = p;
       gw.add_seg(0, 0, b);
       gw.C = s.W; gw.ldc = c->ld;
-      cudaError_t e = launch_gemm(gw, st);
-      if (e == cudaSuccess) {
-        zero_cols_kernel<<<dim3((unsigned)((b + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0, st>>>(
-            s.W, c->ld, (int)b, s.rows(), (int)b);
-        e = cudaGetLastError();
-      }
-      cudaStreamSynchronize(st);
-      cudaFree(ai);
-      if (e != cudaSuccess) return fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
-      s.ready = true;
-      continue;
+      SETUP_TRY(launch_gemm(gw, sq));
+      zero_cols_kernel<<<dim3((unsigned)((b + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0, sq>>>(
+          s.W, c->ld, (int)b, s.rows(), (int)b);
+      SETUP_TRY(cudaGetLastError());
+    } else {
+      GemmOp gw;
+      gw.X = s.ainv; gw.ldx = s.ldb;
+      gw.Y = c->A; gw.ldy = c->ld; gw.yn = complement_map(lo, hi);
+      gw.M = b; gw.N = p - b;
+      gw.add_seg(0, lo, b);
+      gw.C = s.W; gw.ldc = c->ld; gw.cn = complement_map(lo, hi);
+      SETUP_TRY(launch_gemm(gw, sq));
     }
-    GemmOp gw;
-    gw.X = s.ainv; gw.ldx = s.ldb;
-    gw.Y = c->A; gw.ldy = c->ld; gw.yn = complement_map(lo, hi);
-    gw.M = b; gw.N = p - b;
-    gw.add_seg(0, lo, b);
-    gw.C = s.W; gw.ldc = c->ld; gw.cn = complement_map(lo, hi);
-    CUDA_TRY(launch_gemm(gw, st));
-    s.ready = true;
   }
-  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int q = 0; q < S; ++q) SETUP_TRY(cudaStreamSynchronize(ss[q]));
+  SETUP_TRY(cudaMemcpy(infos.data(), dinfo, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost));
+#undef SETUP_TRY
+  cleanup();
+
+  // 3. errors in the reference's order: set by set, symmetry before the pivot
+  for (int j = 0; j < count; ++j) {
+    const double mabs = __builtin_bit_cast(double, hsym[2 * j]);
+    const double skew = __builtin_bit_cast(double, hsym[2 * j + 1]);
+    if (mabs != 0.0 && !(skew <= 1e-12 * mabs)) {
+      if (fail_set) *fail_set = first + j;
+      char buf[256];
+      snprintf(buf, sizeof(buf), "matrix is not symmetric: max |a - a.T| = %.3e exceeds 1.0e-12 * max|a| = %.3e",
+               skew, 1e-12 * mabs);
+      return fail(IBMI_ERR_NOT_SYMMETRIC, buf);
+    }
+    if (infos[j] != INT_MAX) {
+      if (fail_set) *fail_set = first + j;
+      if (fail_pivot) *fail_pivot = infos[j];
+      return fail(IBMI_ERR_NOT_SPD, "non-positive pivot at elimination step " + std::to_string(infos[j]));
+    }
+  }
+  for (int j = 0; j < count; ++j) c->sets[first + j].ready = true;
   invalidate_graph(c);
   return IBMI_OK;
 }

@@ -157,6 +157,23 @@ def pins():
     assert np.abs(orc.guess_takahashi(a, comp) - g_tk).max() <= 1e-12 * np.abs(g_tk).max()
     out["guess_mc"] = g_mc
     out["guess_takahashi"] = g_tk
+    # analysis diagnostics (analysis.py:56-188, linalg.py:277-303)
+    from ibmi import analysis as ran
+
+    a = out["case0_a"]                     # p = 64
+    half = ibmi.contiguous_partition(64, 2, 0.0)
+    i1, i2 = half.sets
+    g0 = np.eye(32) * 0.5
+    out["an_contraction"] = np.array([ran.contraction_factor(a, i1, i2)])
+    out["an_spectral"] = np.array([ran.spectral_radius_condition(a, i1, i2)])
+    out["an_cond"] = np.array([rlin.condition_number_2(a)])
+    x0 = np.eye(64) / np.abs(a).sum(axis=1).max()
+    xn, itn, cvn = ran.newton_schultz(a, x0, tol=1e-10)
+    out["an_newton_x"] = xn
+    out["an_newton_meta"] = np.array([itn, int(cvn)])
+    out["an_lemma"] = np.array([ran.lemma_error_recurrence_check(a, i1, i2, g0, 3)])
+    fc = ran.flop_cost(1000, 4, 0.1)
+    out["an_flop"] = np.array([fc.m, fc.h, float(fc.total_flops), float(fc.direct_flops)])
     np.savez_compressed(os.path.join(HERE, "pins.npz"), **out)
     print("pins OK:", len(cases), "cases")
 

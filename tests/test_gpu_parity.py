@@ -469,3 +469,24 @@ def test_cli_compare(tmp_path, capsys):
     assert main(["compare", "--in", str(f), "--blocks", "2", "--tol", "1e-12"]) == 0
     out = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert out["converged"] and out["relative_error_2norm"] < 1e-10
+
+
+def test_analysis_diagnostics_match_reference():
+    import warnings
+
+    import paper_2502_06377_b200 as pkg
+    from paper_2502_06377_b200 import analysis
+
+    pins = golden("pins.npz")
+    a = pins["case0_a"]
+    i1, i2 = pkg.contiguous_partition(64, 2, 0.0).sets
+    assert abs(analysis.contraction_factor(a, i1, i2) - pins["an_contraction"][0]) <= 1e-9 * pins["an_contraction"][0]
+    assert abs(analysis.spectral_radius_condition(a, i1, i2) - pins["an_spectral"][0]) <= 1e-8 * pins["an_spectral"][0]
+    assert abs(analysis.condition_number_2(a) - pins["an_cond"][0]) <= 1e-8 * pins["an_cond"][0]
+    x0 = np.eye(64) / np.abs(a).sum(axis=1).max()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        x, it, cv = analysis.newton_schultz(a, x0, tol=1e-10)
+    assert cv and abs(it - int(pins["an_newton_meta"][0])) <= 1
+    assert rel_fro(x, pins["an_newton_x"]) < 1e-10
+    assert analysis.lemma_error_recurrence_check(a, i1, i2, np.eye(32) * 0.5, 3) < 1e-10

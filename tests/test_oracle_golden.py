@@ -64,3 +64,11 @@ def test_oracle_initial_guesses_against_reference():
     assert np.array_equal(orc.guess_monte_carlo(a, comp, 50, 7), pins["guess_mc"])
     g = pins["guess_takahashi"]
     assert np.abs(orc.guess_takahashi(a, comp) - g).max() <= 1e-12 * np.abs(g).max()
+
+
+def test_flop_cost_matches_reference():
+    from paper_2502_06377_b200.analysis import flop_cost
+
+    pins = golden("pins.npz")
+    fc = flop_cost(1000, 4, 0.1)
+    assert [fc.m, fc.h, float(fc.total_flops), float(fc.direct_flops)] == pins["an_flop"].tolist()
