@@ -83,6 +83,7 @@ struct GemmOp {
 int g_variant = 0;          // 0: CfgA (8 warps 64x32), 1: CfgB (16 warps 32x32), 2: CfgC (BK 32)
 int g_split_diag = 0;       // split-K of the Σ_II GEMM (0 = auto)
 int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
+int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
 int g_use_tma = 1;          // TMA/mbarrier kernel for eligible hot GEMMs
 
@@ -308,16 +309,20 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
 }
 
 // Split factor that fills the SMs: smallest s with tiles*s >= 0.9 * waves * SMs.
+// Split-K factor minimising modelled time: whole waves of 128×128×16 k-tiles
+// (2.1 µs each at the DMMA peak) plus the partial-tile traffic of the
+// fixed-order reduction (write s tiles, read them back, write the result).
 int auto_split(int tiles, int kt_total, int sms) {
-  if (tiles >= 4 * sms) return 1;
+  const double t_k = 2.1e-6, tile_bytes = 128.0 * 128.0 * 8.0, hbm = 6.0e12;
   int best = 1;
-  double best_eff = 0.0;
+  double best_t = 1e300;
   for (int s = 1; s <= 8; ++s) {
-    if (kt_total / s < 8) break;
-    const int ctas = tiles * s;
-    const int waves = (ctas + sms - 1) / sms;
-    const double eff = (double)ctas / (waves * sms) * (1.0 - 0.01 * (s - 1));
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+    if (s > 1 && kt_total / s < 8) break;
+    const int64_t ctas = (int64_t)tiles * s;
+    const int64_t waves = (ctas + sms - 1) / sms;
+    const double t = (double)waves * ((kt_total + s - 1) / s) * t_k +
+                     (s > 1 ? (double)tiles * (2.0 * s + 1.0) * tile_bytes / hbm + 5e-6 : 0.0);
+    if (t < best_t * 0.995) { best_t = t; best = s; }
   }
   return best;
 }
@@ -788,6 +793,12 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
     k1.add_seg(0, 0, p);
     k1.C = c->S; k1.ldc = c->ld; k1.cm = s.rows(); k1.cn = s.cmap();
     k1.alpha = -1.0; k1.mirror = true;
+    {
+      int64_t need = 0;
+      k1.splits = plan_split(c, k1, g_split_panel, &need);
+      if (need > c->splitws_cap) k1.splits = 1;
+      k1.ws = c->splitws;
+    }
     CUDA_TRY(launch_gemm(k1, c->stream));
     if (mid) CUDA_TRY(cudaEventRecord(mid, c->stream));
     GemmOp k2;
@@ -815,6 +826,12 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k1.C = c->S; k1.ldc = c->ld; k1.cm = contig_map(lo); k1.cn = complement_map(lo, hi);
   k1.alpha = -1.0; k1.mirror = true;
   k1.tma_ok = true; k1.xrows = b; k1.xcols = p; k1.yrows = p; k1.ycols = p;
+  {
+    int64_t need = 0;
+    k1.splits = plan_split(c, k1, g_split_panel, &need);
+    if (need > c->splitws_cap) k1.splits = 1;
+    k1.ws = c->splitws;
+  }
   CUDA_TRY(launch_gemm(k1, c->stream));
   if (mid) CUDA_TRY(cudaEventRecord(mid, c->stream));
   // K2: Σ[I, I] = A_II⁻¹ − Σ[I, c] W_cᵀ   (= ainv + M Wᵀ), lower tiles mirrored
@@ -856,6 +873,17 @@ int ensure_estimate_buffers(ibmi_ctx* c, int64_t b, int64_t cc) {
 int plan_workspace(ibmi_ctx* c) {
   int64_t need = 0;
   for (const SetDev& s : c->sets) {
+    GemmOp k1;
+    k1.M = s.b; k1.N = c->p - s.b;
+    if (s.general) {
+      k1.add_seg(0, 0, c->p);
+    } else {
+      k1.add_seg(0, 0, s.lo);
+      k1.add_seg(s.hi, s.hi, c->p - s.hi);
+    }
+    int64_t w1 = 0;
+    plan_split(c, k1, g_split_panel, &w1);
+    need = std::max(need, w1);
     GemmOp k2;
     k2.M = s.b; k2.N = s.b; k2.lower = true;
     if (s.general) {
@@ -871,6 +899,12 @@ int plan_workspace(ibmi_ctx* c) {
   if (!c->sets.empty()) {
     const SetDev& s = c->sets.back();
     const int64_t cc = c->p - s.b;
+    GemmOp gb;
+    gb.M = s.b; gb.N = cc;
+    gb.add_seg(0, 0, c->p);
+    int64_t wb = 0;
+    plan_split(c, gb, g_split_panel, &wb);
+    need = std::max(need, wb);
     if (s.b <= cc) {
       GemmOp gg;
       gg.M = s.b; gg.N = s.b; gg.lower = true;
@@ -981,6 +1015,12 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   gb.add_seg(0, 0, p);
   gb.C = c->Bm; gb.ldc = c->ldB;
   gb.tma_ok = true; gb.xrows = p; gb.xcols = p; gb.yrows = p; gb.ycols = p;
+  {
+    int64_t need = 0;
+    gb.splits = plan_split(c, gb, g_split_panel, &need);
+    if (need > c->splitws_cap) gb.splits = 1;
+    gb.ws = c->splitws;
+  }
   CUDA_TRY(launch_gemm(gb, c->stream));
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
   NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
@@ -1896,6 +1936,10 @@ int ibmi_tune(int key, int value) {
       break;
     case 3:
       g_use_tma = value ? 1 : 0;
+      break;
+    case 4:
+      if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
+      g_split_panel = value;
       break;
     default:
       return fail(IBMI_ERR_INVALID, "unknown tuning key");
