@@ -3,7 +3,10 @@ the reference-generated golden fixtures.
 
 Tolerances:
   * Σ: relative Frobenius error ≤ 1e-10 against the reference (BASELINE north star);
-  * error trace: |Δerr| ≤ 1e-6·err_ref + 1e-2·tol per sweep;
+  * error trace: |Δerr| ≤ 1e-6·err_ref + 5e-2·tol per sweep (SURVEY B7 proposed 1e-2·tol; the
+    estimate B = Σ[I,:]·A[:,c] is a cancellation whose absolute rounding floor is ~1e-10 at c3 —
+    |Σ| up to 1/nugget = 100 over 8192-term sums — so a different summation order, e.g. split-K,
+    moves err by ~1e-10 = 1e-2·tol);
   * sweep count: exact, or ±1 when some reference error lies inside that band around tol;
   * dense kernels (GEMM, SPD inverse) against float64 torch/numpy: ≤ 1e-13 relative.
 """
@@ -36,7 +39,7 @@ def rel_fro(x, ref):
 
 
 def band_ok(err, ref, tol):
-    return abs(err - ref) <= 1e-6 * ref + 1e-2 * tol
+    return abs(err - ref) <= 1e-6 * ref + 5e-2 * tol
 
 
 def check_trace(errs, ref_errs, tol):
@@ -45,7 +48,7 @@ def check_trace(errs, ref_errs, tol):
     for i in range(n):
         assert band_ok(errs[i], ref_errs[i], tol), (i, errs[i], ref_errs[i])
     if len(errs) != len(ref_errs):
-        near = np.any(np.abs(ref_errs - tol) <= 1e-6 * ref_errs + 1e-2 * tol)
+        near = np.any(np.abs(ref_errs - tol) <= 1e-6 * ref_errs + 5e-2 * tol)
         assert near and abs(len(errs) - len(ref_errs)) <= 1, (len(errs), len(ref_errs))
 
 
@@ -290,7 +293,7 @@ def test_c2_full_solve_frobenius_stop():
     ref_fro = g["frobenius_trace"]
     n = min(len(rep.residual_trace), len(ref_fro))
     fr = np.asarray(rep.residual_trace[:n])
-    assert np.all(np.abs(fr - ref_fro[:n]) <= 1e-6 * ref_fro[:n] + 1e-2 * cfg.tol)
+    assert np.all(np.abs(fr - ref_fro[:n]) <= 1e-6 * ref_fro[:n] + 5e-2 * cfg.tol)
     assert abs(rep.iterations - int(g["iterations"][0])) <= 1
     sample = rep.result[g["sample_i"], g["sample_j"]]
     assert rel_fro(sample, g["sample"]) < 1e-10
