@@ -254,7 +254,33 @@ __global__ void __launch_bounds__(512) power_gram_kernel(PowerParams P) {
     for (int r = gw; r < rows; r += tw) {
       const double* row = M + (int64_t)r * ldm;
       double s = 0.0;
-      if (stage) {
+      if (stage && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+        // 16 independent double2 loads in flight per lane before the FMAs:
+        // the row comes from L2 and the loop is latency-bound otherwise
+        const double2* r2 = reinterpret_cast<const double2*>(row);
+        const double2* y2 = reinterpret_cast<const double2*>(ys);
+        const int n2 = cols >> 1;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int j = lane;
+        for (; j + 15 * 32 < n2; j += 16 * 32) {
+          double2 v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = __ldg(r2 + j + u * 32);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const double2 w = y2[j + u * 32];
+            acc[u & 3] = fma(v[u].x, w.x, acc[u & 3]);
+            acc[u & 3] = fma(v[u].y, w.y, acc[u & 3]);
+          }
+        }
+        for (; j < n2; j += 32) {
+          const double2 v = __ldg(r2 + j), w = y2[j];
+          acc[0] = fma(v.x, w.x, acc[0]);
+          acc[0] = fma(v.y, w.y, acc[0]);
+        }
+        if ((cols & 1) && lane == 0) acc[1] = fma(row[cols - 1], ys[cols - 1], acc[1]);
+        s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      } else if (stage) {
         for (int j = lane; j < cols; j += 32) s = fma(row[j], ys[j], s);
       } else {
         for (int j = lane; j < cols; j += 32) s = fma(row[j], xs * __ldcg(xin + j), s);
