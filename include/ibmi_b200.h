@@ -218,7 +218,8 @@ int ibmi_ipc_close(void* ptr);
  * key 0: GEMM configuration of the hot NT kernels (0: 8 warps 64x32, BK16;
  *        1: 16 warps 32x32, BK16 [default]; 2: 16 warps 32x32, BK32);
  * key 1: split-K factor of the Σ_II GEMM (0 = auto); key 2: of the Gram GEMM;
- * key 3: TMA/mbarrier kernel on/off; key 4: split-K of the panel and estimate GEMMs. */
+ * key 3: TMA/mbarrier kernel on/off; key 4: split-K of the panel and estimate GEMMs;
+ * key 5: cluster (DSMEM) power iteration for Gram order <= 640 on/off. */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

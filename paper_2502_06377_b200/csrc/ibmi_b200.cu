@@ -84,6 +84,7 @@ int g_variant = 0;          // 0: CfgA (8 warps 64x32), 1: CfgB (16 warps 32x32)
 int g_split_diag = 0;       // split-K of the Σ_II GEMM (0 = auto)
 int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
+int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
 int g_use_tma = 1;          // TMA/mbarrier kernel for eligible hot GEMMs
 
@@ -979,6 +980,21 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
   P.mode = mode;
   P.out = nb.out;
   P.smem_cap = (int)(nb.smem_cap / sizeof(double));
+  if (n <= CLUSTER_MAX_N && g_cluster_power) {
+    // small Gram: one 16-CTA cluster, G resident in shared memory, DSMEM exchange
+    const size_t csm = power_cluster_smem((int)n);
+    static bool attr[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+      CUDA_TRY(cudaFuncSetAttribute(power_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      CUDA_TRY(cudaFuncSetAttribute(power_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr[dev & 63] = true;
+    }
+    power_cluster_kernel<<<CLUSTER_CTAS, 256, csm, st>>>(P);
+    if (cudaGetLastError() == cudaSuccess) return IBMI_OK;
+    // cluster not schedulable here: fall through to the grid-wide kernel
+  }
   const size_t smem = (size_t)std::min<int64_t>(n, P.smem_cap) * sizeof(double);
   void* args[] = {&P};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)power_gram_kernel, dim3(nb.blocks), dim3(nb.threads), args, smem,
@@ -1940,6 +1956,9 @@ int ibmi_tune(int key, int value) {
     case 4:
       if (value < 0 || value > 16) return fail(IBMI_ERR_INVALID, "split must be in [0, 16]");
       g_split_panel = value;
+      break;
+    case 5:
+      g_cluster_power = value ? 1 : 0;
       break;
     default:
       return fail(IBMI_ERR_INVALID, "unknown tuning key");

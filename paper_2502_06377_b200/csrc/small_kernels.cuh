@@ -401,3 +401,172 @@ __global__ void dmma_probe_kernel(double* out, int iters, double a, double b) {
 }
 
 }  // namespace ibmi
+
+namespace ibmi {
+
+// ---------------------------------------------------------------------------
+// Small-Gram power iteration on ONE thread-block cluster (n ≤ CLUSTER_MAX_N).
+// The 16 CTAs of the cluster each keep a contiguous slice of G's rows in
+// shared memory for the whole iteration; every iteration each CTA computes
+// its slice of z = G·y, broadcasts the slice and its two partial sums into
+// all 16 CTAs' shared memory over DSMEM, and one cluster barrier (instead of
+// a grid barrier through L2) completes the step.  Same arithmetic sequence and
+// stopping rule as power_gram_kernel (fixed-order sums -> every CTA agrees).
+constexpr int CLUSTER_CTAS = 16;
+constexpr int CLUSTER_MAX_N = 640;
+
+__global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(256)
+    power_cluster_kernel(PowerParams P) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ double csm[];
+  const int n = P.n;
+  const int rank = (int)cluster.block_rank();
+  const int per = (n + CLUSTER_CTAS - 1) / CLUSTER_CTAS;
+  const int r0 = min(n, rank * per), r1 = min(n, r0 + per);
+  const int nr = r1 - r0;
+  double* g = csm;                          // nr × n  (this CTA's rows of G)
+  double* y = g + (size_t)per * n;          // 2 × n   (double-buffered iterate, full copy)
+  double* part = y + 2 * n;                 // 2 × 2 × CLUSTER_CTAS partial sums
+  __shared__ double red[16];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < nr * n; e += blockDim.x) g[e] = P.G[(int64_t)(r0 + e / n) * P.ldg + (e % n)];
+  cluster.sync();
+
+  // Fixed-order sum of one value per CTA, broadcast into every CTA's part[slot].
+  auto publish2 = [&](double a, double b, int slot) -> double2 {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) { red[2 * warp] = a; red[2 * warp + 1] = b; }
+    __syncthreads();
+    if (tid < CLUSTER_CTAS) {
+      double sa = 0.0, sb = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { sa += red[2 * w]; sb += red[2 * w + 1]; }
+      double* dst = cluster.map_shared_rank(part, tid);
+      dst[slot * 2 * CLUSTER_CTAS + 2 * rank] = sa;
+      dst[slot * 2 * CLUSTER_CTAS + 2 * rank + 1] = sb;
+    }
+    cluster.sync();
+    double sa = 0.0, sb = 0.0;
+    for (int q = 0; q < CLUSTER_CTAS; ++q) {
+      sa += part[slot * 2 * CLUSTER_CTAS + 2 * q];
+      sb += part[slot * 2 * CLUSTER_CTAS + 2 * q + 1];
+    }
+    return make_double2(sa, sb);
+  };
+
+  // z = G·(sc·y[cur]) on this CTA's rows; the slice goes into every CTA's y[nxt].
+  auto matvec = [&](int cur, double sc, double& pyz, double& pzz) {
+    const double* yc = y + (size_t)cur * n;
+    const int nxt = cur ^ 1;
+    pyz = 0.0;
+    pzz = 0.0;
+    for (int r = warp; r < nr; r += (int)(blockDim.x >> 5)) {
+      const double* row = g + (size_t)r * n;
+      double s = 0.0;
+      for (int j = lane; j < n; j += 32) s = fma(row[j], sc * yc[j], s);
+      s = warp_sum(s);
+      if (lane < CLUSTER_CTAS) {
+        double* dst = cluster.map_shared_rank(y, lane);
+        dst[(size_t)nxt * n + r0 + r] = s;
+      }
+      if (lane == 0) {
+        pyz = fma(sc * yc[r0 + r], s, pyz);
+        pzz = fma(s, s, pzz);
+      }
+    }
+  };
+
+  int cur = 0, it = 1, slot = 0;
+  bool restarted = false;
+  double prev = -1.0, sigma = 0.0, sc = 1.0, conv = 0.0;
+  if (P.mode == 0) {
+    for (int j = tid; j < n; j += blockDim.x) y[j] = __ldcg(P.vec + j);
+    __syncthreads();
+    double pz = 0.0;
+    for (int r = r0 + tid; r < r1; r += blockDim.x) pz = fma(y[r], y[r], pz);
+    sigma = sqrt(publish2(0.0, pz, slot).y);
+    slot ^= 1;
+    for (;;) {
+      if (sigma == 0.0) {
+        if (restarted) { conv = 1.0; break; }
+        // y = B·vr (rare path: rows of B straight from global memory)
+        double pzz = 0.0;
+        for (int r = r0 + warp; r < r1; r += (int)(blockDim.x >> 5)) {
+          const double* row = P.B + (int64_t)r * P.ldb;
+          double s = 0.0;
+          for (int j = lane; j < P.bcols; j += 32) s = fma(row[j], P.vr[j], s);
+          s = warp_sum(s);
+          if (lane < CLUSTER_CTAS) cluster.map_shared_rank(y, lane)[(size_t)(cur ^ 1) * n + r] = s;
+          if (lane == 0) pzz = fma(s, s, pzz);
+        }
+        double2 s2 = publish2(0.0, pzz, slot);
+        slot ^= 1;
+        cur ^= 1;
+        restarted = true;
+        prev = -1.0;
+        if (it >= P.max_iters) { sigma = 0.0; conv = 0.0; it = P.max_iters; break; }
+        ++it;
+        sigma = sqrt(s2.y);
+        sc = 1.0;
+        continue;
+      }
+      if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
+      prev = sigma;
+      double pyz, pzz;
+      matvec(cur, sc, pyz, pzz);
+      double2 s2 = publish2(pyz, pzz, slot);
+      slot ^= 1;
+      const double nw = sqrt(s2.x);
+      if (nw == 0.0) { conv = 1.0; break; }
+      if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+      sigma = sqrt(s2.y) / nw;
+      sc = 1.0 / nw;
+      cur ^= 1;
+      ++it;
+    }
+  } else {
+    const double v1 = 1.0 / sqrt((double)n);
+    for (int j = tid; j < n; j += blockDim.x) y[j] = v1;
+    __syncthreads();
+    for (;;) {
+      double pyz, pzz;
+      matvec(cur, sc, pyz, pzz);
+      double2 s2 = publish2(pyz, pzz, slot);
+      slot ^= 1;
+      sigma = sqrt(fmax(s2.x, 0.0));
+      if (sigma == 0.0) {
+        if (restarted) { conv = 1.0; break; }
+        if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+        for (int j = tid; j < n; j += blockDim.x) y[(size_t)cur * n + j] = P.vr[j];
+        __syncthreads();
+        cluster.sync();
+        restarted = true;
+        prev = -1.0;
+        sc = 1.0;
+        ++it;
+        continue;
+      }
+      if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
+      prev = sigma;
+      const double nw = sqrt(s2.y);
+      if (nw == 0.0) { conv = 1.0; break; }
+      if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+      sc = 1.0 / nw;
+      cur ^= 1;
+      ++it;
+    }
+  }
+  if (rank == 0 && tid == 0) {
+    P.out[0] = sigma;
+    P.out[1] = conv;
+    P.out[2] = (double)it;
+  }
+  cluster.sync();   // no CTA may exit while others still write into its shared memory
+}
+
+inline size_t power_cluster_smem(int n) {
+  const int per = (n + CLUSTER_CTAS - 1) / CLUSTER_CTAS;
+  return ((size_t)per * n + 2 * (size_t)n + 4 * CLUSTER_CTAS) * sizeof(double);
+}
+
+}  // namespace ibmi
