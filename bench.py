@@ -289,6 +289,14 @@ def run_ours(args):
         ms = float(t.item())
     ms_step = ms / args.steps
     sweeps_s = args.steps / (ms / 1e3)
+    consistent = None
+    if world > 1:
+        # every rank must hold the same estimate (replicated power iteration on gathered B)
+        e_last = torch.tensor([errs[-1][0]], dtype=torch.float64, device=f"cuda:{dev}")
+        lo_, hi_ = e_last.clone(), e_last.clone()
+        torch.distributed.all_reduce(lo_, op=torch.distributed.ReduceOp.MIN)
+        torch.distributed.all_reduce(hi_, op=torch.distributed.ReduceOp.MAX)
+        consistent = bool(lo_.item() == hi_.item())
     kt, panel_tf = None, None
     if world == 1 and not args.sharded:
         # per-kernel-class device times of one sweep (CUDA events on the same stream)
@@ -354,6 +362,8 @@ def run_ours(args):
             "tflops_executed": executed_flops(cfg) * sweeps_s / 1e12,
             "fp64_peak_tflops": peak,
             "setup_s": setup_s,
+            "ranks_consistent": consistent,
+            "exchange": getattr(solver, "exchange", None) if world > 1 else None,
             "time_to_tol": ttt,
             "power_iterations": [e[1] for e in errs],
             "error_trace": [e[0] for e in errs],

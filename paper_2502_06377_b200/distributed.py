@@ -366,14 +366,29 @@ class ShardedSolver:
             raise ValueError(f"unknown exchange {exchange!r}")
         self.exchange = exchange
         if exchange == "p2p":
-            # Σ panels live in IPC-exportable memory; every rank maps every peer's panel
+            # Σ panels live in IPC-exportable memory; every rank maps every peer's panel.
+            # The mapping is agreed collectively: if any rank cannot map a peer, all ranks
+            # fall back to the all_to_all exchange together (nobody is left in a collective).
             self.S, handle = backend.alloc_shared(max(self.n_loc, 1), self.ld)
             handles = [None] * self.world
             self.torch.distributed.all_gather_object(handles, handle, group=self.comm.group)
-            ptrs = [self.S.data_ptr() if h == self.rank else backend.open_peer(handles[h]) for h in range(self.world)]
-            self.peers = backend.index_tensor(np.asarray(ptrs, dtype=np.uint64).view(np.int64))
+            ok = 1.0
+            try:
+                ptrs = [self.S.data_ptr() if h == self.rank else backend.open_peer(handles[h])
+                        for h in range(self.world)]
+            except Exception:          # noqa: BLE001 - any mapping failure -> collective fallback
+                ok, ptrs = 0.0, None
+            flag = self.torch.tensor([ok], dtype=self.torch.float64,
+                                     device="cpu" if self.comm.backend == "gloo" else self.S.device)
+            self.torch.distributed.all_reduce(flag, op=self.torch.distributed.ReduceOp.MIN, group=self.comm.group)
+            if float(flag.item()) == 1.0:
+                self.peers = backend.index_tensor(np.asarray(ptrs, dtype=np.uint64).view(np.int64))
+            else:
+                exchange = "nccl"
+                self.S.zero_()
         else:
             self.S = backend.zeros(max(self.n_loc, 1), self.ld)
+        self.exchange = exchange
         self.own_t = backend.index_tensor(self.own)
         self.plan = [self._plan_set(lo, hi) for (lo, hi) in self.ranges]
 
