@@ -214,6 +214,10 @@ int ibmi_ipc_handle(void* ptr, void* handle64);
 int ibmi_ipc_open(int device, const void* handle64, void** ptr);
 int ibmi_ipc_close(void* ptr);
 
+/* Number of kernels this library has launched in the process (graph replays
+ * count their kernel nodes) — the `gpu_launches` of bench.py. */
+long long ibmi_launch_count(void);
+
 /* Tuning knobs (process-wide; contexts re-capture their sweep graph):
  * key 0: GEMM configuration of the hot NT kernels (0: 8 warps 64x32, BK16;
  *        1: 16 warps 32x32, BK16 [default]; 2: 16 warps 32x32, BK32);

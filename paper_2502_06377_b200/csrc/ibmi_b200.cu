@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -49,6 +50,11 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Every kernel this library launches bumps the counter (graph replays add the
+// number of kernel nodes captured), so callers can report `gpu_launches`.
+std::atomic<long long> g_launches{0};
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // ---------------------------------------------------------------- GEMM launch
 struct GemmOp {
@@ -127,7 +133,7 @@ cudaError_t launch_tma_inst(const GemmParams& P, const TmaMaps& maps, int grid, 
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  gemm_tma_kernel<EPI><<<grid, 256, TMA_SMEM, s>>>(P, maps);
+  gemm_tma_kernel<EPI><<<grid, 256, TMA_SMEM, s>>>(P, maps); note_launch();
   return cudaGetLastError();
 }
 
@@ -150,7 +156,7 @@ template <class CF, bool XT, bool YT, bool V16, int EPI>
 cudaError_t launch_inst(const GemmParams& P, int grid, cudaStream_t s) {
   cudaError_t e = ensure_attr<CF, XT, YT, V16, EPI>();
   if (e != cudaSuccess) return e;
-  gemm_nt_kernel<CF, XT, YT, V16, EPI><<<grid, CF::THREADS, CF::SMEM, s>>>(P);
+  gemm_nt_kernel<CF, XT, YT, V16, EPI><<<grid, CF::THREADS, CF::SMEM, s>>>(P); note_launch();
   return cudaGetLastError();
 }
 
@@ -285,7 +291,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
       else if (epi == EPI_FROB) err = launch_tma_inst<EPI_FROB>(P, maps, grid, s);
       else err = launch_tma_inst<EPI_STORE>(P, maps, grid, s);
       if (err != cudaSuccess || !split) return err;
-      splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P);
+      splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P); note_launch();
       return cudaGetLastError();
     }
   }
@@ -305,7 +311,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
               : launch_inst<CfgA, true, false, false, EPI_STORE>(P, grid, s);
   }
   if (err != cudaSuccess || !split) return err;
-  splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P);
+  splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P); note_launch();
   return cudaGetLastError();
 }
 
@@ -555,7 +561,7 @@ int potrf_enqueue(CholScratch& cs, int n, cudaStream_t s, int* info) {
     const int jb = std::min(CHOL_NB, n - j0);
     const int j1 = j0 + jb;
     double* dblk = cs.dinv + (size_t)blk * CHOL_NB * CHOL_NB;
-    potf2_trti2_kernel<<<1, 256, 0, s>>>(a + (int64_t)j0 * ld + j0, ld, jb, dblk, CHOL_NB, info, j0);
+    potf2_trti2_kernel<<<1, 256, 0, s>>>(a + (int64_t)j0 * ld + j0, ld, jb, dblk, CHOL_NB, info, j0); note_launch();
     CUDA_TRY(cudaGetLastError());
     if (j1 >= n) break;
     // panel: L[j1:, j0:j1] = A[j1:, j0:j1] · L_jj⁻ᵀ   (in place, one N tile)
@@ -612,7 +618,7 @@ int trtri_blocked(CholScratch& cs, int n, cudaStream_t s) {
       CUDA_TRY(launch_gemm(t2, s));
     }
     copy2d_kernel<<<grid2d(jb, jb), 256, 0, s>>>(dblk, CHOL_NB, contig_map(0), contig_map(0),
-                                                 a + (int64_t)j0 * ld + j0, ld, jb, jb, 0);
+                                                 a + (int64_t)j0 * ld + j0, ld, jb, jb, 0); note_launch();
     CUDA_TRY(cudaGetLastError());
   }
   return IBMI_OK;
@@ -650,7 +656,7 @@ int mc_guess_into(const double* A, int64_t lda, int64_t p, const double* w_src, 
     e = cudaMemcpyAsync(w, w_src, (size_t)p * n * sizeof(double),
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) { cs.release(); cudaFree(w); cudaFree(z); return fail(IBMI_ERR_OOM, cudaGetErrorString(e)); }
-  copy2d_kernel<<<grid2d(p, p), 256, 0, st>>>(A, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)p, (int)p, 1);
+  copy2d_kernel<<<grid2d(p, p), 256, 0, st>>>(A, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)p, (int)p, 1); note_launch();
   int64_t piv = -1;
   rc = potrf_blocked(cs, (int)p, st, &piv);
   if (!rc) rc = trtri_blocked(cs, (int)p, st);
@@ -716,6 +722,7 @@ struct ibmi_ctx {
   double* frob_part = nullptr; int frob_cap = 0;
   double* splitws = nullptr; int64_t splitws_cap = 0;   // split-K partial tiles
   int graph_gen = -1;
+  long long graph_launches = 0;   // kernel nodes in the captured sweep
   double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
   double* hpin = nullptr;         // pinned mirror of dscal
   int sms = 148;
@@ -753,7 +760,7 @@ int symcheck(ibmi_ctx* c, RowMap map, int64_t n, const char* what) {
   unsigned long long* d = reinterpret_cast<unsigned long long*>(c->dscal + 8);
   CUDA_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), c->stream));
   const int nt = (int)((n + 31) / 32);
-  symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, c->stream>>>(c->A, c->ld, map, (int)n, d);
+  symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, c->stream>>>(c->A, c->ld, map, (int)n, d); note_launch();
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(c->hpin + 8, c->dscal + 8, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -965,7 +972,7 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
   if (mode == 0) {
     const int threads = 256;
     const int blocks = (int)((b * 32 + threads - 1) / threads);
-    rowsum_scaled_kernel<<<blocks, threads, 0, st>>>(Bm, ldB, (int)b, (int)cc, 1.0 / std::sqrt((double)cc), nb.vec);
+    rowsum_scaled_kernel<<<blocks, threads, 0, st>>>(Bm, ldB, (int)b, (int)cc, 1.0 / std::sqrt((double)cc), nb.vec); note_launch();
     CUDA_TRY(cudaGetLastError());
   }
   if (ev_gram) CUDA_TRY(cudaEventRecord(ev_gram, st));
@@ -991,14 +998,19 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
       CUDA_TRY(cudaFuncSetAttribute(power_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       attr[dev & 63] = true;
     }
-    power_cluster_kernel<<<CLUSTER_CTAS, 256, csm, st>>>(P);
+    power_cluster_kernel<<<CLUSTER_CTAS, 256, csm, st>>>(P); note_launch();
     if (cudaGetLastError() == cudaSuccess) return IBMI_OK;
     // cluster not schedulable here: fall through to the grid-wide kernel
   }
-  const size_t smem = (size_t)std::min<int64_t>(n, P.smem_cap) * sizeof(double);
+  // rows of G kept resident in each CTA's shared memory, after the staged iterate
+  const int64_t rpc = (n + nb.blocks - 1) / nb.blocks;
+  P.resident = 0;
+  if (n <= P.smem_cap) P.resident = (int)std::max<int64_t>(0, std::min<int64_t>(rpc, (P.smem_cap - n) / n));
+  const size_t smem = ((size_t)std::min<int64_t>(n, P.smem_cap) + (size_t)P.resident * n) * sizeof(double);
   void* args[] = {&P};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)power_gram_kernel, dim3(nb.blocks), dim3(nb.threads), args, smem,
                                        st));
+  note_launch();
   return IBMI_OK;
 }
 
@@ -1006,7 +1018,7 @@ void power_launch_shape(int device, int* blocks, int* threads, size_t* smem_cap)
   int sms = 148, maxb = 1;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   *threads = 512;
-  *smem_cap = 200 * 1024;
+  *smem_cap = 220 * 1024;
   cudaFuncSetAttribute(power_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_cap);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&maxb, power_gram_kernel, *threads, *smem_cap);
   *blocks = sms * std::max(1, std::min(maxb, 1));
@@ -1253,7 +1265,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   for (int j = 0; j < count; ++j) {
     const SetDev& s = c->sets[first + j];
     const int nt = (s.b + 31) / 32;
-    symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(c->A, c->ld, s.rows(), s.b, dsym + 2 * j);
+    symcheck_kernel<<<dim3(nt, nt), dim3(32, 8), 0, st>>>(c->A, c->ld, s.rows(), s.b, dsym + 2 * j); note_launch();
   }
   std::vector<unsigned long long> hsym(2 * count);
   cudaError_t e = cudaGetLastError();
@@ -1313,7 +1325,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
     CholScratch& cs = scr[q];
     const int64_t b = s.b, lo = s.lo, hi = s.hi;
     int* info = dinfo + j;
-    copy2d_kernel<<<grid2d(b, b), 256, 0, sq>>>(c->A, c->ld, s.rows(), s.rows(), cs.ws, cs.ldw, (int)b, (int)b, 1);
+    copy2d_kernel<<<grid2d(b, b), 256, 0, sq>>>(c->A, c->ld, s.rows(), s.rows(), cs.ws, cs.ldw, (int)b, (int)b, 1); note_launch();
     SETUP_TRY(cudaGetLastError());
     rc = potrf_enqueue(cs, (int)b, sq, info);
     if (!rc) rc = potri_blocked(cs, (int)b, s.ainv, s.ldb, sq);
@@ -1329,7 +1341,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
       }
       double* ai = gather[q];
       copy2d_kernel<<<grid2d(b, c->ld), 256, 0, sq>>>(c->A, c->ld, s.rows(), contig_map(0), ai, c->ld, (int)b,
-                                                     (int)c->ld, 0);
+                                                     (int)c->ld, 0); note_launch();
       GemmOp gw;
       gw.X = s.ainv; gw.ldx = s.ldb;
       gw.Y = ai; gw.ldy = c->ld; gw.yt = true;
@@ -1338,7 +1350,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
       gw.C = s.W; gw.ldc = c->ld;
       SETUP_TRY(launch_gemm(gw, sq));
       zero_cols_kernel<<<dim3((unsigned)((b + 255) / 256), (unsigned)std::min<int64_t>(b, 65535)), 256, 0, sq>>>(
-          s.W, c->ld, (int)b, s.rows(), (int)b);
+          s.W, c->ld, (int)b, s.rows(), (int)b); note_launch();
       SETUP_TRY(cudaGetLastError());
     } else {
       GemmOp gw;
@@ -1384,13 +1396,13 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
   const SetDev& s0 = c->sets[0];
   const int64_t c0 = p - s0.b;
   cudaStream_t st = c->stream;
-  fill2d_kernel<<<grid2d(p, c->ld), 256, 0, st>>>(c->S, c->ld, (int)p, (int)c->ld, 0.0, 1.0);
+  fill2d_kernel<<<grid2d(p, c->ld), 256, 0, st>>>(c->S, c->ld, (int)p, (int)c->ld, 0.0, 1.0); note_launch();
   CUDA_TRY(cudaGetLastError());
   if (c0 == 0) return IBMI_OK;
   const RowMap cmap = s0.cmap();
   if (kind == IBMI_GUESS_IDENTITY) {
   } else if (kind == IBMI_GUESS_JACOBI) {
-    jacobi_diag_kernel<<<(int)((c0 + 255) / 256), 256, 0, st>>>(c->A, c->ld, c->S, c->ld, cmap, (int)c0);
+    jacobi_diag_kernel<<<(int)((c0 + 255) / 256), 256, 0, st>>>(c->A, c->ld, c->S, c->ld, cmap, (int)c0); note_launch();
     CUDA_TRY(cudaGetLastError());
   } else if (kind == IBMI_GUESS_MATRIX) {
     if (!guess || ldg < c0) return fail(IBMI_ERR_DIM, "guess must be c1 x c1");
@@ -1399,7 +1411,7 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
     cudaError_t e = cudaMemcpy2DAsync(tmp, c0 * 8, guess, ldg * 8, c0 * 8, c0,
                                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
-      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(tmp, c0, c->S, c->ld, cmap, cmap, (int)c0, (int)c0);
+      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(tmp, c0, c->S, c->ld, cmap, cmap, (int)c0, (int)c0); note_launch();
       e = cudaGetLastError();
     }
     cudaStreamSynchronize(st);
@@ -1412,12 +1424,12 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
     double* inv = nullptr;
     cudaError_t e = cudaMalloc(&inv, (size_t)c0 * cs.ldw * sizeof(double));
     if (e != cudaSuccess) { cs.release(); return fail(IBMI_ERR_OOM, cudaGetErrorString(e)); }
-    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 1);
+    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 1); note_launch();
     int64_t piv = -1;
     rc = potrf_blocked(cs, (int)c0, st, &piv);
     if (!rc) rc = potri_blocked(cs, (int)c0, inv, cs.ldw, st);
     if (!rc) {
-      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(inv, cs.ldw, c->S, c->ld, cmap, cmap, (int)c0, (int)c0);
+      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(inv, cs.ldw, c->S, c->ld, cmap, cmap, (int)c0, (int)c0); note_launch();
       cudaStreamSynchronize(st);
     }
     cudaFree(inv);
@@ -1446,9 +1458,9 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
       return fail(IBMI_ERR_OOM, cudaGetErrorString(e));
     }
     const RowMap imap = s0.rows();
-    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 1);
-    copy2d_kernel<<<grid2d(c0, b0), 256, 0, st>>>(c->A, c->ld, cmap, imap, aci, ldb0, (int)c0, (int)b0, 0);
-    copy2d_kernel<<<grid2d(b0, c0), 256, 0, st>>>(s0.W, c->ld, contig_map(0), cmap, wc, ldc0, (int)b0, (int)c0, 0);
+    copy2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(c->A, c->ld, cmap, cmap, cs.ws, cs.ldw, (int)c0, (int)c0, 1); note_launch();
+    copy2d_kernel<<<grid2d(c0, b0), 256, 0, st>>>(c->A, c->ld, cmap, imap, aci, ldb0, (int)c0, (int)b0, 0); note_launch();
+    copy2d_kernel<<<grid2d(b0, c0), 256, 0, st>>>(s0.W, c->ld, contig_map(0), cmap, wc, ldc0, (int)b0, (int)c0, 0); note_launch();
     GemmOp gs;   // S_c[m][n] = A_cc[m][n] − Σ_k A_cI[m][k] W_c[k][n]
     gs.X = aci; gs.ldx = ldb0;
     gs.Y = wc; gs.ldy = ldc0; gs.yt = true;
@@ -1463,7 +1475,7 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
     if (!rc) rc = potrf_blocked(cs, (int)c0, st, &piv);
     if (!rc) rc = potri_blocked(cs, (int)c0, inv, cs.ldw, st);
     if (!rc) {
-      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(inv, cs.ldw, c->S, c->ld, cmap, cmap, (int)c0, (int)c0);
+      scatter2d_kernel<<<grid2d(c0, c0), 256, 0, st>>>(inv, cs.ldw, c->S, c->ld, cmap, cmap, (int)c0, (int)c0); note_launch();
       cudaStreamSynchronize(st);
     }
     cs.release();
@@ -1581,7 +1593,10 @@ int ibmi_sweep(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters,
     c->graph_max = max_iters;
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const long long before = g_launches.load();
       int erc = enqueue_sweep(c, rtol, max_iters);
+      c->graph_launches = g_launches.load() - before;
+      g_launches.fetch_sub(c->graph_launches);     // captured, not launched
       cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
       if (erc == IBMI_OK && ec == cudaSuccess && g) {
         if (cudaGraphInstantiate(&c->graph, g, 0) == cudaSuccess) c->graph_ok = true;
@@ -1593,6 +1608,7 @@ int ibmi_sweep(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters,
   }
   if (c->graph_ok) {
     CUDA_TRY(cudaGraphLaunch(c->graph, c->stream));
+    g_launches.fetch_add(c->graph_launches);
   } else {
     rc = enqueue_sweep(c, rtol, max_iters);
     if (rc) return rc;
@@ -1658,7 +1674,7 @@ int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
   c->frob_cap = (int)cap;
   fr.partial = c->frob_part;
   CUDA_TRY(launch_gemm(fr, c->stream));
-  reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->frob_part, nparts, c->dscal + 3);
+  reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->frob_part, nparts, c->dscal + 3); note_launch();
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaMemcpyAsync(c->hpin + 3, c->dscal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1696,7 +1712,7 @@ int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64
   CholScratch cs;
   int rc = ensure_scratch(cs, (int)n);
   if (rc) { cs.release(); return rc; }
-  copy2d_kernel<<<grid2d(n, n), 256, 0, st>>>(a, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)n, (int)n, 1);
+  copy2d_kernel<<<grid2d(n, n), 256, 0, st>>>(a, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)n, (int)n, 1); note_launch();
   int64_t piv = -1;
   rc = potrf_blocked(cs, (int)n, st, &piv);
   if (rc == IBMI_ERR_NOT_SPD && fail_pivot) *fail_pivot = piv;
@@ -1824,7 +1840,7 @@ int ibmi_gemm(const ibmi_gemm_desc* d, void* stream) {
   if (d->frob_out) {
     op.partial = d->ws;
     CUDA_TRY(launch_gemm(op, st));
-    reduce_partials_kernel<<<1, 1024, 0, st>>>(d->ws, (int)need, d->frob_out);
+    reduce_partials_kernel<<<1, 1024, 0, st>>>(d->ws, (int)need, d->frob_out); note_launch();
     CUDA_TRY(cudaGetLastError());
     return IBMI_OK;
   }
@@ -1936,6 +1952,8 @@ int ibmi_save_sigma_ibmi1(ibmi_ctx* c, const char* path) {
   return rc;
 }
 
+long long ibmi_launch_count(void) { return g_launches.load(); }
+
 int ibmi_tune(int key, int value) {
   switch (key) {
     case 0:
@@ -1992,11 +2010,11 @@ int ibmi_probe_fp64_peak(int device, double* tflops) {
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   const int warps = 8, iters = 20000;
-  dmma_probe_kernel<<<sms * 2, warps * 32>>>(d, 200, 1.0000001, 0.999999);
+  dmma_probe_kernel<<<sms * 2, warps * 32>>>(d, 200, 1.0000001, 0.999999); note_launch();
   float best = 1e30f;
   for (int r = 0; r < 3; ++r) {
     CUDA_TRY(cudaEventRecord(e0));
-    dmma_probe_kernel<<<sms * 2, warps * 32>>>(d, iters, 1.0000001, 0.999999);
+    dmma_probe_kernel<<<sms * 2, warps * 32>>>(d, iters, 1.0000001, 0.999999); note_launch();
     CUDA_TRY(cudaEventRecord(e1));
     CUDA_TRY(cudaEventSynchronize(e1));
     float ms;

@@ -193,6 +193,7 @@ struct PowerParams {
   int max_iters;
   int mode;
   int smem_cap;     // doubles of dynamic shared memory available for staging
+  int resident;     // rows of G each CTA keeps in shared memory (after the staged iterate)
   double* out;      // sigma, converged, iterations
 };
 
@@ -225,7 +226,7 @@ __device__ __forceinline__ void grid_sum2(const double* part, int nb, double& a,
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(512) power_gram_kernel(PowerParams P) {
+__global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double ys[];           // n doubles (the current iterate, scaled)
   __shared__ double red[64];
@@ -295,6 +296,62 @@ __global__ void __launch_bounds__(512) power_gram_kernel(PowerParams P) {
     __syncthreads();
   };
 
+  // z = G·(xs·xin) over this CTA's contiguous row block [rb0, rb1); the first
+  // P.resident rows of the block live in shared memory for the whole kernel.
+  const int rpc = (n + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int rb0 = min(n, (int)blockIdx.x * rpc), rb1 = min(n, rb0 + rpc);
+  double* gres = ys + (stage ? n : 0);
+  const int nres = stage ? min(P.resident, rb1 - rb0) : 0;
+  for (int e = threadIdx.x; e < nres * n; e += blockDim.x) gres[e] = P.G[(int64_t)(rb0 + e / n) * P.ldg + (e % n)];
+  auto gmatvec = [&](const double* xin, double xs, double* zout, double& pyz, double& pzz) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) ys[j] = xs * __ldcg(xin + j);
+    __syncthreads();
+    pyz = 0.0;
+    pzz = 0.0;
+    const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = rb0 + wid; r < rb1; r += nw) {
+      const bool res = r - rb0 < nres;
+      const double* row = res ? gres + (size_t)(r - rb0) * n : P.G + (int64_t)r * P.ldg;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const double2* r2 = reinterpret_cast<const double2*>(row);
+      const double2* y2 = reinterpret_cast<const double2*>(ys);
+      const int n2 = n >> 1;
+      int j = lane;
+      if (res) {
+        for (; j < n2; j += 32) {
+          const double2 v = r2[j], w = y2[j];
+          acc[0] = fma(v.x, w.x, acc[0]);
+          acc[1] = fma(v.y, w.y, acc[1]);
+        }
+      } else {
+        for (; j + 15 * 32 < n2; j += 16 * 32) {
+          double2 v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = __ldg(r2 + j + u * 32);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const double2 w = y2[j + u * 32];
+            acc[u & 3] = fma(v[u].x, w.x, acc[u & 3]);
+            acc[u & 3] = fma(v[u].y, w.y, acc[u & 3]);
+          }
+        }
+        for (; j < n2; j += 32) {
+          const double2 v = __ldg(r2 + j), w = y2[j];
+          acc[0] = fma(v.x, w.x, acc[0]);
+          acc[0] = fma(v.y, w.y, acc[0]);
+        }
+      }
+      if ((n & 1) && lane == 0) acc[2] = fma(row[n - 1], ys[n - 1], acc[2]);
+      double sr = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+      if (lane == 0) {
+        zout[r] = sr;
+        pyz = fma(ys[r], sr, pyz);
+        pzz = fma(sr, sr, pzz);
+      }
+    }
+    __syncthreads();
+  };
+
   auto publish = [&](double a, double b) {   // block partial -> part[phase]
     block_sum2(a, b, red);
     if (threadIdx.x == 0) {
@@ -335,7 +392,8 @@ __global__ void __launch_bounds__(512) power_gram_kernel(PowerParams P) {
       if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
       prev = sigma;
       double pyz, pzz;
-      matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+      if (stage) gmatvec(P.vec + (size_t)cur * n, sc, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+      else matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
       s = publish(pyz, pzz);
       const double nw = sqrt(s.x);
       if (nw == 0.0) { conv = 1.0; break; }
@@ -352,7 +410,8 @@ __global__ void __launch_bounds__(512) power_gram_kernel(PowerParams P) {
     grid.sync();
     for (;;) {
       double pyz, pzz;
-      matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+      if (stage) gmatvec(P.vec + (size_t)cur * n, sc, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
+      else matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
       double2 s = publish(pyz, pzz);
       sigma = sqrt(fmax(s.x, 0.0));
       if (sigma == 0.0) {
