@@ -493,3 +493,22 @@ def test_analysis_diagnostics_match_reference():
     assert cv and abs(it - int(pins["an_newton_meta"][0])) <= 1
     assert rel_fro(x, pins["an_newton_x"]) < 1e-10
     assert analysis.lemma_error_recurrence_check(a, i1, i2, np.eye(32) * 0.5, 3) < 1e-10
+
+
+@pytest.mark.parametrize("p,k,f", [(5, 2, 0.0), (9, 4, 0.0), (33, 3, 0.3), (127, 5, 0.25), (250, 10, 0.1),
+                                   (257, 2, 0.45), (600, 7, 0.0), (1001, 3, 0.2), (2048, 16, 0.125),
+                                   (1500, 4, 0.05)])
+def test_solve_shapes_match_oracle(p, k, f):
+    """Odd orders, tiny sets, many blocks, deep overlaps: every kernel path
+    (TMA / cp.async 16B / 8B, split-K, cluster vs grid power iteration)."""
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+
+    a = random_spd(p, p + k)
+    part = pkg.contiguous_partition(p, k, f)
+    sweeps = 4
+    rep = pkg.solve(a, part, pkg.IbmiConfig(tol=1e-300, max_iterations=sweeps))
+    o = orc.solve(a, part.sets, tol=1e-300, max_iterations=sweeps)
+    assert rel_fro(rep.result, o["result"]) < 1e-10
+    np.testing.assert_allclose(rep.error_trace, o["error_trace"], rtol=1e-6, atol=1e-12)
+    assert np.array_equal(rep.result, rep.result.T)
