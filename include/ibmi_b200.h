@@ -173,9 +173,9 @@ typedef struct {
  *   direct: C[cidx ? cidx[m] : cm(m)][cn(n)] = v;   mirror: C2[c2n(n)][c2m(m)] = v;
  *   lower: only the lower triangle (M == N);  frob_out != NULL: instead of storing,
  *   frob_out[0] = sqrt(sum (delta(row(m), cn(n)) - acc)^2), frob_out[1] = the sum.
- * xrows/xcols/yrows/ycols are the operands' physical extents; tma_safe = 1 promises
- * that K columns read past a segment end are finite and meet zeros in the other
- * operand (lets the TMA kernel be used).  `ws` (ws_len doubles, may be NULL) is
+ * xrows/xcols/yrows/ycols are the operands' physical extents; tma_safe = 1 allows
+ * the TMA kernel (boxes may read past a segment end inside those extents; the
+ * extra k slots are masked, so the memory only has to be readable).  `ws` (ws_len doubles, may be NULL) is
  * scratch for split-K / reduction partials; ibmi_gemm_workspace gives the size. */
 typedef struct {
   const double* x; int64_t ldx; ibmi_map xm; int64_t xrows, xcols;

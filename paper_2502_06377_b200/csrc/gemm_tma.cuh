@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
     mbar_wait(bar_full + 8 * s, (kt / TMA_ST) & 1);
     const double* xs = reinterpret_cast<const double*>(gbase + s * TMA_STAGE_BYTES);
     const double* ys = xs + GB_M * TMA_BK;
+    // The box of a segment's last k-tile may run past the segment into other
+    // valid columns (the next segment, or I): mask those k slots to zero.
+    const int kta = kt_begin + kt;
+    const int klim = kta < P.kt0 ? P.seg[0].len - kta * TMA_BK : P.seg[1].len - (kta - P.kt0) * TMA_BK;
 #pragma unroll
     for (int kk = 0; kk < TMA_BK; kk += 8) {
       const int ch = ((kk >> 1) + t) ^ sw;
@@ -187,6 +191,17 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
         const double2 v = *reinterpret_cast<const double2*>(ys + yrow[j] * TMA_BK + (ch << 1));
         b[j][0] = v.x;
         b[j][1] = v.y;
+      }
+      if (klim < TMA_BK) {
+#pragma unroll
+        for (int ss = 0; ss < 2; ++ss) {
+          if (kk + 2 * t + ss >= klim) {
+#pragma unroll
+            for (int i = 0; i < MI; ++i) a[i][ss] = 0.0;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) b[j][ss] = 0.0;
+          }
+        }
       }
 #pragma unroll
       for (int ss = 0; ss < 2; ++ss)

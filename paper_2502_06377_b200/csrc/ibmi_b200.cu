@@ -74,9 +74,9 @@ struct GemmOp {
   double* partial = nullptr;     // non-null -> Frobenius epilogue
   int splits = 1;                // split-K factor (needs ws: tiles*splits*128*128 doubles)
   double* ws = nullptr;
-  // TMA eligibility: the caller guarantees that K columns read past a segment
-  // end are finite and meet zeros in the other operand (or fall outside
-  // [0, cols), where TMA zero-fills).  rows/cols: physical extent of X and Y.
+  // TMA eligibility: operand rows/cols below are the tensor-map extents (TMA
+  // zero-fills outside them); k slots past a segment end are masked in the
+  // kernel, so any readable memory there is fine.
   bool tma_ok = false;
   int64_t xrows = 0, xcols = 0, yrows = 0, ycols = 0;
   void add_seg(int64_t x0, int64_t y0, int64_t len) {

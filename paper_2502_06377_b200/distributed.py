@@ -464,7 +464,7 @@ class ShardedSolver:
         if n_cl > 0:
             be.gemm(GemmSpec(x=Mbuf, xm=0, y=self._w_loc(k), yn=0, m=b, n=b,
                              segs=[(0, 0, a0), (a0, a1, self.n_loc - a1)], c=top, alpha=-1.0, lower=True,
-                             tma_safe=(a0 % 16 == 0), xrows=b, xcols=n_cl, yrows=b, ycols=self.n_loc))
+                             tma_safe=True, xrows=b, xcols=n_cl, yrows=b, ycols=self.n_loc))
         self.comm.all_reduce(top)     # in p2p mode also the barrier after which the peer stores have landed
         if a1 > a0:
             rel = pl["my_rows_rel"]
