@@ -371,8 +371,12 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
 }
 
 // Fixed-order reduction of split-K partial tiles + the STORE epilogue.
-// grid: one CTA per output tile, 256 threads.
-__global__ void splitk_reduce_kernel(const GemmParams P) {
+// grid: one CTA per output tile, 256 threads.  The tile is processed in
+// 32-row chunks: partial sums and the direct store are coalesced along the
+// row; the mirrored (transposed) store and the peer store go through a shared
+// memory transpose so they are written as contiguous 32-element runs too.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) {
+  __shared__ double tr[32][129];
   const int tile = blockIdx.x;
   int tm, tn;
   if (P.lower) {
@@ -387,20 +391,43 @@ __global__ void splitk_reduce_kernel(const GemmParams P) {
   }
   const bool diag_tile = P.lower && tm == tn;
   const double* src = P.partial + (size_t)tile * P.splits * GB_M * GB_N;
-  for (int e = threadIdx.x; e < GB_M * GB_N; e += blockDim.x) {
-    const int r = e / GB_N, c = e % GB_N;
-    const int m = tm * GB_M + r, n = tn * GB_N + c;
-    if (m >= P.M || n >= P.N) continue;
-    if (diag_tile && m < n) continue;
-    double acc = 0.0;
-    for (int s = 0; s < P.splits; ++s) acc += src[(size_t)s * GB_M * GB_N + e];
-    double v = P.alpha * acc;
-    const int64_t rowc = P.cidx ? P.cidx[m] : map_idx(P.cm, m);
-    if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + map_idx(P.dn, n)];
-    if (P.direct) *direct_addr(P, rowc, n) = v;
-    if (P.mirror) P.C2[map_idx(P.c2n, n) * P.ldc2 + map_idx(P.c2m, m)] = v;
-    if (P.peers) peer_store(P, m, n, v);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = tid & 127;
+  const int n = tn * GB_N + c;
+  const bool ncol_ok = n < P.N;
+  const int64_t colc = ncol_ok ? map_idx(P.cn, n) : 0;
+  const int64_t cold = (ncol_ok && P.beta != 0.0) ? map_idx(P.dn, n) : 0;
+  for (int rc = 0; rc < GB_M; rc += 32) {
+#pragma unroll 4
+    for (int q = 0; q < 16; ++q) {
+      const int r = rc + (tid >> 7) + 2 * q;
+      const int m = tm * GB_M + r;
+      double acc = 0.0;
+      for (int sp = 0; sp < P.splits; ++sp) acc += src[(size_t)sp * GB_M * GB_N + r * GB_N + c];
+      double v = P.alpha * acc;
+      const bool ok = ncol_ok && m < P.M && !(diag_tile && m < n);
+      if (ok) {
+        if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + cold];
+        if (P.direct) P.C[(P.cidx ? P.cidx[m] : map_idx(P.cm, m)) * P.ldc + colc] = v;
+      }
+      tr[r - rc][c] = v;
+    }
+    __syncthreads();
+    if (P.mirror || P.peers) {
+      const int m = tm * GB_M + rc + lane;
+      const bool mrow_ok = m < P.M;
+      const int64_t mcol2 = mrow_ok ? map_idx(P.c2m, m) : 0;
+      for (int cc = warp; cc < GB_N; cc += 8) {
+        const int nn = tn * GB_N + cc;
+        if (!mrow_ok || nn >= P.N || (diag_tile && m < nn)) continue;
+        const double v = tr[lane][cc];
+        if (P.mirror) P.C2[map_idx(P.c2n, nn) * P.ldc2 + mcol2] = v;
+        if (P.peers) peer_store(P, m, nn, v);
+      }
+    }
+    __syncthreads();
   }
+  if (P.peers) __threadfence_system();
 }
 
 }  // namespace ibmi
