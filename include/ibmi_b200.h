@@ -174,8 +174,8 @@ typedef struct {
  *   lower: only the lower triangle (M == N);  frob_out != NULL: instead of storing,
  *   frob_out[0] = sqrt(sum (delta(row(m), cn(n)) - acc)^2), frob_out[1] = the sum.
  * xrows/xcols/yrows/ycols are the operands' physical extents; tma_safe = 1 allows
- * the TMA kernel (boxes may read past a segment end inside those extents; the
- * extra k slots are masked, so the memory only has to be readable).  `ws` (ws_len doubles, may be NULL) is
+ * the TMA kernel (per-segment tensor maps end at the segment end, so boxes
+ * past it are zero-filled by the hardware).  `ws` (ws_len doubles, may be NULL) is
  * scratch for split-K / reduction partials; ibmi_gemm_workspace gives the size. */
 typedef struct {
   const double* x; int64_t ldx; ibmi_map xm; int64_t xrows, xcols;

@@ -26,8 +26,11 @@ constexpr int TMA_TILE_BYTES = GB_M * TMA_BK * 8;          // 16 KB per operand
 constexpr int TMA_STAGE_BYTES = 2 * TMA_TILE_BYTES;        // 32 KB
 constexpr size_t TMA_SMEM = (size_t)TMA_ST * TMA_STAGE_BYTES + 1024 + 2 * TMA_ST * 8;
 
+// One set of maps per K segment: the inner extent of each map ends where its
+// segment ends, so a box that runs past the segment is zero-filled by TMA
+// (exact semantics, no masking in the main loop).
 struct TmaMaps {
-  CUtensorMap xb, xs, yb, ys;                  // big (128-row) and small (8-row) boxes
+  CUtensorMap xb[2], xs[2], yb[2], ys[2];      // big (128-row) and small (8-row) boxes per segment
 };
 
 __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
@@ -126,8 +129,8 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
       mbar_init(bar_empty + 8 * s, 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.xb)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.yb)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.xb[0])) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.yb[0])) : "memory");
   }
   __syncthreads();
 
@@ -139,8 +142,8 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
     const uint32_t fb = bar_full + 8 * s;
     mbar_expect_tx(fb, TMA_STAGE_BYTES);
     const uint32_t dx = base + s * TMA_STAGE_BYTES;
-    tma_operand(dx, &maps.xb, &maps.xs, P.xm, m0, (int)(P.seg[sgi].x0 + ktl * TMA_BK), fb);
-    tma_operand(dx + TMA_TILE_BYTES, &maps.yb, &maps.ys, P.yn, n0, (int)(P.seg[sgi].y0 + ktl * TMA_BK), fb);
+    tma_operand(dx, &maps.xb[sgi], &maps.xs[sgi], P.xm, m0, (int)(P.seg[sgi].x0 + ktl * TMA_BK), fb);
+    tma_operand(dx + TMA_TILE_BYTES, &maps.yb[sgi], &maps.ys[sgi], P.yn, n0, (int)(P.seg[sgi].y0 + ktl * TMA_BK), fb);
   };
 
   if (tid == 0) {
@@ -172,10 +175,6 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
     mbar_wait(bar_full + 8 * s, (kt / TMA_ST) & 1);
     const double* xs = reinterpret_cast<const double*>(gbase + s * TMA_STAGE_BYTES);
     const double* ys = xs + GB_M * TMA_BK;
-    // The box of a segment's last k-tile may run past the segment into other
-    // valid columns (the next segment, or I): mask those k slots to zero.
-    const int kta = kt_begin + kt;
-    const int klim = kta < P.kt0 ? P.seg[0].len - kta * TMA_BK : P.seg[1].len - (kta - P.kt0) * TMA_BK;
 #pragma unroll
     for (int kk = 0; kk < TMA_BK; kk += 8) {
       const int ch = ((kk >> 1) + t) ^ sw;
@@ -191,17 +190,6 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
         const double2 v = *reinterpret_cast<const double2*>(ys + yrow[j] * TMA_BK + (ch << 1));
         b[j][0] = v.x;
         b[j][1] = v.y;
-      }
-      if (klim < TMA_BK) {
-#pragma unroll
-        for (int ss = 0; ss < 2; ++ss) {
-          if (kk + 2 * t + ss >= klim) {
-#pragma unroll
-            for (int i = 0; i < MI; ++i) a[i][ss] = 0.0;
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) b[j][ss] = 0.0;
-          }
-        }
       }
 #pragma unroll
       for (int ss = 0; ss < 2; ++ss)

@@ -74,9 +74,9 @@ struct GemmOp {
   double* partial = nullptr;     // non-null -> Frobenius epilogue
   int splits = 1;                // split-K factor (needs ws: tiles*splits*128*128 doubles)
   double* ws = nullptr;
-  // TMA eligibility: operand rows/cols below are the tensor-map extents (TMA
-  // zero-fills outside them); k slots past a segment end are masked in the
-  // kernel, so any readable memory there is fine.
+  // TMA eligibility: operand rows/cols below are the tensor-map extents; each
+  // K segment gets maps whose inner extent ends at the segment end, so TMA
+  // zero-fills every k slot past it.
   bool tma_ok = false;
   int64_t xrows = 0, xcols = 0, yrows = 0, ycols = 0;
   void add_seg(int64_t x0, int64_t y0, int64_t len) {
@@ -281,10 +281,15 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
       P.kt_total += kt;
     }
     TmaMaps maps;
-    const bool ok = encode_map(&maps.xb, op.X, op.xrows, op.xcols, op.ldx, 128) &&
-                    encode_map(&maps.xs, op.X, op.xrows, op.xcols, op.ldx, 8) &&
-                    encode_map(&maps.yb, op.Y, op.yrows, op.ycols, op.ldy, 128) &&
-                    encode_map(&maps.ys, op.Y, op.yrows, op.ycols, op.ldy, 8);
+    bool ok = true;
+    for (int sg = 0; sg < 2 && ok; ++sg) {
+      const KSeg& k = P.seg[sg];   // P.seg[1] duplicates seg 0 when there is one segment
+      const int64_t xend = std::min<int64_t>(op.xcols, k.x0 + k.len), yend = std::min<int64_t>(op.ycols, k.y0 + k.len);
+      ok = encode_map(&maps.xb[sg], op.X, op.xrows, std::max<int64_t>(xend, 1), op.ldx, 128) &&
+           encode_map(&maps.xs[sg], op.X, op.xrows, std::max<int64_t>(xend, 1), op.ldx, 8) &&
+           encode_map(&maps.yb[sg], op.Y, op.yrows, std::max<int64_t>(yend, 1), op.ldy, 128) &&
+           encode_map(&maps.ys[sg], op.Y, op.yrows, std::max<int64_t>(yend, 1), op.ldy, 8);
+    }
     if (ok) {
       *path = 1;
       if (epi == EPI_PARTIAL) err = launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
