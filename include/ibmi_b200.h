@@ -223,7 +223,8 @@ long long ibmi_launch_count(void);
  *        1: 16 warps 32x32, BK16 [default]; 2: 16 warps 32x32, BK32);
  * key 1: split-K factor of the Σ_II GEMM (0 = auto); key 2: of the Gram GEMM;
  * key 3: TMA/mbarrier kernel on/off; key 4: split-K of the panel and estimate GEMMs;
- * key 5: cluster (DSMEM) power iteration for Gram order <= 640 on/off. */
+ * key 5: cluster (DSMEM) power iteration for Gram order <= 640 on/off;
+ * key 6: minimum k-tiles per split-K slice (default 4). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

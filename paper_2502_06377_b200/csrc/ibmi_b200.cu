@@ -91,6 +91,7 @@ int g_split_diag = 0;       // split-K of the Σ_II GEMM (0 = auto)
 int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
+int g_split_min_kt = 4;     // split-K keeps at least this many k-tiles per split
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
 int g_use_tma = 1;          // TMA/mbarrier kernel for eligible hot GEMMs
 
@@ -328,8 +329,8 @@ int auto_split(int tiles, int kt_total, int sms) {
   const double t_k = 2.1e-6, tile_bytes = 128.0 * 128.0 * 8.0, hbm = 6.0e12;
   int best = 1;
   double best_t = 1e300;
-  for (int s = 1; s <= 8; ++s) {
-    if (s > 1 && kt_total / s < 8) break;
+  for (int s = 1; s <= 16; ++s) {
+    if (s > 1 && kt_total / s < g_split_min_kt) break;
     const int64_t ctas = (int64_t)tiles * s;
     const int64_t waves = (ctas + sms - 1) / sms;
     const double t = (double)waves * ((kt_total + s - 1) / s) * t_k +
@@ -1982,6 +1983,10 @@ int ibmi_tune(int key, int value) {
       break;
     case 5:
       g_cluster_power = value ? 1 : 0;
+      break;
+    case 6:
+      if (value < 1 || value > 64) return fail(IBMI_ERR_INVALID, "min k-tiles per split must be in [1, 64]");
+      g_split_min_kt = value;
       break;
     default:
       return fail(IBMI_ERR_INVALID, "unknown tuning key");
