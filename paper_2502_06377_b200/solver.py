@@ -284,6 +284,15 @@ def _single_set(a, sigma, idx, comp):
     return [(0, idx.size)], np.concatenate([idx, comp]).astype(np.int64)
 
 
+def _require_symmetric_sigma(sigma: np.ndarray) -> None:
+    """The device kernels read a column of Σ as the row with the same index, so
+    Σ must be symmetric (every iterate of the reference is); refuse otherwise
+    rather than silently computing with Σᵀ."""
+    scale = float(np.abs(sigma).max()) if sigma.size else 0.0
+    if scale and float(np.abs(sigma - sigma.T).max()) > 1e-12 * scale:
+        raise ValueError("sigma is not symmetric: the B200 block update requires a symmetric approximation")
+
+
 def block_update(a, sigma, idx, comp) -> None:
     """Apply one block-inverse update to ``sigma`` in place (solver.py:132-144).
 
@@ -295,6 +304,7 @@ def block_update(a, sigma, idx, comp) -> None:
     if a.shape != sigma.shape or a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise DimensionMismatch(f"matrix/approximation shapes differ: {a.shape} vs {sigma.shape}")
     target = sigma if sigma.dtype == np.float64 else np.asarray(sigma, dtype=np.float64)
+    _require_symmetric_sigma(target)
     ranges, perm = _single_set(a, target, idx, comp)
     with DeviceSolver(a, ranges, perm=perm) as ds:
         ds.setup()
@@ -310,6 +320,7 @@ def error_estimate(a, sigma, idx, comp, rtol: float = POWER_RTOL, max_iters: int
     sigma = np.asarray(sigma, dtype=np.float64)
     if a.shape != sigma.shape or a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise DimensionMismatch(f"matrix/approximation shapes differ: {a.shape} vs {sigma.shape}")
+    _require_symmetric_sigma(sigma)
     ranges, perm = _single_set(a, sigma, idx, comp)
     if ranges[0][1] - ranges[0][0] == a.shape[0]:
         raise DimensionMismatch("matrix must be nonempty, got shape (%d, 0)" % a.shape[0])
