@@ -127,6 +127,18 @@ int ibmi_sweep(ibmi_ctx* ctx, double rtol, int max_iters, double* err, int* iter
 int ibmi_sweep_timed(ibmi_ctx* ctx, double rtol, int max_iters, double* err, int* iters, int* converged,
                      float* times);
 
+/* The whole solve loop on the device (solver.py:257-270): a CUDA graph whose
+ * conditional WHILE node replays one sweep plus a one-thread check kernel
+ * until the estimate (stopping 0) or ‖I − AΣ‖_F (stopping 1, evaluated under a
+ * nested IF node only when the estimate allows it) is below tol, or max_sweeps.
+ * Outputs (host, max_sweeps entries, the first *sweeps valid): the estimate,
+ * power iterations / convergence flags, residuals (stopping 1; NaN = skipped)
+ * and per-sweep device time (ms, %globaltimer).  IBMI_ERR_UNSUPPORTED if the
+ * driver cannot build the graph (callers fall back to ibmi_sweep). */
+int ibmi_solve_loop(ibmi_ctx* ctx, double tol, int max_sweeps, double rtol, int max_iters, int stopping,
+                    int* sweeps, int* converged, double* err_trace, int* pow_iters, int* pow_conv,
+                    double* resid_trace, double* sweep_ms);
+
 /* ‖I − AΣ‖_F (BASELINE c2 stopping norm), fused GEMM + reduction. */
 int ibmi_frobenius_residual(ibmi_ctx* ctx, double* out);
 

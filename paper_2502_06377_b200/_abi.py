@@ -47,6 +47,8 @@ SIGNATURES = [
     ("ibmi_sweep", C.c_int, [_P, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("ibmi_sweep_timed", C.c_int, [_P, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                    C.POINTER(C.c_float)]),
+    ("ibmi_solve_loop", C.c_int, [_P, C.c_double, C.c_int, C.c_double, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int), _D, C.POINTER(C.c_int), C.POINTER(C.c_int), _D, _D]),
     ("ibmi_frobenius_residual", C.c_int, [_P, _D]),
     ("ibmi_device_bytes", C.c_int, [_P, C.POINTER(_I64)]),
     ("ibmi_dgemm_nt", C.c_int, [_I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, C.c_double, _P, _I64, _P]),

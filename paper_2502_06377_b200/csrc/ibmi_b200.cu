@@ -1032,7 +1032,8 @@ void power_launch_shape(int device, int* blocks, int* threads, size_t* smem_cap)
 
 // ---- error estimate for set k (solver.py:147-155 + linalg.py:223-274)
 // ev (optional): [0] after the B GEMM, [1] after the Gram GEMM.
-int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaEvent_t* ev = nullptr) {
+int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaEvent_t* ev = nullptr,
+                           bool copy_out = true) {
   const SetDev& s = c->sets[k];
   const int64_t p = c->p, b = s.b, cc = p - b;
   if (cc <= 0) return fail(IBMI_ERR_DIM, "set covers every index: empty complement");
@@ -1061,7 +1062,7 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
               c->power_smem_cap, c->splitws, c->splitws_cap, c->sms};
   rc = enqueue_two_norm(c->Bm, c->ldB, b, cc, rtol, max_iters, nb, c->stream, ev ? ev[1] : nullptr);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(c->hpin, c->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (copy_out) CUDA_TRY(cudaMemcpyAsync(c->hpin, c->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   return IBMI_OK;
 }
 
@@ -1664,9 +1665,7 @@ int ibmi_sweep_timed(ibmi_ctx* c, double rtol, int max_iters, double* err, int* 
   return IBMI_OK;
 }
 
-int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
-  int rc = check_ready(c);
-  if (rc) return rc;
+static int enqueue_frobenius(ibmi_ctx* c) {
   const int64_t p = c->p;
   GemmOp fr;
   fr.X = c->A; fr.ldx = c->ld;
@@ -1682,6 +1681,193 @@ int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
   CUDA_TRY(launch_gemm(fr, c->stream));
   reduce_partials_kernel<<<1, 1024, 0, c->stream>>>(c->frob_part, nparts, c->dscal + 3); note_launch();
   CUDA_TRY(cudaGetLastError());
+  return IBMI_OK;
+}
+
+// Frobenius workspace sized before any capture.
+static int ensure_frob_buffers(ibmi_ctx* c) {
+  GemmOp fr;
+  fr.M = c->p; fr.N = c->p;
+  const int nparts = gemm_grid(fr);
+  int64_t cap = c->frob_cap;
+  if (ensure_buf(&c->frob_part, &cap, nparts, &c->bytes)) return IBMI_ERR_OOM;
+  c->frob_cap = (int)cap;
+  return IBMI_OK;
+}
+
+}  // extern "C"
+
+// ---- device-side solve loop (conditional WHILE graph) -----------------------
+namespace {
+
+int frontier(cudaStream_t st, std::vector<cudaGraphNode_t>& out) {
+  cudaStreamCaptureStatus cs;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CUDA_TRY(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd));
+  out.assign(deps, deps + nd);
+  return IBMI_OK;
+}
+
+int enqueue_sweep_body(ibmi_ctx* c, double rtol, int max_iters) {
+  for (int k = 0; k < (int)c->sets.size(); ++k) {
+    int rc = enqueue_block_update(c, k);
+    if (rc) return rc;
+  }
+  return enqueue_error_estimate(c, (int)c->sets.size() - 1, rtol, max_iters, nullptr, false);
+}
+
+// Builds: start -> WHILE(hw){ sweep; [gate -> IF(hi){ ‖I-AΣ‖_F }]; check }
+int build_loop_graph(ibmi_ctx* c, const LoopState& L, double tol, double rtol, int max_iters, bool frob,
+                     cudaGraph_t* out) {
+  cudaStream_t st = c->stream;
+  const auto mode = cudaStreamCaptureModeThreadLocal;
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaGraphCreate(&g, 0));
+  *out = g;
+  cudaGraphConditionalHandle hw;
+  CUDA_TRY(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+  std::vector<cudaGraphNode_t> deps;
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(st, g, nullptr, nullptr, 0, mode));
+  loop_start_kernel<<<1, 1, 0, st>>>(L); note_launch();
+  int rc = frontier(st, deps);
+  cudaGraph_t tmp = nullptr;
+  CUDA_TRY(cudaStreamEndCapture(st, &tmp));
+  if (rc) return rc;
+  cudaGraphNodeParams wp = {};
+  wp.type = cudaGraphNodeTypeConditional;
+  wp.conditional.handle = hw;
+  wp.conditional.type = cudaGraphCondTypeWhile;
+  wp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  CUDA_TRY(cudaGraphAddNode(&wnode, g, deps.data(), deps.size(), &wp));
+  cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+  CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, mode));
+  rc = enqueue_sweep_body(c, rtol, max_iters);
+  if (!rc && !frob) {
+    loop_check_kernel<<<1, 1, 0, st>>>(hw, L); note_launch();
+  }
+  cudaGraphConditionalHandle hi = 0;
+  if (!rc && frob) {
+    if (cudaGraphConditionalHandleCreate(&hi, g, 0, 0) != cudaSuccess) rc = fail(IBMI_ERR_CUDA, "if handle");
+    if (!rc) {
+      frob_gate_kernel<<<1, 1, 0, st>>>(hi, c->dscal, c->dscal + 3, tol); note_launch();
+      rc = frontier(st, deps);
+    }
+  }
+  cudaError_t ec = cudaStreamEndCapture(st, &tmp);
+  if (rc) return rc;
+  if (ec != cudaSuccess) return fail(IBMI_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ec));
+  if (frob) {
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hi;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    CUDA_TRY(cudaGraphAddNode(&inode, body, deps.data(), deps.size(), &ip));
+    CUDA_TRY(cudaStreamBeginCaptureToGraph(st, ip.conditional.phGraph_out[0], nullptr, nullptr, 0, mode));
+    rc = enqueue_frobenius(c);
+    ec = cudaStreamEndCapture(st, &tmp);
+    if (rc) return rc;
+    if (ec != cudaSuccess) return fail(IBMI_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ec));
+    CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, &inode, nullptr, 1, mode));
+    loop_check_kernel<<<1, 1, 0, st>>>(hw, L); note_launch();
+    ec = cudaStreamEndCapture(st, &tmp);
+    if (ec != cudaSuccess) return fail(IBMI_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ec));
+  }
+  return IBMI_OK;
+}
+
+}  // namespace
+
+int ibmi_solve_loop(ibmi_ctx* c, double tol, int max_sweeps, double rtol, int max_iters, int stopping, int* sweeps,
+                    int* converged, double* err_trace, int* pow_iters, int* pow_conv, double* resid_trace,
+                    double* sweep_ms) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  for (auto& s : c->sets)
+    if (!s.ready) return fail(IBMI_ERR_STATE, "setup not complete");
+  if (max_sweeps < 1 || max_iters < 1) return fail(IBMI_ERR_INVALID, "max_sweeps and max_iters must be >= 1");
+  const SetDev& last = c->sets.back();
+  if (c->p - last.b <= 0) return fail(IBMI_ERR_DIM, "last set covers every index");
+  rc = ensure_estimate_buffers(c, last.b, c->p - last.b);
+  if (!rc) rc = plan_workspace(c);
+  if (!rc && stopping) rc = ensure_frob_buffers(c);
+  if (rc) return rc;
+  if (c->vr == nullptr || c->vr_n != c->p - last.b) return fail(IBMI_ERR_STATE, "restart vector not set");
+  // device trace: err, res (doubles), pit, pconv (ints), ts (u64), it, converged
+  const size_t n = (size_t)max_sweeps;
+  const size_t bytes = n * 8 * 2 + n * 4 * 2 + (n + 1) * 8 + 16;
+  char* buf = nullptr;
+  CUDA_TRY(cudaMalloc(&buf, bytes));
+  LoopState L;
+  L.err = (double*)buf;
+  L.res = L.err + n;
+  L.ts = (unsigned long long*)(L.res + n);
+  L.pit = (int*)(L.ts + n + 1);
+  L.pconv = L.pit + n;
+  L.it = L.pconv + n;
+  L.converged = L.it + 1;
+  L.pw = c->dscal;
+  L.frob = stopping ? c->dscal + 3 : nullptr;
+  L.tol = tol;
+  L.max_sweeps = max_sweeps;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  rc = build_loop_graph(c, L, tol, rtol, max_iters, stopping != 0, &g);
+  if (!rc) {
+    cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+    if (e != cudaSuccess) rc = fail(IBMI_ERR_UNSUPPORTED, std::string("loop graph: ") + cudaGetErrorString(e));
+  }
+  cudaGetLastError();
+  if (!rc) {
+    cudaError_t e = cudaGraphLaunch(ge, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) rc = fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  int h_it = 0, h_conv = 0;
+  if (!rc) {
+    std::vector<double> err(n), res(n);
+    std::vector<int> pit(n), pcv(n);
+    std::vector<unsigned long long> ts(n + 1);
+    cudaError_t e = cudaMemcpy(&h_it, L.it, 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(&h_conv, L.converged, 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(err.data(), L.err, n * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(res.data(), L.res, n * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(pit.data(), L.pit, n * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(pcv.data(), L.pconv, n * 4, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(ts.data(), L.ts, (n + 1) * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      rc = fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+    } else {
+      // every sweep node of the loop ran h_it times
+      for (int i = 0; i < h_it; ++i) {
+        if (err_trace) err_trace[i] = err[i];
+        if (resid_trace) resid_trace[i] = res[i];
+        if (pow_iters) pow_iters[i] = pit[i];
+        if (pow_conv) pow_conv[i] = pcv[i];
+        if (sweep_ms) sweep_ms[i] = (double)(ts[i + 1] - ts[i]) * 1e-6;
+      }
+    }
+  }
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  cudaFree(buf);
+  if (rc) return rc;
+  if (sweeps) *sweeps = h_it;
+  if (converged) *converged = h_conv;
+  return IBMI_OK;
+}
+
+extern "C" {
+
+int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
+  int rc = check_ready(c);
+  if (rc) return rc;
+  rc = enqueue_frobenius(c);
+  if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(c->hpin + 3, c->dscal + 3, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (out) *out = c->hpin[3];

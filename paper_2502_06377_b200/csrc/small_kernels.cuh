@@ -629,3 +629,64 @@ inline size_t power_cluster_smem(int n) {
 }
 
 }  // namespace ibmi
+
+namespace ibmi {
+
+// ---------------------------------------------------------------------------
+// Device-side solve loop (CUDA graph conditional WHILE node): after every
+// sweep a one-thread kernel records the estimate, the power-iteration count
+// and flag, the residual and a %globaltimer stamp, then decides whether the
+// loop continues — the reference's `solve` loop (solver.py:257-270) without a
+// host round trip per sweep.
+struct LoopState {
+  const double* pw;        // power output: sigma, converged, iterations
+  const double* frob;      // residual (sqrt) or nullptr; NaN when the gate skipped it
+  double tol;
+  int max_sweeps;
+  int* it;                 // sweeps done
+  int* converged;
+  double* err;             // [max_sweeps]
+  double* res;             // [max_sweeps]
+  int* pit;                // [max_sweeps]
+  int* pconv;              // [max_sweeps]
+  unsigned long long* ts;  // [max_sweeps + 1]; ts[0] written by loop_start_kernel
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void loop_start_kernel(LoopState L) {
+  *L.it = 0;
+  *L.converged = 0;
+  L.ts[0] = global_ns();
+}
+
+// Frobenius stop: evaluate the 2p³ residual only when it can be < tol, i.e.
+// when the estimate (a lower bound of it) is below tol (+1% rounding margin).
+__global__ void frob_gate_kernel(cudaGraphConditionalHandle h, const double* pw, double* frob, double tol) {
+  frob[0] = __longlong_as_double(0x7ff8000000000000ll);   // NaN unless computed
+  cudaGraphSetConditional(h, pw[0] < 1.01 * tol ? 1u : 0u);
+}
+
+__global__ void loop_check_kernel(cudaGraphConditionalHandle h, LoopState L) {
+  const int i = *L.it;
+  const double e = L.pw[0];
+  L.err[i] = e;
+  L.pconv[i] = L.pw[1] != 0.0;
+  L.pit[i] = (int)L.pw[2];
+  double fr = 0.0;
+  if (L.frob) {
+    fr = L.frob[0];
+    L.res[i] = fr;
+  }
+  L.ts[i + 1] = global_ns();
+  const bool done = L.frob ? (fr < L.tol) : (e <= L.tol);   // NaN < tol is false
+  *L.it = i + 1;
+  if (done) *L.converged = 1;
+  cudaGraphSetConditional(h, (!done && i + 1 < L.max_sweeps) ? 1u : 0u);
+}
+
+}  // namespace ibmi

@@ -251,6 +251,28 @@ class DeviceSolver:
         keys = ("panel_gemm", "diag_gemm", "estimate_gemm", "gram_gemm", "power_iteration", "sweep")
         return e.value, it.value, bool(cv.value), dict(zip(keys, list(t)))
 
+    def solve_loop(self, tol: float, max_sweeps: int, rtol: float, max_iters: int, stopping: str = "estimate"):
+        """Whole solve loop on the device (``ibmi_solve_loop``): returns a dict of
+        per-sweep traces, or raises NotImplementedError if the graph cannot be built."""
+        self._set_restart(self.p - self.sizes[-1])
+        n = int(max_sweeps)
+        err = np.zeros(n)
+        res = np.zeros(n)
+        ms = np.zeros(n)
+        pit = np.zeros(n, dtype=np.int32)
+        pcv = np.zeros(n, dtype=np.int32)
+        sw, cv = C.c_int(), C.c_int()
+        ip = C.POINTER(C.c_int)
+        _abi.check(self._L.ibmi_solve_loop(self._h, float(tol), n, float(rtol), int(max_iters),
+                                           1 if stopping == "frobenius" else 0, C.byref(sw), C.byref(cv),
+                                           _abi.dbl_ptr(err), pit.ctypes.data_as(ip), pcv.ctypes.data_as(ip),
+                                           _abi.dbl_ptr(res), _abi.dbl_ptr(ms)), "solve_loop")
+        k = sw.value
+        return dict(sweeps=k, converged=bool(cv.value), error_trace=err[:k].tolist(), power_iters=pit[:k].tolist(),
+                    power_conv=pcv[:k].astype(bool).tolist(),
+                    residual_trace=res[:k].tolist() if stopping == "frobenius" else [],
+                    sweep_seconds=(ms[:k] * 1e-3).tolist())
+
     def frobenius(self) -> float:
         out = C.c_double()
         _abi.check(self._L.ibmi_frobenius_residual(self._h, C.byref(out)), "frobenius_residual")

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _abi
 from .device import DeviceSolver
-from .exceptions import DimensionMismatch, NoConvergenceWarning
+from .exceptions import DeviceError, DimensionMismatch, NoConvergenceWarning
 from .partition import Partition, complement, validate
 
 __all__ = [
@@ -228,6 +228,26 @@ def run_solve(ds: DeviceSolver, part: Partition, cfg: IbmiConfig, *, a=None, res
     else:
         ds.init_sigma(kind)
     setup_s = time.perf_counter() - t0
+    if callback is None and os.environ.get("IBMI_HOST_LOOP") is None:
+        try:
+            r = ds.solve_loop(cfg.tol, cfg.max_iterations, cfg.norm_rtol, cfg.norm_max_iters, stopping)
+        except (NotImplementedError, DeviceError):
+            r = None            # conditional graphs unavailable: host-driven loop below
+        if r is not None:
+            for ok in r["power_conv"]:
+                if not ok:
+                    warnings.warn(f"two_norm: power iteration did not stabilize in {cfg.norm_max_iters} "
+                                  "iterations; returning last estimate", NoConvergenceWarning, stacklevel=3)
+            t1 = time.perf_counter()
+            result = ds.sigma(on_device=result_on_device) if fetch_result else None
+            if prof:
+                import sys
+
+                print(f"[ibmi] setup {setup_s:.3f}s device loop {sum(r['sweep_seconds']):.3f}s "
+                      f"download {time.perf_counter() - t1:.3f}s", file=sys.stderr)
+            return SolveReport(iterations=r["sweeps"], converged=r["converged"], error_trace=r["error_trace"],
+                               wall_times=r["sweep_seconds"], result=result, power_iterations=r["power_iters"],
+                               residual_trace=r["residual_trace"], setup_seconds=setup_s)
     errs, walls, pits, resid = [], [], [], []
     converged, it = False, 0
     while it < cfg.max_iterations:

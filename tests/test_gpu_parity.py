@@ -524,3 +524,25 @@ def test_block_update_rejects_asymmetric_sigma():
         pkg.block_update(a, s, np.arange(20), np.arange(20, 40))
     with pytest.raises(ValueError):
         pkg.error_estimate(a, s, np.arange(20), np.arange(20, 40))
+
+
+@pytest.mark.parametrize("stopping", ["estimate", "frobenius"])
+def test_device_loop_equals_host_loop(stopping, monkeypatch):
+    """The conditional-graph solve loop gives the host loop's sweeps bit for bit."""
+    import paper_2502_06377_b200 as pkg
+
+    p = 384
+    a = random_spd(p, 51)
+    part = pkg.contiguous_partition(p, 3, 0.1)
+    cfg = pkg.IbmiConfig(tol=1e-11, stopping=stopping)
+    dev = pkg.solve(a, part, cfg)
+    monkeypatch.setenv("IBMI_HOST_LOOP", "1")
+    host = pkg.solve(a, part, cfg)
+    assert dev.iterations == host.iterations and dev.converged == host.converged
+    assert dev.error_trace == host.error_trace
+    assert dev.power_iterations == host.power_iterations
+    assert np.array_equal(dev.result, host.result)
+    if stopping == "frobenius":
+        np.testing.assert_array_equal(np.isnan(dev.residual_trace), np.isnan(host.residual_trace))
+        assert dev.residual_trace[-1] == host.residual_trace[-1] < cfg.tol
+    assert len(dev.wall_times) == dev.iterations and all(w > 0 for w in dev.wall_times)
