@@ -130,9 +130,10 @@ int ibmi_sweep_timed(ibmi_ctx* ctx, double rtol, int max_iters, double* err, int
 /* The whole solve loop on the device (solver.py:257-270): a CUDA graph whose
  * conditional WHILE node replays one sweep plus a one-thread check kernel
  * until the estimate (stopping 0) or ‖I − AΣ‖_F (stopping 1, evaluated under a
- * nested IF node only when the estimate allows it) is below tol, or max_sweeps.
+ * nested IF node only when the estimate allows it; stopping 2, every sweep)
+ * is below tol, or max_sweeps.
  * Outputs (host, max_sweeps entries, the first *sweeps valid): the estimate,
- * power iterations / convergence flags, residuals (stopping 1; NaN = skipped)
+ * power iterations / convergence flags, residuals (stopping 1/2; NaN = skipped)
  * and per-sweep device time (ms, %globaltimer).  IBMI_ERR_UNSUPPORTED if the
  * driver cannot build the graph (callers fall back to ibmi_sweep). */
 int ibmi_solve_loop(ibmi_ctx* ctx, double tol, int max_sweeps, double rtol, int max_iters, int stopping,

@@ -1718,7 +1718,7 @@ int enqueue_sweep_body(ibmi_ctx* c, double rtol, int max_iters) {
 }
 
 // Builds: start -> WHILE(hw){ sweep; [gate -> IF(hi){ ‖I-AΣ‖_F }]; check }
-int build_loop_graph(ibmi_ctx* c, const LoopState& L, double tol, double rtol, int max_iters, bool frob,
+int build_loop_graph(ibmi_ctx* c, const LoopState& L, double gate, double rtol, int max_iters, bool frob,
                      cudaGraph_t* out) {
   cudaStream_t st = c->stream;
   const auto mode = cudaStreamCaptureModeThreadLocal;
@@ -1752,7 +1752,7 @@ int build_loop_graph(ibmi_ctx* c, const LoopState& L, double tol, double rtol, i
   if (!rc && frob) {
     if (cudaGraphConditionalHandleCreate(&hi, g, 0, 0) != cudaSuccess) rc = fail(IBMI_ERR_CUDA, "if handle");
     if (!rc) {
-      frob_gate_kernel<<<1, 1, 0, st>>>(hi, c->dscal, c->dscal + 3, tol); note_launch();
+      frob_gate_kernel<<<1, 1, 0, st>>>(hi, c->dscal, c->dscal + 3, gate); note_launch();
       rc = frontier(st, deps);
     }
   }
@@ -1790,6 +1790,7 @@ int ibmi_solve_loop(ibmi_ctx* c, double tol, int max_sweeps, double rtol, int ma
   for (auto& s : c->sets)
     if (!s.ready) return fail(IBMI_ERR_STATE, "setup not complete");
   if (max_sweeps < 1 || max_iters < 1) return fail(IBMI_ERR_INVALID, "max_sweeps and max_iters must be >= 1");
+  if (stopping < 0 || stopping > 2) return fail(IBMI_ERR_INVALID, "stopping must be 0, 1 or 2");
   const SetDev& last = c->sets.back();
   if (c->p - last.b <= 0) return fail(IBMI_ERR_DIM, "last set covers every index");
   rc = ensure_estimate_buffers(c, last.b, c->p - last.b);
@@ -1816,7 +1817,9 @@ int ibmi_solve_loop(ibmi_ctx* c, double tol, int max_sweeps, double rtol, int ma
   L.max_sweeps = max_sweeps;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
-  rc = build_loop_graph(c, L, tol, rtol, max_iters, stopping != 0, &g);
+    // mode 1 skips the residual while the estimate (a lower bound of it) is above tol
+  const double gate = stopping == 2 ? HUGE_VAL : 1.01 * tol;
+  rc = build_loop_graph(c, L, gate, rtol, max_iters, stopping != 0, &g);
   if (!rc) {
     cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
     if (e != cudaSuccess) rc = fail(IBMI_ERR_UNSUPPORTED, std::string("loop graph: ") + cudaGetErrorString(e));

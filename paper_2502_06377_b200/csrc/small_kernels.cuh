@@ -666,9 +666,10 @@ __global__ void loop_start_kernel(LoopState L) {
 
 // Frobenius stop: evaluate the 2p³ residual only when it can be < tol, i.e.
 // when the estimate (a lower bound of it) is below tol (+1% rounding margin).
-__global__ void frob_gate_kernel(cudaGraphConditionalHandle h, const double* pw, double* frob, double tol) {
+// gate = 1.01·tol (the estimate lower-bounds ‖I−AΣ‖_F) or +inf for every sweep
+__global__ void frob_gate_kernel(cudaGraphConditionalHandle h, const double* pw, double* frob, double gate) {
   frob[0] = __longlong_as_double(0x7ff8000000000000ll);   // NaN unless computed
-  cudaGraphSetConditional(h, pw[0] < 1.01 * tol ? 1u : 0u);
+  cudaGraphSetConditional(h, pw[0] < gate ? 1u : 0u);
 }
 
 __global__ void loop_check_kernel(cudaGraphConditionalHandle h, LoopState L) {

@@ -251,7 +251,8 @@ class DeviceSolver:
         keys = ("panel_gemm", "diag_gemm", "estimate_gemm", "gram_gemm", "power_iteration", "sweep")
         return e.value, it.value, bool(cv.value), dict(zip(keys, list(t)))
 
-    def solve_loop(self, tol: float, max_sweeps: int, rtol: float, max_iters: int, stopping: str = "estimate"):
+    def solve_loop(self, tol: float, max_sweeps: int, rtol: float, max_iters: int, stopping: str = "estimate",
+                   residual_every_sweep: bool = False):
         """Whole solve loop on the device (``ibmi_solve_loop``): returns a dict of
         per-sweep traces, or raises NotImplementedError if the graph cannot be built."""
         self._set_restart(self.p - self.sizes[-1])
@@ -263,8 +264,9 @@ class DeviceSolver:
         pcv = np.zeros(n, dtype=np.int32)
         sw, cv = C.c_int(), C.c_int()
         ip = C.POINTER(C.c_int)
+        mode = 0 if stopping != "frobenius" else (2 if residual_every_sweep else 1)
         _abi.check(self._L.ibmi_solve_loop(self._h, float(tol), n, float(rtol), int(max_iters),
-                                           1 if stopping == "frobenius" else 0, C.byref(sw), C.byref(cv),
+                                           mode, C.byref(sw), C.byref(cv),
                                            _abi.dbl_ptr(err), pit.ctypes.data_as(ip), pcv.ctypes.data_as(ip),
                                            _abi.dbl_ptr(res), _abi.dbl_ptr(ms)), "solve_loop")
         k = sw.value

@@ -230,7 +230,8 @@ def run_solve(ds: DeviceSolver, part: Partition, cfg: IbmiConfig, *, a=None, res
     setup_s = time.perf_counter() - t0
     if callback is None and os.environ.get("IBMI_HOST_LOOP") is None:
         try:
-            r = ds.solve_loop(cfg.tol, cfg.max_iterations, cfg.norm_rtol, cfg.norm_max_iters, stopping)
+            r = ds.solve_loop(cfg.tol, cfg.max_iterations, cfg.norm_rtol, cfg.norm_max_iters, stopping,
+                             cfg.residual_every_sweep)
         except (NotImplementedError, DeviceError):
             r = None            # conditional graphs unavailable: host-driven loop below
         if r is not None:
