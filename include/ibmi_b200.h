@@ -153,6 +153,14 @@ int ibmi_device_bytes(ibmi_ctx* ctx, int64_t* bytes);
 int ibmi_dgemm_nt(int64_t m, int64_t n, int64_t k, double alpha, const double* x, int64_t ldx,
                   const double* y, int64_t ldy, double beta, double* c, int64_t ldc, void* stream);
 
+/* C = alpha · X · Yᵀ by Ozaki-II emulation: `moduli` (8..20) exact INT8
+ * tcgen05 GEMMs of the residues of the row-scaled operands, Chinese
+ * remaindering to the exact integer product, one FP64 rounding.  Accurate to
+ * 2^-t of each row's largest entry, t = min(62, (log2 Π m - 2 - log2 k) / 2).
+ * m <= 65535, k <= 131072.  Synchronises `stream` (shared workspace). */
+int ibmi_dgemm_nt_ozaki(int64_t m, int64_t n, int64_t k, double alpha, const double* x, int64_t ldx,
+                        const double* y, int64_t ldy, double* c, int64_t ldc, int moduli, void* stream);
+
 /* out = A⁻¹ for SPD A (n×n) via blocked Cholesky; replaces spd_inverse
  * (linalg.py:122-130).  On IBMI_ERR_NOT_SPD *fail_pivot = elimination step. */
 int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
@@ -237,7 +245,10 @@ long long ibmi_launch_count(void);
  * key 1: split-K factor of the Σ_II GEMM (0 = auto); key 2: of the Gram GEMM;
  * key 3: TMA/mbarrier kernel on/off; key 4: split-K of the panel and estimate GEMMs;
  * key 5: cluster (DSMEM) power iteration for Gram order <= 640 on/off;
- * key 6: minimum k-tiles per split-K slice (default 4). */
+ * key 6: minimum k-tiles per split-K slice (default 4);
+ * key 7: Ozaki-II FP64 emulation of the panel GEMM on the INT8 tensor cores:
+ *        0 = off (FP64 DMMA, default), 8..20 = number of moduli;
+ * key 8: Ozaki residue-plane budget per N chunk, MB (default 5722 = 6e9 B). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

@@ -28,6 +28,8 @@
 #include "gemm_nt.cuh"
 #include "gemm_tma.cuh"
 #include "small_kernels.cuh"
+#include "igemm_tc.cuh"
+#include "ozaki.cuh"
 
 using namespace ibmi;
 
@@ -338,6 +340,254 @@ int auto_split(int tiles, int kt_total, int sms) {
     if (t < best_t * 0.995) { best_t = t; best = s; }
   }
   return best;
+}
+
+// ------------------------------------------------ Ozaki-II FP64 emulation
+// (ozaki.cuh).  g_oz_n = 0 keeps every GEMM on the FP64 DMMA kernels; 8..20
+// routes the eligible hot GEMMs through n INT8 residue GEMMs on tcgen05.
+int g_oz_n = 0;
+double g_oz_budget = 6e9;      // bytes of Y residue planes per N chunk
+const int kOzModuli[OZ_MAXN] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
+                                223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
+OzTable g_oz_host[OZ_MAXN - OZ_MINN + 1];
+bool g_oz_host_ready = false;
+uint64_t g_oz_dev_ready = 0;   // bit per device: constant tables uploaded
+
+struct Big {   // 192-bit unsigned, 32-bit limbs
+  uint32_t l[OZ_LIMBS] = {0, 0, 0, 0, 0, 0};
+  void mul(uint32_t m) {
+    uint64_t carry = 0;
+    for (int k = 0; k < OZ_LIMBS; ++k) {
+      const uint64_t v = (uint64_t)l[k] * m + carry;
+      l[k] = (uint32_t)v;
+      carry = v >> 32;
+    }
+  }
+  uint32_t mod(uint32_t m) const {
+    uint64_t r = 0;
+    for (int k = OZ_LIMBS - 1; k >= 0; --k) r = ((r << 32) | l[k]) % m;
+    return (uint32_t)r;
+  }
+  double to_double() const {
+    double d = 0.0;
+    for (int k = OZ_LIMBS - 1; k >= 0; --k) d = d * 4294967296.0 + (double)l[k];
+    return d;
+  }
+};
+
+void oz_build_tables() {
+  if (g_oz_host_ready) return;
+  for (int n = OZ_MINN; n <= OZ_MAXN; ++n) {
+    OzTable& T = g_oz_host[n - OZ_MINN];
+    memset(&T, 0, sizeof(T));
+    T.n = n;
+    Big P;
+    P.l[0] = 1;
+    T.log2P = 0.0;
+    for (int i = 0; i < n; ++i) {
+      P.mul((uint32_t)kOzModuli[i]);
+      T.log2P += std::log2((double)kOzModuli[i]);
+    }
+    memcpy(T.P, P.l, sizeof(T.P));
+    const double Pd = P.to_double();
+    for (int i = 0; i < n; ++i) {
+      const uint32_t m = (uint32_t)kOzModuli[i];
+      T.m[i] = (int)m;
+      T.invm[i] = 1.0f / (float)m;
+      uint32_t pw[8];
+      uint64_t v = 1 % m;
+      for (int b = 0; b < 8; ++b) {
+        pw[b] = (uint32_t)v;
+        v = (v * 256) % m;
+      }
+      // v = 2^64 mod m now
+      T.cneg[i] = (int)((m - (uint32_t)v) % m);
+      T.cpow[i][0] = pw[0] | (pw[1] << 8) | (pw[2] << 16) | (pw[3] << 24);
+      T.cpow[i][1] = pw[4] | (pw[5] << 8) | (pw[6] << 16) | (pw[7] << 24);
+      Big Pl;
+      Pl.l[0] = 1;
+      for (int j = 0; j < n; ++j)
+        if (j != i) Pl.mul((uint32_t)kOzModuli[j]);
+      const uint32_t a = Pl.mod(m);
+      uint32_t y = 0;
+      for (uint32_t t = 1; t < m; ++t)
+        if ((uint64_t)a * t % m == 1) { y = t; break; }
+      Pl.mul(y);
+      memcpy(T.w[i], Pl.l, sizeof(T.w[i]));
+      T.f[i] = Pl.to_double() / Pd;
+    }
+  }
+  g_oz_host_ready = true;
+}
+
+cudaError_t oz_upload_tables() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && (g_oz_dev_ready >> dev) & 1) return cudaSuccess;
+  oz_build_tables();
+  e = cudaMemcpyToSymbol(c_oz, g_oz_host, sizeof(g_oz_host));
+  if (e == cudaSuccess && dev < 64) g_oz_dev_ready |= (uint64_t)1 << dev;
+  return e;
+}
+
+// bits per scaled operand entry: K·2^(2t) <= P/4, capped at 62 (int64 path)
+int oz_bits(int n, int64_t K) {
+  oz_build_tables();
+  const double lp = g_oz_host[n - OZ_MINN].log2P;
+  const int t = (int)std::floor((lp - 2.0 - std::log2((double)std::max<int64_t>(K, 1))) * 0.5 - 1e-9);
+  return std::min(62, t);
+}
+
+bool encode_map_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)IG_BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+struct OzWork {
+  int8_t* xq = nullptr; int64_t xq_cap = 0;
+  int8_t* yq = nullptr; int64_t yq_cap = 0;
+  uint8_t* rq = nullptr; int64_t rq_cap = 0;
+  int* ex = nullptr; int64_t ex_cap = 0;
+  int* ey = nullptr; int64_t ey_cap = 0;
+  void release() {
+    for (void* q : {(void*)xq, (void*)yq, (void*)rq, (void*)ex, (void*)ey})
+      if (q) cudaFree(q);
+    xq = yq = nullptr; rq = nullptr; ex = ey = nullptr;
+    xq_cap = yq_cap = rq_cap = ex_cap = ey_cap = 0;
+  }
+};
+
+// Workspace of one emulated GEMM: X planes (n·M·ldq), Y planes of one chunk
+// of nc rows (n·nc·ldq), residues (n·M·ldr).
+struct OzPlan {
+  int64_t K = 0, ldq = 0, nc = 0, ldr = 0;
+  int64_t xq = 0, yq = 0, rq = 0, ex = 0, ey = 0;
+};
+OzPlan oz_plan(const GemmOp& op, int n) {
+  OzPlan pl;
+  for (int i = 0; i < op.nseg; ++i) pl.K += op.seg[i].len;
+  pl.ldq = round_up(std::max<int64_t>(pl.K, 1), 16);
+  int64_t nc = (int64_t)(g_oz_budget / ((double)n * pl.ldq));
+  nc = std::max<int64_t>(IG_BN, nc / IG_BN * IG_BN);
+  if (op.lower) nc = op.N;              // the lower-tile mask needs the whole N range
+  pl.nc = std::min<int64_t>(op.N, nc);
+  pl.ldr = round_up(pl.nc, 16);
+  pl.xq = n * op.M * pl.ldq;
+  pl.yq = n * pl.nc * pl.ldq;
+  pl.rq = n * op.M * pl.ldr;
+  pl.ex = op.M;
+  pl.ey = pl.nc;
+  return pl;
+}
+bool oz_eligible(const GemmOp& op) {
+  return !op.xt && !op.yt && !op.peers && !op.cidx && !op.partial && op.nseg >= 1 && op.M > 0 && op.N > 0;
+}
+template <class T>
+int oz_grow(T** p, int64_t* cap, int64_t need, size_t* bytes) {
+  if (need <= *cap) return IBMI_OK;
+  if (*p) { cudaFree(*p); *bytes -= (size_t)(*cap) * sizeof(T); }
+  *p = nullptr;
+  *cap = 0;
+  CUDA_TRY(cudaMalloc(p, (size_t)need * sizeof(T)));
+  *cap = need;
+  *bytes += (size_t)need * sizeof(T);
+  return IBMI_OK;
+}
+int oz_reserve(OzWork& w, const OzPlan& pl, size_t* bytes) {
+  if (oz_grow(&w.xq, &w.xq_cap, pl.xq, bytes) || oz_grow(&w.yq, &w.yq_cap, pl.yq, bytes) ||
+      oz_grow(&w.rq, &w.rq_cap, pl.rq, bytes) || oz_grow(&w.ex, &w.ex_cap, pl.ex, bytes) ||
+      oz_grow(&w.ey, &w.ey_cap, pl.ey, bytes))
+    return IBMI_ERR_OOM;
+  return IBMI_OK;
+}
+
+RowMap map_shift(const RowMap& m, int64_t j0) {
+  if (m.idx) return list_map(m.idx + j0);
+  if (j0 >= m.split) return RowMap{INT_MAX, m.off1 + (j0 - m.split), 0, nullptr};
+  return RowMap{(int)(m.split - j0), m.off0 + j0, m.off1, nullptr};
+}
+
+cudaError_t oz_convert(const double* X, int64_t ld, RowMap rm, RowMap km, int64_t R, int64_t K, int t, int* ex,
+                       int n, int8_t* Q, int64_t ldq, cudaStream_t s) {
+  oz_rowexp_kernel<<<(unsigned)((R * 32 + 255) / 256), 256, 0, s>>>(X, ld, rm, km, (int)R, (int)K, t, ex);
+  note_launch();
+  const int64_t chunks = ldq / 16;
+  dim3 grid((unsigned)((chunks + 255) / 256), (unsigned)R);
+  oz_split_kernel<<<grid, 256, 0, s>>>(X, ld, rm, km, (int)R, (int)K, ex, n, Q, ldq, R * ldq);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// C = epilogue(X·Yᵀ) through n INT8 residue GEMMs.  The caller reserved the
+// workspace for oz_plan(op, n) (nothing is allocated here: graph capture).
+cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s) {
+  if (!oz_eligible(op) || n < OZ_MINN || n > OZ_MAXN || !tma_encoder()) return cudaErrorInvalidValue;
+  const OzPlan pl = oz_plan(op, n);
+  if (pl.xq > w.xq_cap || pl.yq > w.yq_cap || pl.rq > w.rq_cap || pl.ex > w.ex_cap || pl.ey > w.ey_cap ||
+      op.M > 65535 || pl.nc > 65535)
+    return cudaErrorInvalidValue;
+  cudaError_t e = oz_upload_tables();
+  if (e != cudaSuccess) return e;
+  const int t = oz_bits(n, pl.K);
+  const RowMap xk{op.nseg == 2 ? op.seg[0].len : INT_MAX, op.seg[0].x0, op.nseg == 2 ? op.seg[1].x0 : 0, nullptr};
+  const RowMap yk{op.nseg == 2 ? op.seg[0].len : INT_MAX, op.seg[0].y0, op.nseg == 2 ? op.seg[1].y0 : 0, nullptr};
+  e = oz_convert(op.X, op.ldx, op.xm, xk, op.M, pl.K, t, w.ex, n, w.xq, pl.ldq, s);
+  if (e != cudaSuccess) return e;
+  // epilogue description shared with the DMMA kernels
+  GemmParams P;
+  memset(&P, 0, sizeof(P));
+  P.M = (int)op.M; P.N = (int)op.N;
+  P.C = op.C; P.ldc = op.ldc; P.cm = op.cm; P.cn = op.cn;
+  P.alpha = op.alpha; P.beta = op.beta;
+  P.D = op.D ? op.D : op.C; P.ldd = op.D ? op.ldd : op.ldc; P.dm = op.dm; P.dn = op.dn;
+  P.mirror = op.mirror; P.lower = op.lower;
+  if (op.c2_set) { P.C2 = op.C2; P.ldc2 = op.ldc2; P.c2m = op.c2m; P.c2n = op.c2n; }
+  else { P.C2 = op.C; P.ldc2 = op.ldc; P.c2m = op.cm; P.c2n = op.cn; }
+  P.direct = op.direct ? 1 : 0;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(igemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap mx, my;
+  if (!encode_map_u8(&mx, w.xq, n * op.M, pl.K, pl.ldq, IG_BM)) return cudaErrorInvalidValue;
+  for (int64_t j0 = 0; j0 < op.N; j0 += pl.nc) {
+    const int64_t nc = std::min<int64_t>(pl.nc, op.N - j0);
+    e = oz_convert(op.Y, op.ldy, map_shift(op.yn, j0), yk, nc, pl.K, t, w.ey, n, w.yq, pl.ldq, s);
+    if (e != cudaSuccess) return e;
+    if (!encode_map_u8(&my, w.yq, n * nc, pl.K, pl.ldq, IG_BN)) return cudaErrorInvalidValue;
+    IgemmParams G;
+    memset(&G, 0, sizeof(G));
+    G.M = (int)op.M; G.N = (int)nc; G.K = (int)pl.K;
+    G.tiles_m = (int)((op.M + IG_BM - 1) / IG_BM);
+    G.tiles_n = (int)((nc + IG_BN - 1) / IG_BN);
+    G.planes = n;
+    G.R = w.rq; G.ldr = pl.ldr; G.r_plane = op.M * pl.ldr;
+    for (int l = 0; l < n; ++l) G.mod[l] = g_oz_host[n - OZ_MINN].m[l];
+    G.rows_per_plane_x = (int)op.M;
+    G.rows_per_plane_y = (int)nc;
+    G.lower = op.lower ? 1 : 0;
+    const int total = G.tiles_m * G.tiles_n * n;
+    igemm_tc_kernel<<<std::min(total, sms), IG_THREADS, IG_SMEM, s>>>(mx, my, G);
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    OzCrt E;
+    E.R = w.rq; E.ldr = pl.ldr; E.rplane = op.M * pl.ldr;
+    E.ex = w.ex; E.ey = w.ey; E.n = n; E.M = (int)op.M; E.ncols = (int)nc; E.j_off = (int)j0;
+    dim3 cg((unsigned)((nc + 127) / 128), (unsigned)((op.M + 31) / 32));
+    oz_crt_kernel<<<cg, 256, 0, s>>>(P, E);
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // ------------------------------------------------------ host <-> device staging
@@ -727,6 +977,7 @@ struct ibmi_ctx {
   double* vr = nullptr; int64_t vr_n = 0;
   double* frob_part = nullptr; int frob_cap = 0;
   double* splitws = nullptr; int64_t splitws_cap = 0;   // split-K partial tiles
+  OzWork oz;                      // Ozaki-II planes / residues (g_oz_n > 0)
   int graph_gen = -1;
   long long graph_launches = 0;   // kernel nodes in the captured sweep
   double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
@@ -840,13 +1091,15 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k1.C = c->S; k1.ldc = c->ld; k1.cm = contig_map(lo); k1.cn = complement_map(lo, hi);
   k1.alpha = -1.0; k1.mirror = true;
   k1.tma_ok = true; k1.xrows = b; k1.xcols = p; k1.yrows = p; k1.ycols = p;
-  {
+  if (g_oz_n > 0) {
+    CUDA_TRY(oz_gemm(k1, c->oz, g_oz_n, c->sms, c->stream));
+  } else {
     int64_t need = 0;
     k1.splits = plan_split(c, k1, g_split_panel, &need);
     if (need > c->splitws_cap) k1.splits = 1;
     k1.ws = c->splitws;
+    CUDA_TRY(launch_gemm(k1, c->stream));
   }
-  CUDA_TRY(launch_gemm(k1, c->stream));
   if (mid) CUDA_TRY(cudaEventRecord(mid, c->stream));
   // K2: Σ[I, I] = A_II⁻¹ − Σ[I, c] W_cᵀ   (= ainv + M Wᵀ), lower tiles mirrored
   GemmOp k2;
@@ -930,6 +1183,21 @@ int plan_workspace(ibmi_ctx* c) {
   }
   if (need > c->splitws_cap) {
     if (ensure_buf(&c->splitws, &c->splitws_cap, need, &c->bytes)) return IBMI_ERR_OOM;
+  }
+  if (g_oz_n > 0) {
+    OzPlan tot;
+    for (const SetDev& s : c->sets) {
+      if (s.general) continue;
+      GemmOp k1;
+      k1.M = s.b; k1.N = c->p - s.b;
+      k1.add_seg(0, 0, s.lo);
+      k1.add_seg(s.hi, s.hi, c->p - s.hi);
+      const OzPlan pl = oz_plan(k1, g_oz_n);
+      tot.xq = std::max(tot.xq, pl.xq); tot.yq = std::max(tot.yq, pl.yq); tot.rq = std::max(tot.rq, pl.rq);
+      tot.ex = std::max(tot.ex, pl.ex); tot.ey = std::max(tot.ey, pl.ey);
+    }
+    int rc = oz_reserve(c->oz, tot, &c->bytes);
+    if (rc) return rc;
   }
   return IBMI_OK;
 }
@@ -1146,6 +1414,7 @@ int ibmi_destroy(ibmi_ctx* c) {
     if (s.comp) cudaFree(s.comp);
   }
   c->cs.release();
+  c->oz.release();
   for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal, c->splitws})
     if (q) cudaFree(q);
   if (c->hpin) cudaFreeHost(c->hpin);
@@ -1899,6 +2168,38 @@ int ibmi_dgemm_nt(int64_t m, int64_t n, int64_t k, double alpha, const double* x
   return IBMI_OK;
 }
 
+int ibmi_dgemm_nt_ozaki(int64_t m, int64_t n, int64_t k, double alpha, const double* x, int64_t ldx,
+                        const double* y, int64_t ldy, double* c, int64_t ldc, int moduli, void* stream) {
+  if (m < 0 || n < 0 || k < 0) return fail(IBMI_ERR_DIM, "negative dimension");
+  if (!x || !y || !c) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (moduli < OZ_MINN || moduli > OZ_MAXN) return fail(IBMI_ERR_INVALID, "moduli must be in [8, 20]");
+  if (m > 65535 || n > INT_MAX || k > (1 << 17)) return fail(IBMI_ERR_DIM, "m <= 65535 and k <= 131072 required");
+  if (m == 0 || n == 0) return IBMI_OK;
+  GemmOp op;
+  op.X = x; op.ldx = ldx;
+  op.Y = y; op.ldy = ldy;
+  op.M = m; op.N = n;
+  op.add_seg(0, 0, k);
+  op.C = c; op.ldc = ldc;
+  op.alpha = alpha;
+  if (k == 0) { op.nseg = 1; op.seg[0] = KSeg{0, 0, 0}; }
+  static std::mutex mu;
+  static OzWork work;
+  static size_t bytes = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  int sms = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  int rc = oz_reserve(work, oz_plan(op, moduli), &bytes);
+  if (rc) return rc;
+  CUDA_TRY(oz_gemm(op, work, moduli, sms, st));
+  CUDA_TRY(cudaStreamSynchronize(st));   // the shared workspace is reused by the next call
+  return IBMI_OK;
+}
+
 int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
                      void* stream) {
   if (n < 1) return fail(IBMI_ERR_DIM, "matrix must be nonempty");
@@ -2176,6 +2477,15 @@ int ibmi_tune(int key, int value) {
     case 6:
       if (value < 1 || value > 64) return fail(IBMI_ERR_INVALID, "min k-tiles per split must be in [1, 64]");
       g_split_min_kt = value;
+      break;
+    case 7:
+      if (value != 0 && (value < OZ_MINN || value > OZ_MAXN))
+        return fail(IBMI_ERR_INVALID, "Ozaki moduli must be 0 (FP64 DMMA) or in [8, 20]");
+      g_oz_n = value;
+      break;
+    case 8:
+      if (value < 64) return fail(IBMI_ERR_INVALID, "Ozaki chunk budget must be >= 64 MB");
+      g_oz_budget = (double)value * 1048576.0;
       break;
     default:
       return fail(IBMI_ERR_INVALID, "unknown tuning key");

@@ -110,6 +110,23 @@ def dgemm_nt(x, y, alpha: float = 1.0, beta: float = 0.0, c=None):
     return c
 
 
+def dgemm_nt_ozaki(x, y, moduli: int = 18, alpha: float = 1.0):
+    """``alpha · x · yᵀ`` by Ozaki-II emulation on the INT8 tensor cores
+    (``ibmi_dgemm_nt_ozaki``): ``moduli`` exact residue GEMMs, CRT, one FP64
+    rounding; accurate to 2^-t of each row's largest entry."""
+    torch = _torch()
+    m, k = x.shape
+    n, k2 = y.shape
+    if k != k2:
+        raise DimensionMismatch(f"inner dimensions differ: {tuple(x.shape)} vs {tuple(y.shape)}")
+    c = torch.zeros((m, n), dtype=torch.float64, device=x.device)
+    rc = _abi.lib().ibmi_dgemm_nt_ozaki(m, n, k, float(alpha), C.c_void_p(x.data_ptr()), x.stride(0),
+                                        C.c_void_p(y.data_ptr()), y.stride(0), C.c_void_p(c.data_ptr()),
+                                        c.stride(0), int(moduli), _stream(x))
+    _abi.check(rc, "dgemm_nt_ozaki")
+    return c
+
+
 def matmul(a, b):
     """``a @ b`` in float64 (linalg.py:175-183) on the device (a·(bᵀ)ᵀ)."""
     a = as_matrix(a)

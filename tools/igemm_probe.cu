@@ -1,0 +1,185 @@
+// Standalone probe of the tcgen05 INT8 GEMM (csrc/igemm_tc.cuh): exactness
+// against a scalar int32 reference and throughput at the c4 panel shape.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
+//        -o tools/igemm_probe tools/igemm_probe.cu -lcuda
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "../paper_2502_06377_b200/csrc/igemm_tc.cuh"
+
+using namespace ibmi;
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      printf("CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      exit(1);                                                                       \
+    }                                                                                \
+  } while (0)
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+
+static void make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)IG_BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    printf("encode failed %d\n", (int)r);
+    exit(1);
+  }
+}
+
+__global__ void ref_kernel(const int8_t* x, const int8_t* y, int M, int N, int K, int64_t ld, int32_t* c) {
+  int n = blockIdx.x * blockDim.x + threadIdx.x, m = blockIdx.y;
+  if (n >= N) return;
+  int32_t s = 0;
+  for (int k = 0; k < K; ++k) s += (int32_t)x[(int64_t)m * ld + k] * (int32_t)y[(int64_t)n * ld + k];
+  c[(int64_t)m * N + n] = s;
+}
+
+__global__ void fill_kernel(int8_t* p, int64_t n, uint32_t seed) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    p[i] = (int8_t)(h & 0xff);
+  }
+}
+
+int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
+  const int64_t ld = (K + 15) / 16 * 16;
+  const int64_t rx = (int64_t)(M + IG_BM - 1) / IG_BM * IG_BM, ry = (int64_t)(N + IG_BN - 1) / IG_BN * IG_BN;
+  int8_t *x, *y;
+  CK(cudaMalloc(&x, rx * ld * planes));
+  CK(cudaMalloc(&y, ry * ld * planes));
+  CK(cudaMemset(x, 0, rx * ld * planes));
+  CK(cudaMemset(y, 0, ry * ld * planes));
+  fill_kernel<<<1024, 256>>>(x, rx * ld * planes, 1234);
+  fill_kernel<<<1024, 256>>>(y, ry * ld * planes, 99);
+  // zero K padding columns and padding rows of every plane so planes are exact
+  CK(cudaDeviceSynchronize());
+  {
+    std::vector<int8_t> hx(rx * ld * planes), hy(ry * ld * planes);
+    CK(cudaMemcpy(hx.data(), x, hx.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hy.data(), y, hy.size(), cudaMemcpyDeviceToHost));
+    for (int l = 0; l < planes; ++l) {
+      for (int64_t r = 0; r < rx; ++r)
+        for (int64_t k = 0; k < ld; ++k)
+          if (r >= M || k >= K) hx[(l * rx + r) * ld + k] = 0;
+      for (int64_t r = 0; r < ry; ++r)
+        for (int64_t k = 0; k < ld; ++k)
+          if (r >= N || k >= K) hy[(l * ry + r) * ld + k] = 0;
+    }
+    CK(cudaMemcpy(x, hx.data(), hx.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(y, hy.data(), hy.size(), cudaMemcpyHostToDevice));
+  }
+  CUtensorMap mx, my;
+  make_map(&mx, x, rx * planes, K, ld, IG_BM);
+  make_map(&my, y, ry * planes, K, ld, IG_BN);
+  IgemmParams P{};
+  P.M = M;
+  P.N = N;
+  P.K = K;
+  P.tiles_m = (M + IG_BM - 1) / IG_BM;
+  P.tiles_n = (N + IG_BN - 1) / IG_BN;
+  P.planes = planes;
+  P.rows_per_plane_x = (int)rx;
+  P.rows_per_plane_y = (int)ry;
+  const int64_t ldr = (N + 15) / 16 * 16;
+  uint8_t* R;
+  int32_t* C32;
+  CK(cudaMalloc(&R, (int64_t)M * ldr * planes));
+  CK(cudaMalloc(&C32, (int64_t)M * N * 4));
+  P.R = R;
+  P.ldr = ldr;
+  P.r_plane = (int64_t)M * ldr;
+  P.C32 = C32;
+  P.ldc32 = N;
+  for (int l = 0; l < planes; ++l) P.mod[l] = mod;
+  CK(cudaFuncSetAttribute(igemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG_SMEM));
+  int sms;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int total = P.tiles_m * P.tiles_n * planes;
+  const int grid = total < sms ? total : sms;
+  igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  int bad = 0;
+  if (check) {
+    int32_t* Cr;
+    CK(cudaMalloc(&Cr, (int64_t)M * N * 4));
+    ref_kernel<<<dim3((N + 127) / 128, M), 128>>>(x, y, M, N, K, ld, Cr);
+    CK(cudaDeviceSynchronize());
+    std::vector<int32_t> a((int64_t)M * N), b((int64_t)M * N);
+    CK(cudaMemcpy(b.data(), Cr, b.size() * 4, cudaMemcpyDeviceToHost));
+    if (mod == 0) {
+      CK(cudaMemcpy(a.data(), C32, a.size() * 4, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < (int64_t)M * N; ++i)
+        if (a[i] != b[i]) {
+          if (bad < 5) printf("  mismatch at %lld,%lld: %d vs %d\n", (long long)(i / N), (long long)(i % N), a[i], b[i]);
+          ++bad;
+        }
+    } else {
+      std::vector<uint8_t> rr((int64_t)M * ldr);
+      CK(cudaMemcpy(rr.data(), R, rr.size(), cudaMemcpyDeviceToHost));
+      for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) {
+          int e = b[m * N + n] % mod;
+          if (e < 0) e += mod;
+          if (rr[m * ldr + n] != e) {
+            if (bad < 5) printf("  mismatch at %lld,%lld: %d vs %d\n", (long long)m, (long long)n, rr[m * ldr + n], e);
+            ++bad;
+          }
+        }
+    }
+    CK(cudaFree(Cr));
+  }
+  float ms = 0;
+  if (reps > 0) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int i = 0; i < 2; ++i) igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+    CK(cudaEventRecord(e0));
+    for (int i = 0; i < reps; ++i) igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    ms /= reps;
+  }
+  const double ops = 2.0 * M * N * (double)K * planes;
+  printf("M=%d N=%d K=%d planes=%d mod=%d grid=%d: %s%d bad; %.3f ms  %.1f TOPS\n", M, N, K, planes, mod, grid,
+         check ? "" : "(unchecked) ", bad, ms, reps > 0 ? ops / ms * 1e-9 : 0.0);
+  CK(cudaFree(x));
+  CK(cudaFree(y));
+  CK(cudaFree(R));
+  CK(cudaFree(C32));
+  return bad;
+}
+
+int main(int argc, char** argv) {
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q));
+  int bad = 0;
+  bad += run(128, 256, 128, 1, 0, true, 0);
+  bad += run(256, 512, 1024, 1, 0, true, 0);
+  bad += run(300, 700, 1000, 1, 0, true, 0);
+  bad += run(1000, 1100, 2000, 2, 251, true, 0);
+  bad += run(640, 1280, 4096, 3, 256, true, 0);
+  printf("correctness: %s\n", bad ? "FAIL" : "ok");
+  run(2560, 14080, 14080, 1, 251, false, 5);
+  run(2560, 14080, 14080, 4, 251, false, 3);
+  run(8192, 8192, 8192, 1, 0, false, 5);
+  run(8192, 8192, 8192, 1, 251, false, 5);
+  return bad ? 1 : 0;
+}
