@@ -161,6 +161,14 @@ int ibmi_dgemm_nt(int64_t m, int64_t n, int64_t k, double alpha, const double* x
 int ibmi_dgemm_nt_ozaki(int64_t m, int64_t n, int64_t k, double alpha, const double* x, int64_t ldx,
                         const double* y, int64_t ldy, double* c, int64_t ldc, int moduli, void* stream);
 
+/* FP64 emulation of the context's hot GEMMs (panel, Σ_II and error-estimate
+ * GEMMs of contiguous sets): moduli = 0 keeps the FP64 DMMA kernels (default);
+ * 8..20 runs each of them as that many exact INT8 tcgen05 GEMMs of residues
+ * (Ozaki-II, see ibmi_dgemm_nt_ozaki).  Residue planes of the constant
+ * operands (W_k, rows of A) are cached when HBM allows. */
+int ibmi_set_emulation(ibmi_ctx* ctx, int moduli);
+int ibmi_get_emulation(ibmi_ctx* ctx, int* moduli);
+
 /* out = A⁻¹ for SPD A (n×n) via blocked Cholesky; replaces spd_inverse
  * (linalg.py:122-130).  On IBMI_ERR_NOT_SPD *fail_pivot = elimination step. */
 int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
@@ -246,8 +254,8 @@ long long ibmi_launch_count(void);
  * key 3: TMA/mbarrier kernel on/off; key 4: split-K of the panel and estimate GEMMs;
  * key 5: cluster (DSMEM) power iteration for Gram order <= 640 on/off;
  * key 6: minimum k-tiles per split-K slice (default 4);
- * key 7: Ozaki-II FP64 emulation of the panel GEMM on the INT8 tensor cores:
- *        0 = off (FP64 DMMA, default), 8..20 = number of moduli;
+ * key 7: default of ibmi_set_emulation for contexts created afterwards
+ *        (0 = FP64 DMMA, 8..20 = Ozaki-II moduli);
  * key 8: Ozaki residue-plane budget per N chunk, MB (default 5722 = 6e9 B). */
 int ibmi_tune(int key, int value);
 

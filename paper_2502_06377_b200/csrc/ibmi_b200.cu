@@ -394,16 +394,14 @@ void oz_build_tables() {
       const uint32_t m = (uint32_t)kOzModuli[i];
       T.m[i] = (int)m;
       T.invm[i] = 1.0f / (float)m;
-      uint32_t pw[8];
-      uint64_t v = 1 % m;
-      for (int b = 0; b < 8; ++b) {
-        pw[b] = (uint32_t)v;
-        v = (v * 256) % m;
-      }
-      // v = 2^64 mod m now
-      T.cneg[i] = (int)((m - (uint32_t)v) % m);
-      T.cpow[i][0] = pw[0] | (pw[1] << 8) | (pw[2] << 16) | (pw[3] << 24);
-      T.cpow[i][1] = pw[4] | (pw[5] << 8) | (pw[6] << 16) | (pw[7] << 24);
+      T.k21[i] = (uint32_t)((1ull << 21) % m);
+      T.k42[i] = (uint32_t)((1ull << 42) % m);
+      int sh = 0;
+      while ((2u << sh) <= m) ++sh;                  // sh = floor(log2 m)
+      if ((m & (m - 1)) == 0) --sh;                  // power of two: magic 2^(32+sh)/m exact, < 2^32
+      T.sh[i] = sh;
+      T.magic[i] = (uint32_t)(((1ull << (32 + sh)) + m - 1) / m);
+      T.bias[i] = (int)(m * (((1u << 30) + m - 1) / m));
       Big Pl;
       Pl.l[0] = 1;
       for (int j = 0; j < n; ++j)
@@ -414,7 +412,7 @@ void oz_build_tables() {
         if ((uint64_t)a * t % m == 1) { y = t; break; }
       Pl.mul(y);
       memcpy(T.w[i], Pl.l, sizeof(T.w[i]));
-      T.f[i] = Pl.to_double() / Pd;
+      T.f[i] = (float)(Pl.to_double() / Pd);
     }
   }
   g_oz_host_ready = true;
@@ -518,29 +516,14 @@ cudaError_t oz_convert(const double* X, int64_t ld, RowMap rm, RowMap km, int64_
                        int n, int8_t* Q, int64_t ldq, cudaStream_t s) {
   oz_rowexp_kernel<<<(unsigned)((R * 32 + 255) / 256), 256, 0, s>>>(X, ld, rm, km, (int)R, (int)K, t, ex);
   note_launch();
-  const int64_t chunks = ldq / 16;
-  dim3 grid((unsigned)((chunks + 255) / 256), (unsigned)R);
-  oz_split_kernel<<<grid, 256, 0, s>>>(X, ld, rm, km, (int)R, (int)K, ex, n, Q, ldq, R * ldq);
+  const int64_t chunks = ldq / OZ_SPLIT_V;
+  dim3 grid((unsigned)((chunks + 255) / 256), (unsigned)std::min<int64_t>(R, 65535));
+  OZ_DISPATCH(n, oz_split_launch, grid, s, X, ld, rm, km, (int)R, (int)K, ex, Q, ldq, R * ldq);
   note_launch();
   return cudaGetLastError();
 }
 
-// C = epilogue(X·Yᵀ) through n INT8 residue GEMMs.  The caller reserved the
-// workspace for oz_plan(op, n) (nothing is allocated here: graph capture).
-cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s) {
-  if (!oz_eligible(op) || n < OZ_MINN || n > OZ_MAXN || !tma_encoder()) return cudaErrorInvalidValue;
-  const OzPlan pl = oz_plan(op, n);
-  if (pl.xq > w.xq_cap || pl.yq > w.yq_cap || pl.rq > w.rq_cap || pl.ex > w.ex_cap || pl.ey > w.ey_cap ||
-      op.M > 65535 || pl.nc > 65535)
-    return cudaErrorInvalidValue;
-  cudaError_t e = oz_upload_tables();
-  if (e != cudaSuccess) return e;
-  const int t = oz_bits(n, pl.K);
-  const RowMap xk{op.nseg == 2 ? op.seg[0].len : INT_MAX, op.seg[0].x0, op.nseg == 2 ? op.seg[1].x0 : 0, nullptr};
-  const RowMap yk{op.nseg == 2 ? op.seg[0].len : INT_MAX, op.seg[0].y0, op.nseg == 2 ? op.seg[1].y0 : 0, nullptr};
-  e = oz_convert(op.X, op.ldx, op.xm, xk, op.M, pl.K, t, w.ex, n, w.xq, pl.ldq, s);
-  if (e != cudaSuccess) return e;
-  // epilogue description shared with the DMMA kernels
+GemmParams oz_epilogue(const GemmOp& op) {
   GemmParams P;
   memset(&P, 0, sizeof(P));
   P.M = (int)op.M; P.N = (int)op.N;
@@ -551,43 +534,149 @@ cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s)
   if (op.c2_set) { P.C2 = op.C2; P.ldc2 = op.ldc2; P.c2m = op.c2m; P.c2n = op.c2n; }
   else { P.C2 = op.C; P.ldc2 = op.ldc; P.c2m = op.cm; P.c2n = op.cn; }
   P.direct = op.direct ? 1 : 0;
+  return P;
+}
+
+// INT8 residue GEMMs + CRT epilogue of one N chunk [j0, j0 + nc).
+cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t* xq, const int* ex, const int8_t* yq,
+                     const int* ey, int64_t K, int64_t ldq, int64_t j0, int64_t nc, uint8_t* rq, int sms,
+                     cudaStream_t s) {
   static bool attr = false;
+  cudaError_t e;
   if (!attr) {
     e = cudaFuncSetAttribute(igemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG_SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   CUtensorMap mx, my;
-  if (!encode_map_u8(&mx, w.xq, n * op.M, pl.K, pl.ldq, IG_BM)) return cudaErrorInvalidValue;
+  if (!encode_map_u8(&mx, xq, n * op.M, K, ldq, IG_BM) || !encode_map_u8(&my, yq, n * nc, K, ldq, IG_BN))
+    return cudaErrorInvalidValue;
+  const int64_t ldr = round_up(nc, 16);
+  IgemmParams G;
+  memset(&G, 0, sizeof(G));
+  G.M = (int)op.M; G.N = (int)nc; G.K = (int)K;
+  G.tiles_m = (int)((op.M + IG_BM - 1) / IG_BM);
+  G.tiles_n = (int)((nc + IG_BN - 1) / IG_BN);
+  G.planes = n;
+  G.R = rq; G.ldr = ldr; G.r_plane = op.M * ldr;
+  for (int l = 0; l < n; ++l) G.mod[l] = g_oz_host[n - OZ_MINN].m[l];
+  G.rows_per_plane_x = (int)op.M;
+  G.rows_per_plane_y = (int)nc;
+  G.lower = (op.lower && j0 == 0) ? 1 : 0;
+  const int total = G.tiles_m * G.tiles_n * n;
+  igemm_tc_kernel<<<std::min(total, sms), IG_THREADS, IG_SMEM, s>>>(mx, my, G);
+  note_launch();
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  OzCrt E;
+  E.R = rq; E.ldr = ldr; E.rplane = op.M * ldr;
+  E.ex = ex; E.ey = ey; E.n = n; E.M = (int)op.M; E.ncols = (int)nc; E.j_off = (int)j0;
+  dim3 cg((unsigned)((nc + 127) / 128), (unsigned)((op.M + 31) / 32));
+  OZ_DISPATCH(n, oz_crt_launch, cg, s, P, E);
+  note_launch();
+  return cudaGetLastError();
+}
+
+bool oz_fits(const GemmOp& op, const OzWork& w, int n) {
+  const OzPlan pl = oz_plan(op, n);
+  return oz_eligible(op) && pl.xq <= w.xq_cap && pl.yq <= w.yq_cap && pl.rq <= w.rq_cap && pl.ex <= w.ex_cap &&
+         pl.ey <= w.ey_cap && op.M <= 65535 && pl.nc <= 65535;
+}
+
+// Residue planes converted earlier (a cache or the previous GEMM's operand):
+// plane l of row r at q + (l*rows + r)*ldq, exponents e[r].
+struct OzPre {
+  const int8_t* q = nullptr;
+  const int* e = nullptr;
+};
+
+// K map of an operand: logical k -> column, from the GEMM's K segments.
+inline RowMap oz_kmap(const GemmOp& op, bool y) {
+  if (op.nseg == 2) return RowMap{op.seg[0].len, y ? op.seg[0].y0 : op.seg[0].x0, y ? op.seg[1].y0 : op.seg[1].x0, nullptr};
+  return RowMap{INT_MAX, y ? op.seg[0].y0 : op.seg[0].x0, 0, nullptr};
+}
+
+// C = epilogue(X·Yᵀ) through n INT8 residue GEMMs.  The caller reserved the
+// workspace (nothing is allocated here: graph capture).  xp / yp: operand
+// planes already converted (same n, K map and K); x_in_ybuf: convert X into
+// the Y buffers (when yp points at the X buffers of the previous call).
+cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s, OzPre xp = OzPre(),
+                    OzPre yp = OzPre(), bool x_in_ybuf = false) {
+  if (!oz_eligible(op) || n < OZ_MINN || n > OZ_MAXN || !tma_encoder()) return cudaErrorInvalidValue;
+  const OzPlan pl = oz_plan(op, n);
+  if (op.M > 65535 || op.N > 65535) return cudaErrorInvalidValue;
+  const int64_t xneed = n * op.M * pl.ldq;
+  if (!xp.q) {
+    if (x_in_ybuf ? (xneed > w.yq_cap || op.M > w.ey_cap) : (xneed > w.xq_cap || op.M > w.ex_cap))
+      return cudaErrorInvalidValue;
+  }
+  if (yp.q ? (n * op.M * round_up(op.N, 16) > w.rq_cap)
+           : (x_in_ybuf || pl.yq > w.yq_cap || pl.ey > w.ey_cap || pl.rq > w.rq_cap))
+    return cudaErrorInvalidValue;
+  cudaError_t e = oz_upload_tables();
+  if (e != cudaSuccess) return e;
+  const int t = oz_bits(n, pl.K);
+  const GemmParams P = oz_epilogue(op);
+  if (!xp.q) {
+    int8_t* q = x_in_ybuf ? w.yq : w.xq;
+    int* ex = x_in_ybuf ? w.ey : w.ex;
+    e = oz_convert(op.X, op.ldx, op.xm, oz_kmap(op, false), op.M, pl.K, t, ex, n, q, pl.ldq, s);
+    if (e != cudaSuccess) return e;
+    xp.q = q;
+    xp.e = ex;
+  }
+  if (yp.q) return oz_chunk(op, P, n, xp.q, xp.e, yp.q, yp.e, pl.K, pl.ldq, 0, op.N, w.rq, sms, s);
   for (int64_t j0 = 0; j0 < op.N; j0 += pl.nc) {
     const int64_t nc = std::min<int64_t>(pl.nc, op.N - j0);
-    e = oz_convert(op.Y, op.ldy, map_shift(op.yn, j0), yk, nc, pl.K, t, w.ey, n, w.yq, pl.ldq, s);
+    e = oz_convert(op.Y, op.ldy, map_shift(op.yn, j0), oz_kmap(op, true), nc, pl.K, t, w.ey, n, w.yq, pl.ldq, s);
     if (e != cudaSuccess) return e;
-    if (!encode_map_u8(&my, w.yq, n * nc, pl.K, pl.ldq, IG_BN)) return cudaErrorInvalidValue;
-    IgemmParams G;
-    memset(&G, 0, sizeof(G));
-    G.M = (int)op.M; G.N = (int)nc; G.K = (int)pl.K;
-    G.tiles_m = (int)((op.M + IG_BM - 1) / IG_BM);
-    G.tiles_n = (int)((nc + IG_BN - 1) / IG_BN);
-    G.planes = n;
-    G.R = w.rq; G.ldr = pl.ldr; G.r_plane = op.M * pl.ldr;
-    for (int l = 0; l < n; ++l) G.mod[l] = g_oz_host[n - OZ_MINN].m[l];
-    G.rows_per_plane_x = (int)op.M;
-    G.rows_per_plane_y = (int)nc;
-    G.lower = op.lower ? 1 : 0;
-    const int total = G.tiles_m * G.tiles_n * n;
-    igemm_tc_kernel<<<std::min(total, sms), IG_THREADS, IG_SMEM, s>>>(mx, my, G);
-    note_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    OzCrt E;
-    E.R = w.rq; E.ldr = pl.ldr; E.rplane = op.M * pl.ldr;
-    E.ex = w.ex; E.ey = w.ey; E.n = n; E.M = (int)op.M; E.ncols = (int)nc; E.j_off = (int)j0;
-    dim3 cg((unsigned)((nc + 127) / 128), (unsigned)((op.M + 31) / 32));
-    oz_crt_kernel<<<cg, 256, 0, s>>>(P, E);
-    note_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = oz_chunk(op, P, n, xp.q, xp.e, w.yq, w.ey, pl.K, pl.ldq, j0, nc, w.rq, sms, s);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// Residue planes of a constant operand (W_k, rows of A), kept across sweeps.
+struct OzCache {
+  int8_t* q = nullptr;
+  int* e = nullptr;
+  int n = 0;
+  size_t bytes = 0;
+  void release() {
+    if (q) cudaFree(q);
+    if (e) cudaFree(e);
+    q = nullptr;
+    e = nullptr;
+    n = 0;
+    bytes = 0;
+  }
+  OzPre pre() const { OzPre p; p.q = q; p.e = e; return p; }
+};
+
+// Convert op's X (y = false) or Y (y = true) operand into a cache if the
+// device has `margin` bytes to spare afterwards.  Returns false (no cache) otherwise.
+bool oz_cache_build(OzCache& cc, const GemmOp& op, bool y, int n, size_t margin, cudaStream_t s, size_t* ctx_bytes) {
+  const OzPlan pl = oz_plan(op, n);
+  const int64_t rows = y ? op.N : op.M;
+  const size_t need = (size_t)n * rows * pl.ldq + (size_t)rows * sizeof(int);
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || fr < need + margin) { cudaGetLastError(); return false; }
+  if (cudaMalloc(&cc.q, (size_t)n * rows * pl.ldq) != cudaSuccess) { cudaGetLastError(); cc.q = nullptr; return false; }
+  if (cudaMalloc(&cc.e, (size_t)rows * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(cc.q);
+    cc.q = nullptr;
+    cc.e = nullptr;
+    return false;
+  }
+  if (oz_upload_tables() != cudaSuccess) { cc.release(); return false; }
+  const int t = oz_bits(n, pl.K);
+  cudaError_t e = y ? oz_convert(op.Y, op.ldy, op.yn, oz_kmap(op, true), rows, pl.K, t, cc.e, n, cc.q, pl.ldq, s)
+                    : oz_convert(op.X, op.ldx, op.xm, oz_kmap(op, false), rows, pl.K, t, cc.e, n, cc.q, pl.ldq, s);
+  if (e != cudaSuccess) { cc.release(); return false; }
+  cc.n = n;
+  cc.bytes = need;
+  *ctx_bytes += need;
+  return true;
 }
 
 // ------------------------------------------------------ host <-> device staging
@@ -977,7 +1066,11 @@ struct ibmi_ctx {
   double* vr = nullptr; int64_t vr_n = 0;
   double* frob_part = nullptr; int frob_cap = 0;
   double* splitws = nullptr; int64_t splitws_cap = 0;   // split-K partial tiles
-  OzWork oz;                      // Ozaki-II planes / residues (g_oz_n > 0)
+  OzWork oz;                      // Ozaki-II planes / residues (oz_n > 0)
+  int oz_n = 0;                   // 0: FP64 DMMA GEMMs; 8..20: Ozaki-II with oz_n moduli
+  std::vector<OzCache> oz_w;      // per set: residue planes of W_k (K = complement)
+  OzCache oz_a;                   // residue planes of A[c_K, :] (error estimate of the last set)
+  int oz_a_set = -1;
   int graph_gen = -1;
   long long graph_launches = 0;   // kernel nodes in the captured sweep
   double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
@@ -1004,6 +1097,17 @@ int ensure_buf(double** p, int64_t* cap, int64_t need, size_t* bytes) {
   *cap = need;
   *bytes += (size_t)need * 8;
   return IBMI_OK;
+}
+
+void oz_drop_caches(ibmi_ctx* c) {
+  for (auto& w : c->oz_w) {
+    c->bytes -= w.bytes;
+    w.release();
+  }
+  c->oz_w.clear();
+  c->bytes -= c->oz_a.bytes;
+  c->oz_a.release();
+  c->oz_a_set = -1;
 }
 
 void invalidate_graph(ibmi_ctx* c) {
@@ -1091,8 +1195,9 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k1.C = c->S; k1.ldc = c->ld; k1.cm = contig_map(lo); k1.cn = complement_map(lo, hi);
   k1.alpha = -1.0; k1.mirror = true;
   k1.tma_ok = true; k1.xrows = b; k1.xcols = p; k1.yrows = p; k1.ycols = p;
-  if (g_oz_n > 0) {
-    CUDA_TRY(oz_gemm(k1, c->oz, g_oz_n, c->sms, c->stream));
+  const bool wcache = c->oz_n > 0 && k < (int)c->oz_w.size() && c->oz_w[k].q && c->oz_w[k].n == c->oz_n;
+  if (c->oz_n > 0) {
+    CUDA_TRY(oz_gemm(k1, c->oz, c->oz_n, c->sms, c->stream, wcache ? c->oz_w[k].pre() : OzPre()));
   } else {
     int64_t need = 0;
     k1.splits = plan_split(c, k1, g_split_panel, &need);
@@ -1112,6 +1217,17 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k2.alpha = -1.0; k2.beta = 1.0; k2.D = s.ainv; k2.ldd = s.ldb;
   k2.lower = true; k2.mirror = true;
   k2.tma_ok = true; k2.xrows = p; k2.xcols = p; k2.yrows = b; k2.ycols = p;
+  if (c->oz_n > 0) {   // W's residue planes (cache, or K1's X buffers) are K2's Y
+    if (wcache) {
+      CUDA_TRY(oz_gemm(k2, c->oz, c->oz_n, c->sms, c->stream, OzPre(), c->oz_w[k].pre()));
+    } else {
+      OzPre wp;
+      wp.q = c->oz.xq;
+      wp.e = c->oz.ex;
+      CUDA_TRY(oz_gemm(k2, c->oz, c->oz_n, c->sms, c->stream, OzPre(), wp, /*x_in_ybuf=*/true));
+    }
+    return IBMI_OK;
+  }
   int64_t need = 0;
   k2.splits = plan_split(c, k2, g_split_diag, &need);
   if (need > c->splitws_cap) k2.splits = 1;    // workspace is planned by plan_workspace()
@@ -1184,7 +1300,8 @@ int plan_workspace(ibmi_ctx* c) {
   if (need > c->splitws_cap) {
     if (ensure_buf(&c->splitws, &c->splitws_cap, need, &c->bytes)) return IBMI_ERR_OOM;
   }
-  if (g_oz_n > 0) {
+  if (c->oz_n > 0) {
+    const int n = c->oz_n;
     OzPlan tot;
     for (const SetDev& s : c->sets) {
       if (s.general) continue;
@@ -1192,12 +1309,64 @@ int plan_workspace(ibmi_ctx* c) {
       k1.M = s.b; k1.N = c->p - s.b;
       k1.add_seg(0, 0, s.lo);
       k1.add_seg(s.hi, s.hi, c->p - s.hi);
-      const OzPlan pl = oz_plan(k1, g_oz_n);
+      const OzPlan pl = oz_plan(k1, n);
+      tot.xq = std::max(tot.xq, pl.xq); tot.yq = std::max(tot.yq, pl.yq); tot.rq = std::max(tot.rq, pl.rq);
+      tot.ex = std::max(tot.ex, pl.ex); tot.ey = std::max(tot.ey, pl.ey);
+      // K2 (y_pre): X = Σ[I, c] into the Y buffers, residues b × b
+      tot.yq = std::max(tot.yq, n * s.b * pl.ldq);
+      tot.ey = std::max(tot.ey, (int64_t)s.b);
+      tot.rq = std::max(tot.rq, n * s.b * round_up(s.b, 16));
+    }
+    if (!c->sets.empty() && !c->sets.back().general) {
+      const SetDev& s = c->sets.back();
+      GemmOp gb;
+      gb.M = s.b; gb.N = c->p - s.b;
+      gb.add_seg(0, 0, c->p);
+      const OzPlan pl = oz_plan(gb, n);
       tot.xq = std::max(tot.xq, pl.xq); tot.yq = std::max(tot.yq, pl.yq); tot.rq = std::max(tot.rq, pl.rq);
       tot.ex = std::max(tot.ex, pl.ex); tot.ey = std::max(tot.ey, pl.ey);
     }
     int rc = oz_reserve(c->oz, tot, &c->bytes);
     if (rc) return rc;
+    // constant operands: W_k (all sets) and A[c_K, :] keep their planes when
+    // the device has room (margin 4 GB); otherwise they are converted per use
+    if (c->oz_w.size() != c->sets.size()) {
+      for (auto& w : c->oz_w) w.release();
+      c->oz_w.assign(c->sets.size(), OzCache());
+    }
+    const size_t margin = (size_t)4 << 30;
+    for (size_t k = 0; k < c->sets.size(); ++k) {
+      const SetDev& s = c->sets[k];
+      OzCache& wc = c->oz_w[k];
+      if (s.general || !s.ready || (wc.q && wc.n == n)) continue;
+      c->bytes -= wc.bytes;
+      wc.release();
+      GemmOp k1;
+      k1.X = s.W; k1.ldx = c->ld; k1.xm = contig_map(0);
+      k1.M = s.b; k1.N = c->p - s.b;
+      k1.add_seg(0, 0, s.lo);
+      k1.add_seg(s.hi, s.hi, c->p - s.hi);
+      if (!oz_cache_build(wc, k1, false, n, margin, c->stream, &c->bytes)) break;
+    }
+    const int last = (int)c->sets.size() - 1;
+    if (last >= 0 && !c->sets[last].general && !(c->oz_a.q && c->oz_a.n == n && c->oz_a_set == last)) {
+      c->bytes -= c->oz_a.bytes;
+      c->oz_a.release();
+      c->oz_a_set = -1;
+      const SetDev& s = c->sets[last];
+      GemmOp gb;
+      gb.Y = c->A; gb.ldy = c->ld; gb.yn = s.cmap();
+      gb.M = s.b; gb.N = c->p - s.b;
+      gb.add_seg(0, 0, c->p);
+      if (oz_cache_build(c->oz_a, gb, true, n, margin, c->stream, &c->bytes)) c->oz_a_set = last;
+    }
+    if (c->oz_a.q) {   // the cached estimate runs as one N chunk: residues b × c
+      const SetDev& s = c->sets[last];
+      OzPlan more;
+      more.rq = n * s.b * round_up(c->p - s.b, 16);
+      rc = oz_reserve(c->oz, more, &c->bytes);
+      if (rc) return rc;
+    }
   }
   return IBMI_OK;
 }
@@ -1318,13 +1487,17 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   gb.add_seg(0, 0, p);
   gb.C = c->Bm; gb.ldc = c->ldB;
   gb.tma_ok = true; gb.xrows = p; gb.xcols = p; gb.yrows = p; gb.ycols = p;
-  {
+  if (c->oz_n > 0 && !s.general && oz_fits(gb, c->oz, c->oz_n)) {
+    const bool acache = c->oz_a_set == k && c->oz_a.q && c->oz_a.n == c->oz_n &&
+                        c->oz_n * b * round_up(cc, 16) <= c->oz.rq_cap;
+    CUDA_TRY(oz_gemm(gb, c->oz, c->oz_n, c->sms, c->stream, OzPre(), acache ? c->oz_a.pre() : OzPre()));
+  } else {
     int64_t need = 0;
     gb.splits = plan_split(c, gb, g_split_panel, &need);
     if (need > c->splitws_cap) gb.splits = 1;
     gb.ws = c->splitws;
+    CUDA_TRY(launch_gemm(gb, c->stream));
   }
-  CUDA_TRY(launch_gemm(gb, c->stream));
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
   NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
               c->power_smem_cap, c->splitws, c->splitws_cap, c->sms};
@@ -1386,6 +1559,7 @@ int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
     c->own_stream = true;
   }
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  c->oz_n = g_oz_n;
   prepare_gemm_attributes();
   power_launch_shape(device, &c->power_blocks, &c->power_threads, &c->power_smem_cap);
   const size_t mat = (size_t)p * c->ld * sizeof(double);
@@ -1415,6 +1589,8 @@ int ibmi_destroy(ibmi_ctx* c) {
   }
   c->cs.release();
   c->oz.release();
+  for (auto& w : c->oz_w) w.release();
+  c->oz_a.release();
   for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal, c->splitws})
     if (q) cudaFree(q);
   if (c->hpin) cudaFreeHost(c->hpin);
@@ -1440,6 +1616,9 @@ int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
   c->a_set = true;
   for (auto& s : c->sets) s.ready = false;
   invalidate_graph(c);
+  c->bytes -= c->oz_a.bytes;
+  c->oz_a.release();
+  c->oz_a_set = -1;
   int rc = symcheck(c, contig_map(0), p, "matrix");
   if (rc) { c->a_set = false; return rc; }
   return IBMI_OK;
@@ -1461,6 +1640,7 @@ int ibmi_set_partition(ibmi_ctx* c, int k, const int64_t* lo, const int64_t* hi)
     if (s.comp) cudaFree(s.comp);
     if (s.W) c->bytes -= (size_t)s.b * c->ld * 8 + (size_t)s.b * s.ldb * 8;
   }
+  oz_drop_caches(c);
   c->sets.assign(k, SetDev());
   for (int j = 0; j < k; ++j) {
     c->sets[j].lo = lo[j];
@@ -1533,6 +1713,10 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   if (count == 0) return IBMI_OK;
   const int64_t p = c->p;
   cudaStream_t st = c->stream;
+  for (int j = first; j < first + count && j < (int)c->oz_w.size(); ++j) {
+    c->bytes -= c->oz_w[j].bytes;
+    c->oz_w[j].release();
+  }
 
   // 1. symmetry of every A_II (linalg.py:68-77), one sync for all sets
   unsigned long long* dsym = nullptr;
@@ -2197,6 +2381,25 @@ int ibmi_dgemm_nt_ozaki(int64_t m, int64_t n, int64_t k, double alpha, const dou
   if (rc) return rc;
   CUDA_TRY(oz_gemm(op, work, moduli, sms, st));
   CUDA_TRY(cudaStreamSynchronize(st));   // the shared workspace is reused by the next call
+  return IBMI_OK;
+}
+
+int ibmi_set_emulation(ibmi_ctx* c, int moduli) {
+  if (!c) return fail(IBMI_ERR_INVALID, "null context");
+  if (moduli != 0 && (moduli < OZ_MINN || moduli > OZ_MAXN))
+    return fail(IBMI_ERR_INVALID, "moduli must be 0 (FP64 DMMA) or in [8, 20]");
+  if (moduli == c->oz_n) return IBMI_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->oz_n = moduli;
+  oz_drop_caches(c);
+  invalidate_graph(c);
+  return IBMI_OK;
+}
+
+int ibmi_get_emulation(ibmi_ctx* c, int* moduli) {
+  if (!c || !moduli) return fail(IBMI_ERR_INVALID, "null argument");
+  *moduli = c->oz_n;
   return IBMI_OK;
 }
 

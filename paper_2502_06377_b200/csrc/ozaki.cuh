@@ -30,10 +30,13 @@ struct OzTable {
   int n;
   int m[OZ_MAXN];
   float invm[OZ_MAXN];
-  uint32_t cpow[OZ_MAXN][2];     // bytes i=0..3 / 4..7: 2^(8i) mod m, packed for dp4a
-  int cneg[OZ_MAXN];             // (-2^64) mod m: two's-complement correction of a negative int64
+  uint32_t k21[OZ_MAXN];         // 2^21 mod m
+  uint32_t k42[OZ_MAXN];         // 2^42 mod m
+  uint32_t magic[OZ_MAXN];       // ceil(2^(32+sh)/m): floor(s/m) = umulhi(s, magic) >> sh for s < 2^31
+  int sh[OZ_MAXN];
+  int bias[OZ_MAXN];             // m·ceil(2^30/m): makes a signed limb sum non-negative, ≡ 0 mod m
   uint32_t w[OZ_MAXN][OZ_LIMBS]; // CRT weights (P/m_l)·((P/m_l)^-1 mod m_l) < P
-  double f[OZ_MAXN];             // w_l / P
+  float f[OZ_MAXN];              // w_l / P (fp32 suffices: q = rint(Σ r_l f_l) needs |error| < 1/4)
   uint32_t P[OZ_LIMBS];
   double log2P;
 };
@@ -59,58 +62,85 @@ __global__ void oz_rowexp_kernel(const double* __restrict__ X, int64_t ld, RowMa
   if (lane == 0) ex[warp] = mx > 0.0 ? t - 1 - ilogb(mx) : 0;
 }
 
-// residue of a two's-complement int64 v modulo table entry l, in [0, m)
-__device__ __forceinline__ int oz_mod(const OzTable& T, int l, uint64_t v) {
-  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
-  int s = (int)__dp4a(lo, T.cpow[l][0], __dp4a(hi, T.cpow[l][1], 0u));
-  s += ((int64_t)v < 0) ? T.cneg[l] : 0;          // s < 8*255*255 + 256 < 2^20: exact in fp32
-  const int m = T.m[l];
-  int q = __float2int_rz((float)s * T.invm[l]);
-  int r = s - q * m;
-  r += r < 0 ? m : 0;
-  r -= r >= m ? m : 0;
-  return r;
+// |rint(x · 2^e)| as an unsigned integer (<= 2^62 by the choice of e), by
+// integer operations on the IEEE fields (no ldexp / F2I.S64).  Subnormals and
+// zero give 0.
+__device__ __forceinline__ uint64_t oz_scaled_mag(double x, int e) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(x);
+  const int E = (int)((bits >> 52) & 0x7ff);
+  if (E == 0) return 0;
+  const uint64_t mant = (bits & 0xfffffffffffffull) | 0x10000000000000ull;
+  const int s = E - 1075 + e;                   // x = ±mant · 2^(E-1075)
+  if (s >= 0) return mant << s;
+  if (s < -54) return 0;
+  return (mant + (1ull << (-s - 1))) >> (-s);
 }
 
-// ---- step 2: residue planes.  Thread = (row r, 16 consecutive logical k);
+// symmetric residue (|r| <= m/2) of the signed a = c0 + c1·2^21 + c2·2^42
+// (|c0|, |c1| < 2^21, |c2| < 2^20) modulo entry l: the limb sum plus a bias
+// ≡ 0 (mod m) lies in [0, 2^31), where the multiply-high division is exact.
+// Rounding the quotient of s + (m-1)/2 gives the symmetric remainder directly.
+__device__ __forceinline__ int oz_sym_residue(const OzTable& T, int l, int c0, int c1, int c2) {
+  const uint32_t m = (uint32_t)T.m[l];
+  const uint32_t s = (uint32_t)(c2 * (int)T.k42[l] + T.bias[l] + c1 * (int)T.k21[l] + c0);
+  const uint32_t q = __umulhi(s + ((m - 1) >> 1), T.magic[l]) >> 7;   // every modulus is in [129, 256]
+  return (int)(s - q * m);
+}
+
+// ---- step 2: residue planes.  Thread = (row r, 8 consecutive logical k);
 // plane l of row r lives at Q + l*qplane + r*ldq.  Columns k >= K are zero.
-__global__ void __launch_bounds__(256) oz_split_kernel(const double* __restrict__ X, int64_t ld, RowMap rm,
-                                                       RowMap km, int R, int K, const int* __restrict__ ex, int n,
-                                                       int8_t* __restrict__ Q, int64_t ldq, int64_t qplane) {
-  const int r = blockIdx.y;
-  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * 16;
-  if (r >= R || k0 >= ldq) return;
-  const OzTable& T = c_oz[n - OZ_MINN];
-  const double* row = X + map_idx(rm, r) * ld;
-  const int e = ex[r];
-  int64_t v[16];
-  const bool fast = km.idx == nullptr && (km.split >= k0 + 16 || km.split <= k0) && k0 + 16 <= K;
-  if (fast) {
-    const double* q = row + map_idx(km, k0);
+constexpr int OZ_SPLIT_V = 8;
+template <int NM>
+__global__ void __launch_bounds__(256, 3) oz_split_kernel(const double* __restrict__ X, int64_t ld, RowMap rm,
+                                                          RowMap km, int R, int K, const int* __restrict__ ex,
+                                                          int8_t* __restrict__ Q, int64_t ldq, int64_t qplane) {
+  constexpr int V = OZ_SPLIT_V;
+  constexpr int n = NM;
+  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * V;
+  if (k0 >= ldq) return;
+  const OzTable& T = c_oz[NM - OZ_MINN];
+  for (int r = blockIdx.y; r < R; r += gridDim.y) {
+    const double* row = X + map_idx(rm, r) * ld;
+    const int e = ex[r];
+    double x[V];
+    const bool fast = km.idx == nullptr && (km.split >= k0 + V || km.split <= k0) && k0 + V <= K;
+    const double* q1 = row + map_idx(km, k0);
+    if (fast && (reinterpret_cast<uintptr_t>(q1) & 15) == 0) {
+      const double2* q = reinterpret_cast<const double2*>(q1);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __double2ll_rn(ldexp(q[i], e));
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = (k0 + i < K) ? __double2ll_rn(ldexp(row[map_idx(km, k0 + i)], e)) : 0;
-  }
-  int8_t* dst = Q + (int64_t)r * ldq + k0;
-#pragma unroll 1
-  for (int l = 0; l < n; ++l) {
-    const int m = T.m[l];
-    const int half = (m - 1) >> 1;
-    uint32_t w[4];
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      uint32_t pk = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        int x = oz_mod(T, l, (uint64_t)v[4 * g + b]);
-        x -= x > half ? m : 0;                       // symmetric residue: |x| <= 128
-        pk |= ((uint32_t)(x & 0xff)) << (8 * b);
+      for (int i = 0; i < V / 2; ++i) {
+        const double2 v = __ldcs(q + i);
+        x[2 * i] = v.x;
+        x[2 * i + 1] = v.y;
       }
-      w[g] = pk;
+    } else if (fast) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = q1[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) x[i] = (k0 + i < K) ? row[map_idx(km, k0 + i)] : 0.0;
     }
-    *reinterpret_cast<uint4*>(dst + (int64_t)l * qplane) = make_uint4(w[0], w[1], w[2], w[3]);
+    int c0[V], c1[V], c2[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const uint64_t a = oz_scaled_mag(x[i], e);
+      const int sg = x[i] < 0.0 ? -1 : 1;
+      c0[i] = sg * (int)((uint32_t)a & 0x1fffffu);
+      c1[i] = sg * (int)((uint32_t)(a >> 21) & 0x1fffffu);
+      c2[i] = sg * (int)(a >> 42);
+    }
+    int8_t* dst = Q + (int64_t)r * ldq + k0;
+#pragma unroll
+    for (int l = 0; l < NM; ++l) {
+      {
+        int v[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = oz_sym_residue(T, l, c0[i], c1[i], c2[i]);
+        const uint32_t w0 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+        const uint32_t w1 = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+        *reinterpret_cast<uint2*>(dst + (int64_t)l * qplane) = make_uint2(w0, w1);
+      }
+    }
   }
 }
 
@@ -124,21 +154,22 @@ struct OzCrt {
 };
 
 // Exact C' from n residues; returns C' · 2^-shift as FP64.
+template <int NM>
 __device__ __forceinline__ double oz_crt_value(const OzTable& T, const uint32_t* rs, int byte, int shift) {
   int64_t acc[OZ_LIMBS];
 #pragma unroll
   for (int k = 0; k < OZ_LIMBS; ++k) acc[k] = 0;
-  double fq = 0.0;
+  float fq = 0.0f;
 #pragma unroll
-  for (int l = 0; l < OZ_MAXN; ++l) {
-    if (l < T.n) {
+  for (int l = 0; l < NM; ++l) {
+    {
       const uint32_t r = (rs[l] >> (8 * byte)) & 0xffu;
 #pragma unroll
       for (int k = 0; k < OZ_LIMBS; ++k) acc[k] += (int64_t)((uint64_t)r * T.w[l][k]);
-      fq = fma((double)r, T.f[l], fq);
+      fq = fmaf((float)r, T.f[l], fq);
     }
   }
-  const int64_t q = (int64_t)rint(fq);
+  const int64_t q = (int64_t)rintf(fq);
 #pragma unroll
   for (int k = 0; k < OZ_LIMBS; ++k) acc[k] -= q * (int64_t)T.P[k];
 #pragma unroll
@@ -162,15 +193,19 @@ __device__ __forceinline__ double oz_crt_value(const OzTable& T, const uint32_t*
   double d = 0.0;
 #pragma unroll
   for (int k = OZ_LIMBS - 1; k >= 0; --k) d = fma(d, 4294967296.0, (double)L[k]);
-  return ldexp(neg ? -d : d, -shift);
+  d = neg ? -d : d;
+  const int be = 1023 - shift;                 // 2^-shift as a normal double when in range
+  if (be >= 1 && be <= 2046) return d * __longlong_as_double((int64_t)be << 52);
+  return ldexp(d, -shift);
 }
 
 // Block: 256 threads = 8 warps; tile 32 rows x 128 columns; thread = 4
 // consecutive columns of 4 rows.  Mirror stores go through a shared-memory
 // transpose so both stores are coalesced.
+template <int NM>
 __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const OzCrt E) {
   __shared__ double tile[32][129];
-  const OzTable& T = c_oz[E.n - OZ_MINN];
+  const OzTable& T = c_oz[NM - OZ_MINN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 128;
   const int jl = j0 + 4 * lane;
@@ -183,11 +218,10 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
     double v4[4] = {0.0, 0.0, 0.0, 0.0};
     bool ok4[4] = {false, false, false, false};
     if (i < E.M && jl < E.ncols) {
-      uint32_t rs[OZ_MAXN];
+      uint32_t rs[NM];
       const uint8_t* src = E.R + (int64_t)i * E.ldr + jl;
 #pragma unroll
-      for (int l = 0; l < OZ_MAXN; ++l)
-        rs[l] = l < E.n ? *reinterpret_cast<const uint32_t*>(src + (int64_t)l * E.rplane) : 0u;
+      for (int l = 0; l < NM; ++l) rs[l] = __ldcs(reinterpret_cast<const unsigned int*>(src + (int64_t)l * E.rplane));
       const int exi = E.ex[i];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -195,7 +229,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
         if (j >= E.ncols) break;
         const int n = E.j_off + j;
         if (P.lower && i < n) continue;
-        double v = P.alpha * oz_crt_value(T, rs, b, exi + E.ey[j]);
+        double v = P.alpha * oz_crt_value<NM>(T, rs, b, exi + E.ey[j]);
         if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, i) * P.ldd + map_idx(P.dn, n)];
         v4[b] = v;
         ok4[b] = true;
@@ -221,6 +255,34 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
     if (__double_as_longlong(v) == -1ll) continue;   // not computed (lower mask)
     P.C2[map_idx(P.c2n, E.j_off + j) * P.ldc2 + mc] = v;
   }
+}
+
+// n (moduli) -> template instance
+#define OZ_DISPATCH(n, F, ...)                  \
+  switch (n) {                                  \
+    case 8: F<8>(__VA_ARGS__); break;           \
+    case 9: F<9>(__VA_ARGS__); break;           \
+    case 10: F<10>(__VA_ARGS__); break;         \
+    case 11: F<11>(__VA_ARGS__); break;         \
+    case 12: F<12>(__VA_ARGS__); break;         \
+    case 13: F<13>(__VA_ARGS__); break;         \
+    case 14: F<14>(__VA_ARGS__); break;         \
+    case 15: F<15>(__VA_ARGS__); break;         \
+    case 16: F<16>(__VA_ARGS__); break;         \
+    case 17: F<17>(__VA_ARGS__); break;         \
+    case 18: F<18>(__VA_ARGS__); break;         \
+    case 19: F<19>(__VA_ARGS__); break;         \
+    default: F<20>(__VA_ARGS__); break;         \
+  }
+
+template <int NM>
+void oz_split_launch(dim3 grid, cudaStream_t s, const double* X, int64_t ld, RowMap rm, RowMap km, int R, int K,
+                     const int* ex, int8_t* Q, int64_t ldq, int64_t qplane) {
+  oz_split_kernel<NM><<<grid, 256, 0, s>>>(X, ld, rm, km, R, K, ex, Q, ldq, qplane);
+}
+template <int NM>
+void oz_crt_launch(dim3 grid, cudaStream_t s, const GemmParams& P, const OzCrt& E) {
+  oz_crt_kernel<NM><<<grid, 256, 0, s>>>(P, E);
 }
 
 }  // namespace ibmi

@@ -157,6 +157,16 @@ class DeviceSolver:
             _abi.check(self._L.ibmi_set_restart_vector(self._h, n, _abi.dbl_ptr(v)), "set_restart_vector")
             self._restart_n = n
 
+    def set_emulation(self, moduli: int):
+        """0: FP64 DMMA GEMMs; 8..20: Ozaki-II emulation with that many moduli."""
+        _abi.check(self._L.ibmi_set_emulation(self._h, int(moduli)), "set_emulation")
+
+    @property
+    def emulation(self) -> int:
+        n = C.c_int()
+        _abi.check(self._L.ibmi_get_emulation(self._h, C.byref(n)), "get_emulation")
+        return n.value
+
     def setup(self, first: int = 0, count: int = -1):
         fs, fp = C.c_int(-1), C.c_int64(-1)
         rc = self._L.ibmi_setup(self._h, first, count, C.byref(fs), C.byref(fp))

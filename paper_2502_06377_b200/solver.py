@@ -10,7 +10,10 @@ Extensions (all optional, defaults reproduce the reference):
 * ``IbmiConfig.initial_guess="jacobi"``: Σ₀[c₁,c₁] = diag(1/A_ii) (BASELINE c1/c2);
 * ``IbmiConfig.stopping="frobenius"``: stop on ‖I − AΣ‖_F < tol (BASELINE c2);
 * ``SolveReport.power_iterations`` / ``residual_trace`` / ``setup_seconds``;
-* ``solve(..., result_on_device=True)`` returns Σ as a CUDA tensor.
+* ``solve(..., result_on_device=True)`` returns Σ as a CUDA tensor;
+* ``IbmiConfig.gemm="ozaki"``: the hot GEMMs run as ``ozaki_moduli`` exact INT8
+  tensor-core GEMMs of residues (Ozaki-II FP64 emulation, ``ibmi_set_emulation``)
+  instead of FP64 DMMA; ``gemm=None`` keeps the library default (``ibmi_tune(7)``).
 """
 
 from __future__ import annotations
@@ -52,6 +55,7 @@ GUESS_TAKAHASHI = "takahashi"
 GUESS_JACOBI = "jacobi"
 GUESS_CHOICES = (GUESS_IDENTITY, GUESS_LOCAL_INVERSE, GUESS_MONTE_CARLO, GUESS_TAKAHASHI, GUESS_JACOBI)
 STOPPING_CHOICES = ("estimate", "frobenius")
+GEMM_CHOICES = (None, "dmma", "ozaki")
 
 
 @dataclass(frozen=True)
@@ -67,6 +71,8 @@ class IbmiConfig:
     norm_max_iters: int = POWER_MAX_ITERS
     stopping: str = "estimate"
     residual_every_sweep: bool = False
+    gemm: str | None = None
+    ozaki_moduli: int = 16
 
     def __post_init__(self):
         if not self.tol > 0:
@@ -80,6 +86,10 @@ class IbmiConfig:
             raise ValueError(f"mc_samples must be >= 1, got {self.mc_samples}")
         if self.stopping not in STOPPING_CHOICES:
             raise ValueError(f"unknown stopping rule {self.stopping!r}; expected one of {STOPPING_CHOICES}")
+        if self.gemm not in GEMM_CHOICES:
+            raise ValueError(f"unknown gemm {self.gemm!r}; expected one of {GEMM_CHOICES}")
+        if self.gemm == "ozaki" and not 8 <= self.ozaki_moduli <= 20:
+            raise ValueError(f"ozaki_moduli must be in [8, 20], got {self.ozaki_moduli}")
 
 
 @dataclass
@@ -216,6 +226,9 @@ def run_solve(ds: DeviceSolver, part: Partition, cfg: IbmiConfig, *, a=None, res
     """The sweep loop of ``solve`` (solver.py:241-278) on a prepared device state."""
     prof = os.environ.get("IBMI_PROFILE") is not None
     stopping = getattr(cfg, "stopping", "estimate")
+    gemm = getattr(cfg, "gemm", None)
+    if gemm is not None:
+        ds.set_emulation(int(getattr(cfg, "ozaki_moduli", 16)) if gemm == "ozaki" else 0)
     t0 = time.perf_counter()
     ds.setup()
     kind = _GUESS_KIND[cfg.initial_guess]

@@ -108,6 +108,22 @@ if __name__ == "__main__":
     if "timing" in what:
         timing()
     for w in what:
+        if w.startswith("profile:"):
+            _, nm, mod = w.split(":")
+            from paper_2502_06377_b200 import configs
+            from paper_2502_06377_b200.device import DeviceSolver
+            cfg = configs.get_config(nm)
+            a = torch.as_tensor(configs.make_matrix(nm), device=dev)
+            _abi.check(L.ibmi_tune(7, int(mod)))
+            ds = DeviceSolver(a, partition=cfg.partition())
+            ds.setup()
+            ds.init_sigma(1 if cfg.guess == "jacobi" else 0)
+            ds.sweep(1e-9, 5000)
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStart()
+            ds.sweep(1e-9, 5000)
+            torch.cuda.synchronize()
+            torch.cuda.cudart().cudaProfilerStop()
         if w.startswith("sweeps:"):
             _, nm, ns = w.split(":")
             sweeps(nm, int(ns))
