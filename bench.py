@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1 (diagnostic)")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance run")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"])
+    ap.add_argument("--gemm", default="dmma", choices=["dmma", "ozaki"],
+                    help="headline GEMM path: FP64 DMMA (default) or Ozaki-II INT8 emulation")
+    ap.add_argument("--moduli", type=int, default=16, help="Ozaki-II moduli (8..20)")
+    ap.add_argument("--no-alt", action="store_true", help="skip measuring the other GEMM path")
     return ap.parse_args()
 
 
@@ -212,6 +216,69 @@ def executed_flops(cfg):
     return tot + 2.0 * b * p * c + b * b * c
 
 
+INT8_PEAK_TOPS = 4500.0   # B200 dense INT8 tensor peak (nominal, B200_PROFILING.md: fp8/int8 4.5 P dense)
+
+
+def measure_single(solver, cfg, args, stream, guess, mode, moduli, setup_s0):
+    """Timed sweeps, per-kernel-class breakdown and time to tolerance of one
+    GEMM mode ("dmma" or "ozaki") on a prepared single-GPU DeviceSolver."""
+    import torch
+    from paper_2502_06377_b200 import _abi as abi_mod
+
+    L = abi_mod.lib()
+    t0 = time.perf_counter()
+    solver.set_emulation(moduli if mode == "ozaki" else 0)
+    solver.init_sigma(1 if guess == "jacobi" else 0)
+    for _ in range(args.warmup):          # first sweep also builds the residue-plane caches
+        solver.sweep(1e-9, 5000)
+    torch.cuda.synchronize()
+    errs = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = L.ibmi_launch_count()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            errs.append(solver.sweep(1e-9, 5000))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = L.ibmi_launch_count() - launches0
+    sigma = solver.sigma(on_device=True).clone() if cfg.p <= 32768 else None   # c5: Σ alone is 34 GB
+    # per-kernel-class device times (CUDA events on the same stream), best of 2
+    if mode == "ozaki":
+        abi_mod.check(L.ibmi_tune(9, 1))
+    timed = [solver.sweep_timed(1e-9, 5000)[3] for _ in range(2)]
+    kt = {k: min(t[k] for t in timed) for k in timed[0]}
+    igemm = None
+    if mode == "ozaki":
+        import ctypes as C
+
+        tms, tops, nl = C.c_double(), C.c_double(), C.c_int()
+        abi_mod.check(L.ibmi_emulation_timing(C.byref(tms), C.byref(tops), C.byref(nl)))
+        abi_mod.check(L.ibmi_tune(9, 0))
+        igemm = {"ms": tms.value / 2, "int8_ops": tops.value / 2, "launches": nl.value // 2}
+    ttt = None
+    if not args.no_ttt:
+        solver.init_sigma(1 if guess == "jacobi" else 0)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        n_to_tol = 0
+        for n_to_tol in range(1, cfg.max_iterations + 1):
+            e, _, _ = solver.sweep(1e-9, 5000)
+            # exact skip: ‖I − AΣ‖_F ≥ err, so the residual is needed only once err < tol
+            fr = solver.frobenius() if cfg.stopping == "frobenius" and e < 1.01 * cfg.tol else None
+            if cfg.stopping == "frobenius" and fr is None:
+                continue
+            if (fr < cfg.tol) if fr is not None else (e <= cfg.tol):
+                break
+        torch.cuda.synchronize()
+        ttt = {"seconds": setup_s0 + time.perf_counter() - t1, "sweeps": n_to_tol, "tol": cfg.tol,
+               "stopping": cfg.stopping, "setup_s": setup_s0}
+    return {"ms": ms, "sweeps_s": args.steps / (ms / 1e3), "errs": errs, "launches": launches, "kt": kt,
+            "igemm": igemm, "ttt": ttt, "sigma": sigma, "clocks": clk.summary(),
+            "switch_s": time.perf_counter() - t0}
+
+
 def run_ours(args):
     import torch
 
@@ -254,11 +321,29 @@ def run_ours(args):
         solver = DeviceSolver(a_dev, partition=part, device=dev, stream=stream.cuda_stream)
         del a_dev
         t0 = time.perf_counter()
+        solver.set_emulation(args.moduli if args.gemm == "ozaki" else 0)
         solver.setup()
         solver.init_sigma(1 if guess == "jacobi" else 0)
         torch.cuda.synchronize()
         setup_s = time.perf_counter() - t0
-        sweep = lambda: solver.sweep(1e-9, 5000)          # noqa: E731
+        head = measure_single(solver, cfg, args, stream, guess, args.gemm, args.moduli, setup_s)
+        alt = None
+        if not args.no_alt:
+            alt_mode = "ozaki" if args.gemm == "dmma" else "dmma"
+            alt = measure_single(solver, cfg, args, stream, guess, alt_mode, args.moduli, setup_s)
+            alt["sigma_rel_fro_vs_headline"] = (
+                float(torch.linalg.norm(alt["sigma"] - head["sigma"]) / torch.linalg.norm(head["sigma"]))
+                if head["sigma"] is not None else None)
+            alt["mode"] = alt_mode
+            del alt["sigma"]
+        del head["sigma"]
+        solver.close()
+        torch.cuda.empty_cache()
+        ms, errs, launches, kt, ttt = head["ms"], head["errs"], head["launches"], head["kt"], head["ttt"]
+        sweeps_s = head["sweeps_s"]
+        ms_step = ms / args.steps
+        consistent = None
+        clocks = head["clocks"]
     else:
         from paper_2502_06377_b200.distributed import ShardedSolver
 
@@ -269,65 +354,41 @@ def run_ours(args):
         setup_s = time.perf_counter() - t0
         del a_dev
         sweep = lambda: solver.sweep(1e-9, 5000)          # noqa: E731
-    for _ in range(args.warmup):
-        sweep()
-    errs = []
-    if world > 1 or args.sharded:
+        for _ in range(args.warmup):
+            sweep()
+        errs = []
         torch.distributed.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    from paper_2502_06377_b200 import _abi as abi_mod
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        from paper_2502_06377_b200 import _abi as abi_mod
 
-    launches0 = abi_mod.lib().ibmi_launch_count()
-    with ClockSampler(dev) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            errs.append(sweep())
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    launches = abi_mod.lib().ibmi_launch_count() - launches0
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    sweeps_s = args.steps / (ms / 1e3)
-    consistent = None
-    if world > 1:
-        # every rank must hold the same estimate (replicated power iteration on gathered B)
-        e_last = torch.tensor([errs[-1][0]], dtype=torch.float64, device=f"cuda:{dev}")
-        lo_, hi_ = e_last.clone(), e_last.clone()
-        torch.distributed.all_reduce(lo_, op=torch.distributed.ReduceOp.MIN)
-        torch.distributed.all_reduce(hi_, op=torch.distributed.ReduceOp.MAX)
-        consistent = bool(lo_.item() == hi_.item())
-    kt, panel_tf = None, None
-    if world == 1 and not args.sharded:
-        # per-kernel-class device times of one sweep (CUDA events on the same stream)
-        timed = [solver.sweep_timed(1e-9, 5000)[3] for _ in range(2)]
-        kt = {k: min(t[k] for t in timed) for k in timed[0]}
-        panel_flops = sum(2.0 * b * (p - b) ** 2 for b in sizes)
-        panel_tf = panel_flops / (kt["panel_gemm"] * 1e-3) / 1e12
-    # time to tolerance from a fresh Σ0 (setup included), same solver state machine
-    ttt = None
-    if world == 1 and not args.sharded and not args.no_ttt:
-        solver.init_sigma(1 if guess == "jacobi" else 0)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        n_to_tol = 0
-        for n_to_tol in range(1, cfg.max_iterations + 1):
-            e, _, _ = solver.sweep(1e-9, 5000)
-            # exact skip: ‖I − AΣ‖_F ≥ err, so the residual is needed only once err < tol
-            fr = solver.frobenius() if cfg.stopping == "frobenius" and e < 1.01 * cfg.tol else None
-            if cfg.stopping == "frobenius" and fr is None:
-                continue
-            if (fr < cfg.tol) if fr is not None else (e <= cfg.tol):
-                break
-        torch.cuda.synchronize()
-        ttt = {"seconds": setup_s + time.perf_counter() - t0, "sweeps": n_to_tol, "tol": cfg.tol,
-               "stopping": cfg.stopping, "setup_s": setup_s}
-    solver.close()
-    torch.cuda.empty_cache()
+        launches0 = abi_mod.lib().ibmi_launch_count()
+        with ClockSampler(dev) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                errs.append(sweep())
+            e1.record(stream)
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        launches = abi_mod.lib().ibmi_launch_count() - launches0
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        ms_step = ms / args.steps
+        sweeps_s = args.steps / (ms / 1e3)
+        consistent = None
+        if world > 1:
+            # every rank must hold the same estimate (replicated power iteration on gathered B)
+            e_last = torch.tensor([errs[-1][0]], dtype=torch.float64, device=f"cuda:{dev}")
+            lo_, hi_ = e_last.clone(), e_last.clone()
+            torch.distributed.all_reduce(lo_, op=torch.distributed.ReduceOp.MIN)
+            torch.distributed.all_reduce(hi_, op=torch.distributed.ReduceOp.MAX)
+            consistent = bool(lo_.item() == hi_.item())
+        kt, ttt, head, alt = None, None, None, None
+        clocks = clk.summary()
+        solver.close()
+        torch.cuda.empty_cache()
 
     e2e = None
     if not args.no_e2e and a_host is not None and rank == 0 and world == 1:
@@ -336,31 +397,59 @@ def run_ours(args):
         for _ in range(2):   # best of 2: the first call also pays one-time CUDA module/graph set-up
             t0 = time.perf_counter()
             rep = pkg.solve(a_host, part, pkg.IbmiConfig(tol=1e-300, max_iterations=args.steps,
-                                                         initial_guess=guess))
+                                                         initial_guess=guess, gemm=args.gemm,
+                                                         ozaki_moduli=args.moduli))
             walls.append(time.perf_counter() - t0)
             del rep.result
         wall = min(walls)
         e2e = {"value": args.steps / wall, "unit": "sweeps/s", "walls_s": walls,
                "h2d_bytes_per_step": int(p * p * 8 / args.steps),
                "d2h_bytes_per_step": int(p * p * 8 / args.steps) + 8,
-               "note": "solve(a_host, part, IbmiConfig(max_iterations=steps)) wall time incl. A upload, setup, "
-                       "sweeps, per-sweep error readback and Sigma download (best of 2 calls)"}
+               "note": f"solve(a_host, part, IbmiConfig(max_iterations=steps, gemm={args.gemm!r})) wall time incl. "
+                       "A upload, setup, sweeps, per-sweep error readback and Sigma download (best of 2 calls)"}
     cpu = None
     if not args.no_cpu_baseline and rank == 0 and world == 1 and a_host is not None:
         s = cpu_sample(cfg, a_host)
         cpu = {"value": 1.0 / s["sweep_s"], "unit": "sweeps/s", "cores": os.cpu_count(), "kind": "port",
                "sample": s["sample"], "setup_one_set_s": s["setup_one_set_s"]}
+
+    def roofline(mode, kt_, igemm_):
+        if kt_ is None:
+            return None
+        if mode == "ozaki":
+            ach = igemm_["int8_ops"] / (igemm_["ms"] * 1e-3) / 1e12 if igemm_ and igemm_["ms"] > 0 else None
+            return {"bound": "tensor", "kernel": "igemm_tc_kernel (INT8 residue GEMMs of the Ozaki-II emulation, "
+                                                 "tcgen05.mma kind::i8, TMA, TMEM)",
+                    "achieved": ach, "peak": INT8_PEAK_TOPS, "unit": "TOPS",
+                    "frac": ach / INT8_PEAK_TOPS if ach else None, "traffic": None,
+                    "launches_per_sweep": igemm_["launches"] if igemm_ else None,
+                    "kernel_ms_per_sweep": igemm_["ms"] if igemm_ else None,
+                    "peak_source": "nominal B200 dense INT8/FP8 tensor peak (B200_PROFILING.md); "
+                                   "achieved = algorithmic INT8 ops / CUDA-event time of every igemm launch of a sweep"}
+        panel_flops = sum(2.0 * b * (p - b) ** 2 for b in sizes)
+        panel_tf = panel_flops / (kt_["panel_gemm"] * 1e-3) / 1e12
+        return {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
+                "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s", "frac": panel_tf / peak,
+                "traffic": 6.50e9,
+                "traffic_note": "ncu dram read+write bytes of one interior-set panel GEMM launch "
+                                "(profiles/r01_c4_sweep.md); algorithmic minimum 2.38e9",
+                "peak_source": "measured on this box: DMMA m8n8k4 throughput probe (ibmi_probe_fp64_peak)"}
+
     if rank == 0:
         tf = flops * sweeps_s / 1e12
+        mode = args.gemm if world == 1 and not args.sharded else "dmma"
         line = {
             "metric": "IBMI sweeps/s (FP64) at p=16384" if args.config == "c4" else f"IBMI sweeps/s ({args.config})",
             "value": sweeps_s, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None,
+            "dtype": "f64" if mode == "dmma" else f"f64 via int8 (Ozaki-II, {args.moduli} moduli)",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {cfg.description}", "p": p, "sets": part.k,
                        "overlap": cfg.overlap, "set_sizes": sorted(set(sizes)),
                        "l2": "inputs (A, Sigma) exceed L2; no flush",
-                       "parallelism": f"row-panel sharded x{world}" if world > 1 else "single"},
+                       "parallelism": f"row-panel sharded x{world}" if world > 1 else "single",
+                       "gemm": mode},
             "tflops": tf,
             "tflops_frac_of_peak": tf / world / peak,
             "tflops_executed": executed_flops(cfg) * sweeps_s / 1e12,
@@ -372,20 +461,27 @@ def run_ours(args):
             "power_iterations": [e[1] for e in errs],
             "error_trace": [e[0] for e in errs],
             "kernel_ms_per_sweep": kt,
-            "roofline": {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
-                         "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s",
-                         "frac": panel_tf / peak if panel_tf else None,
-                         "traffic": 6.50e9,
-                         "traffic_note": "ncu dram read+write bytes of one interior-set panel GEMM launch "
-                                         "(profiles/r01_c4_sweep.md); algorithmic minimum 2.38e9",
-                         "peak_source": "measured on this box: DMMA m8n8k4 throughput probe (ibmi_probe_fp64_peak)"},
+            "roofline": roofline(mode, kt, head["igemm"] if head else None),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "gpu_launches_note": "kernels launched by libibmi_b200.so inside the timed region on rank 0 "
                                  "(graph replays count their kernel nodes)",
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
+        if alt is not None:
+            line["alt"] = {
+                "gemm": alt["mode"], "moduli": args.moduli if alt["mode"] == "ozaki" else None,
+                "value": alt["sweeps_s"], "unit": "sweeps/s", "ms_per_step": alt["ms"] / args.steps,
+                "tflops": flops * alt["sweeps_s"] / 1e12,
+                "tflops_frac_of_fp64_peak": flops * alt["sweeps_s"] / 1e12 / peak,
+                "sigma_rel_fro_vs_headline": alt["sigma_rel_fro_vs_headline"],
+                "error_trace": [e[0] for e in alt["errs"]],
+                "time_to_tol": alt["ttt"], "kernel_ms_per_sweep": alt["kt"],
+                "roofline": roofline(alt["mode"], alt["kt"], alt["igemm"]),
+                "gpu_launches": int(alt["launches"]), "clocks": alt["clocks"],
+                "note": "same context, same Sigma0 and sweep count; Sigma compared after warmup+steps sweeps",
+            }
         print(json.dumps(line), flush=True)
     if world > 1 or args.sharded:
         torch.distributed.destroy_process_group()

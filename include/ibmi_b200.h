@@ -168,6 +168,10 @@ int ibmi_dgemm_nt_ozaki(int64_t m, int64_t n, int64_t k, double alpha, const dou
  * operands (W_k, rows of A) are cached when HBM allows. */
 int ibmi_set_emulation(ibmi_ctx* ctx, int moduli);
 int ibmi_get_emulation(ibmi_ctx* ctx, int* moduli);
+/* With ibmi_tune(9, 1), every eagerly launched INT8 residue GEMM is bracketed
+ * by CUDA events on its stream; this returns (and clears) their summed device
+ * time, algorithmic INT8 ops and launch count (the emulated roofline). */
+int ibmi_emulation_timing(double* ms, double* int8_ops, int* launches);
 
 /* out = A⁻¹ for SPD A (n×n) via blocked Cholesky; replaces spd_inverse
  * (linalg.py:122-130).  On IBMI_ERR_NOT_SPD *fail_pivot = elimination step. */
@@ -256,7 +260,8 @@ long long ibmi_launch_count(void);
  * key 6: minimum k-tiles per split-K slice (default 4);
  * key 7: default of ibmi_set_emulation for contexts created afterwards
  *        (0 = FP64 DMMA, 8..20 = Ozaki-II moduli);
- * key 8: Ozaki residue-plane budget per N chunk, MB (default 5722 = 6e9 B). */
+ * key 8: Ozaki residue-plane budget per N chunk, MB (default 5722 = 6e9 B);
+ * key 9: event-time the INT8 GEMM launches (ibmi_emulation_timing) on/off. */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

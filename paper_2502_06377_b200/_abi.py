@@ -53,6 +53,7 @@ SIGNATURES = [
     ("ibmi_device_bytes", C.c_int, [_P, C.POINTER(_I64)]),
     ("ibmi_dgemm_nt", C.c_int, [_I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, C.c_double, _P, _I64, _P]),
     ("ibmi_set_emulation", C.c_int, [_P, C.c_int]),
+    ("ibmi_emulation_timing", C.c_int, [_P, _P, _P]),
     ("ibmi_get_emulation", C.c_int, [_P, _P]),
     ("ibmi_dgemm_nt_ozaki", C.c_int, [_I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, _P, _I64, C.c_int, _P]),
     ("ibmi_spd_inverse", C.c_int, [_I64, _P, _I64, _P, _I64, C.POINTER(_I64), _P]),

@@ -346,6 +346,9 @@ int auto_split(int tiles, int kt_total, int sms) {
 // (ozaki.cuh).  g_oz_n = 0 keeps every GEMM on the FP64 DMMA kernels; 8..20
 // routes the eligible hot GEMMs through n INT8 residue GEMMs on tcgen05.
 int g_oz_n = 0;
+bool g_oz_timing = false;      // ibmi_tune(9): event-time every INT8 GEMM launch (eager paths only)
+struct OzEvent { cudaEvent_t a, b; double ops; };
+std::vector<OzEvent> g_oz_events;
 double g_oz_budget = 6e9;      // bytes of Y residue planes per N chunk
 const int kOzModuli[OZ_MAXN] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227,
                                 223, 217, 211, 199, 197, 193, 191, 181, 179, 173};
@@ -564,8 +567,30 @@ cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t*
   G.rows_per_plane_y = (int)nc;
   G.lower = (op.lower && j0 == 0) ? 1 : 0;
   const int total = G.tiles_m * G.tiles_n * n;
+  cudaEvent_t tev[2] = {nullptr, nullptr};
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  const bool timing = g_oz_timing && cap == cudaStreamCaptureStatusNone;
+  if (timing) {   // per-launch CUDA events on the launching stream (never during graph capture)
+    cudaEventCreate(&tev[0]);
+    cudaEventCreate(&tev[1]);
+    cudaEventRecord(tev[0], s);
+  }
   igemm_tc_kernel<<<std::min(total, sms), IG_THREADS, IG_SMEM, s>>>(mx, my, G);
   note_launch();
+  if (timing) {
+    cudaEventRecord(tev[1], s);
+    // algorithmic INT8 ops of the launch (lower mode: the tiles it runs)
+    double ops = 2.0 * (double)op.M * (double)nc * (double)K * n;
+    if (G.lower) {
+      int64_t run = 0;
+      for (int tm = 0; tm < G.tiles_m; ++tm)
+        for (int tn = 0; tn < G.tiles_n; ++tn)
+          if (!(tn * IG_BN > tm * IG_BM + IG_BM - 1)) ++run;
+      ops *= (double)run / (double)(G.tiles_m * G.tiles_n);
+    }
+    g_oz_events.push_back({tev[0], tev[1], ops});
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   OzCrt E;
   E.R = rq; E.ldr = ldr; E.rplane = op.M * ldr;
@@ -2384,6 +2409,26 @@ int ibmi_dgemm_nt_ozaki(int64_t m, int64_t n, int64_t k, double alpha, const dou
   return IBMI_OK;
 }
 
+int ibmi_emulation_timing(double* ms, double* int8_ops, int* launches) {
+  double tms = 0.0, tops = 0.0;
+  int nl = 0;
+  int rc = IBMI_OK;
+  for (auto& e : g_oz_events) {
+    float m = 0.0f;
+    if (cudaEventSynchronize(e.b) != cudaSuccess || cudaEventElapsedTime(&m, e.a, e.b) != cudaSuccess) rc = IBMI_ERR_CUDA;
+    tms += m;
+    tops += e.ops;
+    ++nl;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  g_oz_events.clear();
+  if (ms) *ms = tms;
+  if (int8_ops) *int8_ops = tops;
+  if (launches) *launches = nl;
+  return rc == IBMI_OK ? IBMI_OK : fail(rc, "event timing failed");
+}
+
 int ibmi_set_emulation(ibmi_ctx* c, int moduli) {
   if (!c) return fail(IBMI_ERR_INVALID, "null context");
   if (moduli != 0 && (moduli < OZ_MINN || moduli > OZ_MAXN))
@@ -2686,6 +2731,9 @@ int ibmi_tune(int key, int value) {
         return fail(IBMI_ERR_INVALID, "Ozaki moduli must be 0 (FP64 DMMA) or in [8, 20]");
       g_oz_n = value;
       break;
+    case 9:
+      g_oz_timing = value != 0;
+      return IBMI_OK;          // no graph re-capture: timing applies to eager launches only
     case 8:
       if (value < 64) return fail(IBMI_ERR_INVALID, "Ozaki chunk budget must be >= 64 MB");
       g_oz_budget = (double)value * 1048576.0;

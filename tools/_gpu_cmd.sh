@@ -1,4 +1,4 @@
-timeout 600 python tools/ozaki_probe.py accuracy sweeps:c4:6 > gpurun_out/ozaki3.log 2>&1; echo rc=$?
-timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/oz_launches.csv python tools/ozaki_probe.py profile:c4:16 > gpurun_out/ncu_oz.log 2>&1; echo ncu=$?
-timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none -k regex:"oz_split|oz_crt" -c 4 -o gpurun_out/oz_full2 python tools/ozaki_probe.py profile:c4:16 > gpurun_out/ncu_oz_full.log 2>&1; echo ncufull=$?
-tail -12 gpurun_out/ozaki3.log
+timeout 900 python bench.py > gpurun_out/bench_c4.log 2>&1; echo bench=$?
+tail -1 gpurun_out/bench_c4.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); a=d.get('alt') or {}; print(d['value'], d['e2e'], d['roofline'], d['time_to_tol']); print(a.get('value'), a.get('sigma_rel_fro_vs_headline'), a.get('roofline'), a.get('time_to_tol'), a.get('kernel_ms_per_sweep'))"
+timeout 900 python bench.py --gemm ozaki --no-alt > gpurun_out/bench_c4_oz.log 2>&1; echo bench=$?
+tail -1 gpurun_out/bench_c4_oz.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'], d['roofline'], d['time_to_tol'], d['kernel_ms_per_sweep'])"
