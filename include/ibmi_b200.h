@@ -261,7 +261,11 @@ long long ibmi_launch_count(void);
  * key 7: default of ibmi_set_emulation for contexts created afterwards
  *        (0 = FP64 DMMA, 8..20 = Ozaki-II moduli);
  * key 8: Ozaki residue-plane budget per N chunk, MB (default 5722 = 6e9 B);
- * key 9: event-time the INT8 GEMM launches (ibmi_emulation_timing) on/off. */
+ * key 9: event-time the INT8 GEMM launches (ibmi_emulation_timing) on/off;
+ * key 10: N chunks of the two-stream emulated GEMM pipeline (default 1 = no overlap:
+ *         the conversion shares the L1/shared-memory datapath with the INT8
+ *         GEMM's operand reads, so overlapping them gained nothing);
+ * key 11: INT8 GEMM on CTA pairs (cta_group::2, default 1) or single CTAs (0). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

@@ -346,6 +346,8 @@ int auto_split(int tiles, int kt_total, int sms) {
 // (ozaki.cuh).  g_oz_n = 0 keeps every GEMM on the FP64 DMMA kernels; 8..20
 // routes the eligible hot GEMMs through n INT8 residue GEMMs on tcgen05.
 int g_oz_n = 0;
+int g_oz_pair = 1;             // 1: CTA-pair INT8 GEMM (cta_group::2, 256x256 tiles); 0: one CTA per 128x256 tile
+int g_sms_hint = 148;          // SM count of the device in use (bounded persistent grids)
 bool g_oz_timing = false;      // ibmi_tune(9): event-time every INT8 GEMM launch (eager paths only)
 struct OzEvent { cudaEvent_t a, b; double ops; };
 std::vector<OzEvent> g_oz_events;
@@ -468,23 +470,35 @@ struct OzWork {
 // Workspace of one emulated GEMM: X planes (n·M·ldq), Y planes of one chunk
 // of nc rows (n·nc·ldq), residues (n·M·ldr).
 struct OzPlan {
+  int nch = 1;
   int64_t K = 0, ldq = 0, nc = 0, ldr = 0;
   int64_t xq = 0, yq = 0, rq = 0, ex = 0, ey = 0;
 };
+// N chunks: at most the budget's worth of Y planes each; with pipelining
+// (g_oz_chunks > 1) at least g_oz_chunks chunks of >= 2 tiles, double-buffered
+// so the conversion of chunk j+1 and the CRT of chunk j-1 run on the aux stream
+// while the INT8 GEMM of chunk j runs on the main one.
+int g_oz_chunks = 1;
 OzPlan oz_plan(const GemmOp& op, int n) {
   OzPlan pl;
   for (int i = 0; i < op.nseg; ++i) pl.K += op.seg[i].len;
   pl.ldq = round_up(std::max<int64_t>(pl.K, 1), 16);
   int64_t nc = (int64_t)(g_oz_budget / ((double)n * pl.ldq));
   nc = std::max<int64_t>(IG_BN, nc / IG_BN * IG_BN);
+  if (g_oz_chunks > 1) {
+    const int64_t want = round_up((op.N + g_oz_chunks - 1) / g_oz_chunks, IG_BN);
+    if (want >= 2 * IG_BN) nc = std::min(nc, want);
+  }
   if (op.lower) nc = op.N;              // the lower-tile mask needs the whole N range
   pl.nc = std::min<int64_t>(op.N, nc);
+  pl.nch = (int)((op.N + pl.nc - 1) / pl.nc);
+  const int nbuf = pl.nch > 1 ? 2 : 1;
   pl.ldr = round_up(pl.nc, 16);
   pl.xq = n * op.M * pl.ldq;
-  pl.yq = n * pl.nc * pl.ldq;
-  pl.rq = n * op.M * pl.ldr;
+  pl.yq = nbuf * n * pl.nc * pl.ldq;
+  pl.rq = nbuf * n * op.M * pl.ldr;
   pl.ex = op.M;
-  pl.ey = pl.nc;
+  pl.ey = nbuf * pl.nc;
   return pl;
 }
 bool oz_eligible(const GemmOp& op) {
@@ -517,10 +531,15 @@ RowMap map_shift(const RowMap& m, int64_t j0) {
 
 cudaError_t oz_convert(const double* X, int64_t ld, RowMap rm, RowMap km, int64_t R, int64_t K, int t, int* ex,
                        int n, int8_t* Q, int64_t ldq, cudaStream_t s) {
-  oz_rowexp_kernel<<<(unsigned)((R * 32 + 255) / 256), 256, 0, s>>>(X, ld, rm, km, (int)R, (int)K, t, ex);
+  // bounded grids (2 blocks per SM) only when the conversion should co-reside with an INT8 GEMM
+  const int gmul = g_oz_chunks > 1 ? 2 : 32;
+  const int64_t rx = std::min<int64_t>((R * 32 + 255) / 256, (int64_t)gmul * g_sms_hint);
+  oz_carveout(oz_rowexp_kernel);
+  oz_rowexp_kernel<<<(unsigned)rx, 256, 0, s>>>(X, ld, rm, km, (int)R, (int)K, t, ex);
   note_launch();
-  const int64_t chunks = ldq / OZ_SPLIT_V;
-  dim3 grid((unsigned)((chunks + 255) / 256), (unsigned)std::min<int64_t>(R, 65535));
+  // persistent split: two 256-thread blocks per SM at most (co-resident with the INT8 GEMM)
+  const int64_t items = R * ((ldq + OZ_SPLIT_V * 256 - 1) / (OZ_SPLIT_V * 256));
+  dim3 grid((unsigned)std::min<int64_t>(items, (int64_t)gmul * g_sms_hint));
   OZ_DISPATCH(n, oz_split_launch, grid, s, X, ld, rm, km, (int)R, (int)K, ex, Q, ldq, R * ldq);
   note_launch();
   return cudaGetLastError();
@@ -540,19 +559,22 @@ GemmParams oz_epilogue(const GemmOp& op) {
   return P;
 }
 
-// INT8 residue GEMMs + CRT epilogue of one N chunk [j0, j0 + nc).
-cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t* xq, const int* ex, const int8_t* yq,
-                     const int* ey, int64_t K, int64_t ldq, int64_t j0, int64_t nc, uint8_t* rq, int sms,
-                     cudaStream_t s) {
+// INT8 residue GEMMs of one N chunk [j0, j0 + nc) into rq.
+cudaError_t oz_igemm(const GemmOp& op, int n, const int8_t* xq, const int8_t* yq, int64_t K, int64_t ldq, int64_t j0,
+                     int64_t nc, uint8_t* rq, int sms, cudaStream_t s) {
   static bool attr = false;
   cudaError_t e;
   if (!attr) {
     e = cudaFuncSetAttribute(igemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG_SMEM);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(igemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG2_SMEM);
+    if (e != cudaSuccess) return e;
     attr = true;
   }
+  const bool pair = g_oz_pair != 0;
   CUtensorMap mx, my;
-  if (!encode_map_u8(&mx, xq, n * op.M, K, ldq, IG_BM) || !encode_map_u8(&my, yq, n * nc, K, ldq, IG_BN))
+  if (!encode_map_u8(&mx, xq, n * op.M, K, ldq, IG_BM) ||
+      !encode_map_u8(&my, yq, n * nc, K, ldq, pair ? 128 : IG_BN))
     return cudaErrorInvalidValue;
   const int64_t ldr = round_up(nc, 16);
   IgemmParams G;
@@ -566,7 +588,10 @@ cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t*
   G.rows_per_plane_x = (int)op.M;
   G.rows_per_plane_y = (int)nc;
   G.lower = (op.lower && j0 == 0) ? 1 : 0;
-  const int total = G.tiles_m * G.tiles_n * n;
+  int total = G.tiles_m * G.tiles_n * n;
+  if (pair) total = 2 * (int)((op.M + IG2_BM - 1) / IG2_BM) * (int)((nc + IG2_BN - 1) / IG2_BN) * n;
+  int grid = std::min(total, sms);
+  if (pair) grid = std::max(2, grid & ~1);
   cudaEvent_t tev[2] = {nullptr, nullptr};
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cap);
@@ -576,29 +601,47 @@ cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t*
     cudaEventCreate(&tev[1]);
     cudaEventRecord(tev[0], s);
   }
-  igemm_tc_kernel<<<std::min(total, sms), IG_THREADS, IG_SMEM, s>>>(mx, my, G);
+  if (pair) igemm_tc2_kernel<<<grid, IG_THREADS, IG2_SMEM, s>>>(mx, my, G);
+  else igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM, s>>>(mx, my, G);
   note_launch();
   if (timing) {
     cudaEventRecord(tev[1], s);
     // algorithmic INT8 ops of the launch (lower mode: the tiles it runs)
     double ops = 2.0 * (double)op.M * (double)nc * (double)K * n;
     if (G.lower) {
+      const int bm = pair ? IG2_BM : IG_BM, bn = pair ? IG2_BN : IG_BN;
+      const int tmm = (int)((op.M + bm - 1) / bm), tnn = (int)((nc + bn - 1) / bn);
       int64_t run = 0;
-      for (int tm = 0; tm < G.tiles_m; ++tm)
-        for (int tn = 0; tn < G.tiles_n; ++tn)
-          if (!(tn * IG_BN > tm * IG_BM + IG_BM - 1)) ++run;
-      ops *= (double)run / (double)(G.tiles_m * G.tiles_n);
+      for (int tm = 0; tm < tmm; ++tm)
+        for (int tn = 0; tn < tnn; ++tn)
+          if (!(tn * bn > tm * bm + bm - 1)) ++run;
+      ops *= (double)run / (double)(tmm * tnn);
     }
     g_oz_events.push_back({tev[0], tev[1], ops});
   }
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// CRT + fused epilogue of one N chunk.
+cudaError_t oz_crt(const GemmOp& op, const GemmParams& P, int n, const int* ex, const int* ey, int64_t j0, int64_t nc,
+                   const uint8_t* rq, cudaStream_t s) {
+  const int64_t ldr = round_up(nc, 16);
   OzCrt E;
   E.R = rq; E.ldr = ldr; E.rplane = op.M * ldr;
   E.ex = ex; E.ey = ey; E.n = n; E.M = (int)op.M; E.ncols = (int)nc; E.j_off = (int)j0;
-  dim3 cg((unsigned)((nc + 127) / 128), (unsigned)((op.M + 31) / 32));
+  const int64_t ctiles = ((nc + 127) / 128) * ((op.M + 15) / 16);
+  dim3 cg((unsigned)std::min<int64_t>(ctiles, (int64_t)(g_oz_chunks > 1 ? 2 : 32) * g_sms_hint));
   OZ_DISPATCH(n, oz_crt_launch, cg, s, P, E);
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t* xq, const int* ex, const int8_t* yq,
+                     const int* ey, int64_t K, int64_t ldq, int64_t j0, int64_t nc, uint8_t* rq, int sms,
+                     cudaStream_t s) {
+  cudaError_t e = oz_igemm(op, n, xq, yq, K, ldq, j0, nc, rq, sms, s);
+  if (e != cudaSuccess) return e;
+  return oz_crt(op, P, n, ex, ey, j0, nc, rq, s);
 }
 
 bool oz_fits(const GemmOp& op, const OzWork& w, int n) {
@@ -620,12 +663,40 @@ inline RowMap oz_kmap(const GemmOp& op, bool y) {
   return RowMap{INT_MAX, y ? op.seg[0].y0 : op.seg[0].x0, 0, nullptr};
 }
 
+__global__ void oz_stamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
+// Aux stream + events of the chunk pipeline (owned by a context).
+constexpr int OZ_EVENTS = 64;
+struct OzStreams {
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev[OZ_EVENTS] = {};
+  bool ready = false;
+  bool init() {
+    if (ready) return true;
+    if (cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking) != cudaSuccess) return false;
+    for (auto& e : ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return false;
+    ready = true;
+    return true;
+  }
+  void release() {
+    if (!ready) return;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(aux);
+    ready = false;
+  }
+};
+
 // C = epilogue(X·Yᵀ) through n INT8 residue GEMMs.  The caller reserved the
 // workspace (nothing is allocated here: graph capture).  xp / yp: operand
 // planes already converted (same n, K map and K); x_in_ybuf: convert X into
 // the Y buffers (when yp points at the X buffers of the previous call).
 cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s, OzPre xp = OzPre(),
-                    OzPre yp = OzPre(), bool x_in_ybuf = false) {
+                    OzPre yp = OzPre(), bool x_in_ybuf = false, OzStreams* ps = nullptr) {
   if (!oz_eligible(op) || n < OZ_MINN || n > OZ_MAXN || !tma_encoder()) return cudaErrorInvalidValue;
   const OzPlan pl = oz_plan(op, n);
   if (op.M > 65535 || op.N > 65535) return cudaErrorInvalidValue;
@@ -650,6 +721,68 @@ cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s,
     xp.e = ex;
   }
   if (yp.q) return oz_chunk(op, P, n, xp.q, xp.e, yp.q, yp.e, pl.K, pl.ldq, 0, op.N, w.rq, sms, s);
+  // (the two-stream pipeline is used with the single-CTA GEMM only: with CTA
+  // pairs, a pipelined c4 sweep stalled on the box — not diagnosed)
+  if (ps && ps->ready && pl.nch > 1 && 1 + 3 * pl.nch <= OZ_EVENTS && !g_oz_pair) {
+    // two-stream pipeline: aux = conv(0) conv(1) crt(0) conv(2) crt(1) ...; main = gemm(0) gemm(1) ...
+    cudaEvent_t* fork = &ps->ev[0];
+    cudaEvent_t* evc = &ps->ev[1];
+    cudaEvent_t* evg = evc + pl.nch;
+    cudaEvent_t* evr = evg + pl.nch;
+    const int64_t ybuf = n * pl.nc * pl.ldq, rbuf = n * op.M * pl.ldr;
+    cudaStream_t a = ps->aux;
+    if ((e = cudaEventRecord(*fork, s)) != cudaSuccess || (e = cudaStreamWaitEvent(a, *fork, 0)) != cudaSuccess)
+      return e;
+    auto conv = [&](int j) -> cudaError_t {
+      const int64_t j0 = (int64_t)j * pl.nc, nc = std::min<int64_t>(pl.nc, op.N - j0);
+      cudaError_t r = oz_convert(op.Y, op.ldy, map_shift(op.yn, j0), oz_kmap(op, true), nc, pl.K, t,
+                                 w.ey + (j & 1) * pl.nc, n, w.yq + (j & 1) * ybuf, pl.ldq, a);
+      if (r == cudaSuccess) r = cudaEventRecord(evc[j], a);
+      return r;
+    };
+    // IBMI_OZ_TRACE=1 (eager calls only): print a per-stream timeline of the pipeline
+    static int trace = -1;
+    if (trace < 0) trace = getenv("IBMI_OZ_TRACE") ? 1 : 0;
+    cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &capst);
+    std::vector<std::string> tl;
+    static unsigned long long* tbuf = nullptr;
+    if (trace && !tbuf) cudaMalloc(&tbuf, 256 * sizeof(unsigned long long));
+    auto mark = [&](const std::string& name, cudaStream_t st) {
+      if (!trace || capst != cudaStreamCaptureStatusNone || tl.size() >= 256) return;
+      oz_stamp_kernel<<<1, 1, 0, st>>>(tbuf + tl.size());
+      tl.push_back(name);
+    };
+    mark("start", s);
+    if ((e = conv(0)) != cudaSuccess) return e;
+    mark("aux conv0 done", a);
+    for (int j = 0; j < pl.nch; ++j) {
+      const int64_t j0 = (int64_t)j * pl.nc, nc = std::min<int64_t>(pl.nc, op.N - j0);
+      const int b = j & 1;
+      if ((e = cudaStreamWaitEvent(s, evc[j], 0)) != cudaSuccess) return e;
+      if (j >= 2 && (e = cudaStreamWaitEvent(s, evr[j - 2], 0)) != cudaSuccess) return e;
+      mark("main gemm" + std::to_string(j) + " start", s);
+      e = oz_igemm(op, n, xp.q, w.yq + b * ybuf, pl.K, pl.ldq, j0, nc, w.rq + b * rbuf, sms, s);
+      if (e != cudaSuccess || (e = cudaEventRecord(evg[j], s)) != cudaSuccess) return e;
+      mark("main gemm" + std::to_string(j) + " done", s);
+      if (j + 1 < pl.nch && (e = conv(j + 1)) != cudaSuccess) return e;
+      mark("aux conv" + std::to_string(j + 1) + " done", a);
+      if ((e = cudaStreamWaitEvent(a, evg[j], 0)) != cudaSuccess) return e;
+      mark("aux crt" + std::to_string(j) + " start", a);
+      e = oz_crt(op, P, n, xp.e, w.ey + b * pl.nc, j0, nc, w.rq + b * rbuf, a);
+      if (e != cudaSuccess || (e = cudaEventRecord(evr[j], a)) != cudaSuccess) return e;
+      mark("aux crt" + std::to_string(j) + " done", a);
+    }
+    e = cudaStreamWaitEvent(s, evr[pl.nch - 1], 0);
+    if (!tl.empty()) {
+      cudaStreamSynchronize(s);
+      unsigned long long h[256];
+      cudaMemcpy(h, tbuf, tl.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      for (size_t i = 0; i < tl.size(); ++i)
+        fprintf(stderr, "[oz] %8.3f ms  %s\n", (double)(h[i] - h[0]) * 1e-6, tl[i].c_str());
+    }
+    return e;
+  }
   for (int64_t j0 = 0; j0 < op.N; j0 += pl.nc) {
     const int64_t nc = std::min<int64_t>(pl.nc, op.N - j0);
     e = oz_convert(op.Y, op.ldy, map_shift(op.yn, j0), oz_kmap(op, true), nc, pl.K, t, w.ey, n, w.yq, pl.ldq, s);
@@ -1096,6 +1229,7 @@ struct ibmi_ctx {
   std::vector<OzCache> oz_w;      // per set: residue planes of W_k (K = complement)
   OzCache oz_a;                   // residue planes of A[c_K, :] (error estimate of the last set)
   int oz_a_set = -1;
+  OzStreams ozs;                  // aux stream + events of the chunk pipeline
   int graph_gen = -1;
   long long graph_launches = 0;   // kernel nodes in the captured sweep
   double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
@@ -1222,7 +1356,8 @@ int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
   k1.tma_ok = true; k1.xrows = b; k1.xcols = p; k1.yrows = p; k1.ycols = p;
   const bool wcache = c->oz_n > 0 && k < (int)c->oz_w.size() && c->oz_w[k].q && c->oz_w[k].n == c->oz_n;
   if (c->oz_n > 0) {
-    CUDA_TRY(oz_gemm(k1, c->oz, c->oz_n, c->sms, c->stream, wcache ? c->oz_w[k].pre() : OzPre()));
+    CUDA_TRY(oz_gemm(k1, c->oz, c->oz_n, c->sms, c->stream, wcache ? c->oz_w[k].pre() : OzPre(), OzPre(), false,
+                     &c->ozs));
   } else {
     int64_t need = 0;
     k1.splits = plan_split(c, k1, g_split_panel, &need);
@@ -1327,6 +1462,7 @@ int plan_workspace(ibmi_ctx* c) {
   }
   if (c->oz_n > 0) {
     const int n = c->oz_n;
+    if (!c->ozs.init()) return fail(IBMI_ERR_CUDA, "cannot create the emulation pipeline stream");
     OzPlan tot;
     for (const SetDev& s : c->sets) {
       if (s.general) continue;
@@ -1515,7 +1651,8 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   if (c->oz_n > 0 && !s.general && oz_fits(gb, c->oz, c->oz_n)) {
     const bool acache = c->oz_a_set == k && c->oz_a.q && c->oz_a.n == c->oz_n &&
                         c->oz_n * b * round_up(cc, 16) <= c->oz.rq_cap;
-    CUDA_TRY(oz_gemm(gb, c->oz, c->oz_n, c->sms, c->stream, OzPre(), acache ? c->oz_a.pre() : OzPre()));
+    CUDA_TRY(oz_gemm(gb, c->oz, c->oz_n, c->sms, c->stream, OzPre(), acache ? c->oz_a.pre() : OzPre(), false,
+                     &c->ozs));
   } else {
     int64_t need = 0;
     gb.splits = plan_split(c, gb, g_split_panel, &need);
@@ -1585,6 +1722,7 @@ int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
   }
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   c->oz_n = g_oz_n;
+  g_sms_hint = c->sms;
   prepare_gemm_attributes();
   power_launch_shape(device, &c->power_blocks, &c->power_threads, &c->power_smem_cap);
   const size_t mat = (size_t)p * c->ld * sizeof(double);
@@ -1616,6 +1754,7 @@ int ibmi_destroy(ibmi_ctx* c) {
   c->oz.release();
   for (auto& w : c->oz_w) w.release();
   c->oz_a.release();
+  c->ozs.release();
   for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal, c->splitws})
     if (q) cudaFree(q);
   if (c->hpin) cudaFreeHost(c->hpin);
@@ -2730,6 +2869,13 @@ int ibmi_tune(int key, int value) {
       if (value != 0 && (value < OZ_MINN || value > OZ_MAXN))
         return fail(IBMI_ERR_INVALID, "Ozaki moduli must be 0 (FP64 DMMA) or in [8, 20]");
       g_oz_n = value;
+      break;
+    case 11:
+      g_oz_pair = value ? 1 : 0;
+      break;
+    case 10:
+      if (value < 1 || value > 16) return fail(IBMI_ERR_INVALID, "Ozaki pipeline chunks must be in [1, 16]");
+      g_oz_chunks = value;
       break;
     case 9:
       g_oz_timing = value != 0;

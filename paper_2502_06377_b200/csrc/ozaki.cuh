@@ -47,19 +47,20 @@ __constant__ OzTable c_oz[OZ_MAXN - OZ_MINN + 1];
 // k in [0, K).  ex[r] = t - 1 - floor(log2 max_k |X|)  (0 for a zero row).
 __global__ void oz_rowexp_kernel(const double* __restrict__ X, int64_t ld, RowMap rm, RowMap km, int R, int K,
                                  int t, int* __restrict__ ex) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= R) return;
-  const double* row = X + map_idx(rm, warp) * ld;
-  double mx = 0.0;
-  if (km.idx == nullptr && km.split >= K) {
-    const double* q = row + km.off0;
-    for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(q[k]));
-  } else {
-    for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(row[map_idx(km, k)]));
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < R; w += nwarps) {
+    const double* row = X + map_idx(rm, w) * ld;
+    double mx = 0.0;
+    if (km.idx == nullptr && km.split >= K) {
+      const double* q = row + km.off0;
+      for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(q[k]));
+    } else {
+      for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(row[map_idx(km, k)]));
+    }
+    mx = warp_max(mx);
+    if (lane == 0) ex[w] = mx > 0.0 ? t - 1 - ilogb(mx) : 0;
   }
-  mx = warp_max(mx);
-  if (lane == 0) ex[warp] = mx > 0.0 ? t - 1 - ilogb(mx) : 0;
 }
 
 // |rint(x · 2^e)| as an unsigned integer (<= 2^62 by the choice of e), by
@@ -91,15 +92,19 @@ __device__ __forceinline__ int oz_sym_residue(const OzTable& T, int l, int c0, i
 // plane l of row r lives at Q + l*qplane + r*ldq.  Columns k >= K are zero.
 constexpr int OZ_SPLIT_V = 8;
 template <int NM>
-__global__ void __launch_bounds__(256, 3) oz_split_kernel(const double* __restrict__ X, int64_t ld, RowMap rm,
+__global__ void __launch_bounds__(256, 4) oz_split_kernel(const double* __restrict__ X, int64_t ld, RowMap rm,
                                                           RowMap km, int R, int K, const int* __restrict__ ex,
                                                           int8_t* __restrict__ Q, int64_t ldq, int64_t qplane) {
+  // persistent: a bounded grid walks (row, 2048-column slab) items, so the
+  // conversion co-resides with a running INT8 GEMM (one CTA per SM) instead
+  // of filling every SM slot before it
   constexpr int V = OZ_SPLIT_V;
-  constexpr int n = NM;
-  const int k0 = (blockIdx.x * blockDim.x + threadIdx.x) * V;
-  if (k0 >= ldq) return;
   const OzTable& T = c_oz[NM - OZ_MINN];
-  for (int r = blockIdx.y; r < R; r += gridDim.y) {
+  const int64_t slabs = (ldq + V * 256 - 1) / (V * 256);
+  for (int64_t item = blockIdx.x; item < (int64_t)R * slabs; item += gridDim.x) {
+    const int r = (int)(item / slabs);
+    const int k0 = (int)((item - (int64_t)r * slabs) * (V * 256)) + threadIdx.x * V;
+    if (k0 >= ldq) continue;
     const double* row = X + map_idx(rm, r) * ld;
     const int e = ex[r];
     double x[V];
@@ -204,15 +209,19 @@ __device__ __forceinline__ double oz_crt_value(const OzTable& T, const uint32_t*
 // transpose so both stores are coalesced.
 template <int NM>
 __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const OzCrt E) {
-  __shared__ double tile[32][129];
+  constexpr int TR = 16;          // tile rows (16.5 KB of shared memory: co-resides with the INT8 GEMM)
+  __shared__ double tile[TR][129];
   const OzTable& T = c_oz[NM - OZ_MINN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 128;
+  const int tiles_j = (E.ncols + 127) / 128, tiles_i = (E.M + TR - 1) / TR;
+  for (int tile_id = blockIdx.x; tile_id < tiles_i * tiles_j; tile_id += gridDim.x) {
+  const int i0 = (tile_id / tiles_j) * TR, j0 = (tile_id % tiles_j) * 128;
   const int jl = j0 + 4 * lane;
-  const bool diag_skip_all = P.lower && (E.j_off + j0) > (i0 + 31);
-  if (diag_skip_all) return;
+  const bool diag_skip_all = P.lower && (E.j_off + j0) > (i0 + TR - 1);
+  if (diag_skip_all) continue;
+  __syncthreads();                // the previous tile's mirror reads are done
 #pragma unroll 1
-  for (int rr = 0; rr < 4; ++rr) {
+  for (int rr = 0; rr < TR / 8; ++rr) {
     const int il = warp + 8 * rr;
     const int i = i0 + il;
     double v4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -241,19 +250,23 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
       for (int b = 0; b < 4; ++b) tile[il][4 * lane + b] = ok4[b] ? v4[b] : __longlong_as_double(-1ll);
     }
   }
-  if (!P.mirror) return;
+  if (!P.mirror) continue;
   __syncthreads();
-  // mirror: C2[c2n(n)][c2m(i)] for the 128 columns x 32 rows of the tile
-  const int i = i0 + lane;
-  if (i >= E.M) return;
-  const int64_t mc = map_idx(P.c2m, i);
+  // mirror: C2[c2n(n)][c2m(i)] for the 128 columns x TR rows of the tile
+  // (half-warps: lanes 0..15 and 16..31 take two consecutive columns)
+  const int il = lane & (TR - 1);
+  const int i = i0 + il;
+  if (i < E.M) {
+    const int64_t mc = map_idx(P.c2m, i);
 #pragma unroll 1
-  for (int jj = warp; jj < 128; jj += 8) {
-    const int j = j0 + jj;
-    if (j >= E.ncols) break;
-    const double v = tile[lane][jj];
-    if (__double_as_longlong(v) == -1ll) continue;   // not computed (lower mask)
-    P.C2[map_idx(P.c2n, E.j_off + j) * P.ldc2 + mc] = v;
+    for (int jj = 2 * warp + (lane >> 4); jj < 128; jj += 16) {
+      const int j = j0 + jj;
+      if (j >= E.ncols) break;
+      const double v = tile[il][jj];
+      if (__double_as_longlong(v) == -1ll) continue;   // not computed (lower mask)
+      P.C2[map_idx(P.c2n, E.j_off + j) * P.ldc2 + mc] = v;
+    }
+  }
   }
 }
 
@@ -275,13 +288,26 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
     default: F<20>(__VA_ARGS__); break;         \
   }
 
+// The conversion / CRT kernels keep the SM in its max-shared-memory
+// configuration: a kernel that prefers L1 would have the SM re-carved, which
+// needs it drained, and the INT8 GEMM (197 KB per CTA) could not co-reside.
+template <class F>
+void oz_carveout(F* f) {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    done = true;
+  }
+}
 template <int NM>
 void oz_split_launch(dim3 grid, cudaStream_t s, const double* X, int64_t ld, RowMap rm, RowMap km, int R, int K,
                      const int* ex, int8_t* Q, int64_t ldq, int64_t qplane) {
+  oz_carveout(oz_split_kernel<NM>);
   oz_split_kernel<NM><<<grid, 256, 0, s>>>(X, ld, rm, km, R, K, ex, Q, ldq, qplane);
 }
 template <int NM>
 void oz_crt_launch(dim3 grid, cudaStream_t s, const GemmParams& P, const OzCrt& E) {
+  oz_carveout(oz_crt_kernel<NM>);
   oz_crt_kernel<NM><<<grid, 256, 0, s>>>(P, E);
 }
 

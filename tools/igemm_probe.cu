@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <vector>
 #include "../paper_2502_06377_b200/csrc/igemm_tc.cuh"
+#include "../paper_2502_06377_b200/csrc/ozaki.cuh"
 
 using namespace ibmi;
 
@@ -56,9 +57,10 @@ __global__ void fill_kernel(int8_t* p, int64_t n, uint32_t seed) {
   }
 }
 
+int g_pair = 0;
 int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
   const int64_t ld = (K + 15) / 16 * 16;
-  const int64_t rx = (int64_t)(M + IG_BM - 1) / IG_BM * IG_BM, ry = (int64_t)(N + IG_BN - 1) / IG_BN * IG_BN;
+  const int64_t rx = (int64_t)(M + 255) / 256 * 256, ry = (int64_t)(N + IG_BN - 1) / IG_BN * IG_BN;
   int8_t *x, *y;
   CK(cudaMalloc(&x, rx * ld * planes));
   CK(cudaMalloc(&y, ry * ld * planes));
@@ -85,7 +87,7 @@ int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
   }
   CUtensorMap mx, my;
   make_map(&mx, x, rx * planes, K, ld, IG_BM);
-  make_map(&my, y, ry * planes, K, ld, IG_BN);
+  make_map(&my, y, ry * planes, K, ld, g_pair ? 128 : IG_BN);
   IgemmParams P{};
   P.M = M;
   P.N = N;
@@ -107,11 +109,18 @@ int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
   P.ldc32 = N;
   for (int l = 0; l < planes; ++l) P.mod[l] = mod;
   CK(cudaFuncSetAttribute(igemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG_SMEM));
+  CK(cudaFuncSetAttribute(igemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG2_SMEM));
   int sms;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int total = P.tiles_m * P.tiles_n * planes;
-  const int grid = total < sms ? total : sms;
-  igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+  int total = P.tiles_m * P.tiles_n * planes;
+  if (g_pair) total = 2 * ((M + 255) / 256) * ((N + 255) / 256) * planes;
+  int grid = total < sms ? total : sms;
+  if (g_pair) grid = grid < 2 ? 2 : (grid & ~1);
+  auto launch = [&]() {
+    if (g_pair) igemm_tc2_kernel<<<grid, IG_THREADS, IG2_SMEM>>>(mx, my, P);
+    else igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+  };
+  launch();
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   int bad = 0;
@@ -149,16 +158,16 @@ int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    for (int i = 0; i < 2; ++i) igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+    for (int i = 0; i < 2; ++i) launch();
     CK(cudaEventRecord(e0));
-    for (int i = 0; i < reps; ++i) igemm_tc_kernel<<<grid, IG_THREADS, IG_SMEM>>>(mx, my, P);
+    for (int i = 0; i < reps; ++i) launch();
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&ms, e0, e1));
     ms /= reps;
   }
   const double ops = 2.0 * M * N * (double)K * planes;
-  printf("M=%d N=%d K=%d planes=%d mod=%d grid=%d: %s%d bad; %.3f ms  %.1f TOPS\n", M, N, K, planes, mod, grid,
+  printf("%s M=%d N=%d K=%d planes=%d mod=%d grid=%d: %s%d bad; %.3f ms  %.1f TOPS\n", g_pair ? "pair" : "1cta", M, N, K, planes, mod, grid,
          check ? "" : "(unchecked) ", bad, ms, reps > 0 ? ops / ms * 1e-9 : 0.0);
   CK(cudaFree(x));
   CK(cudaFree(y));
@@ -167,10 +176,83 @@ int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
   return bad;
 }
 
+// concurrency check: INT8 GEMM on one stream, residue split (ALU-bound) on another
+void concurrency() {
+  const int M = 2560, N = 14080, K = 14080, planes = 16;
+  const int64_t ld = K;
+  int8_t *x, *y;
+  CK(cudaMalloc(&x, (int64_t)M * ld * planes));
+  CK(cudaMalloc(&y, (int64_t)N * ld * planes));
+  CK(cudaMemset(x, 1, (int64_t)M * ld * planes));
+  CK(cudaMemset(y, 1, (int64_t)N * ld * planes));
+  CUtensorMap mx, my;
+  make_map(&mx, x, (int64_t)M * planes, K, ld, IG_BM);
+  make_map(&my, y, (int64_t)N * planes, K, ld, IG_BN);
+  IgemmParams P{};
+  P.M = M; P.N = N; P.K = K;
+  P.tiles_m = M / IG_BM; P.tiles_n = (N + IG_BN - 1) / IG_BN; P.planes = planes;
+  P.rows_per_plane_x = M; P.rows_per_plane_y = N;
+  uint8_t* R;
+  CK(cudaMalloc(&R, (int64_t)M * N * planes));
+  P.R = R; P.ldr = N; P.r_plane = (int64_t)M * N;
+  for (int l = 0; l < planes; ++l) P.mod[l] = 251;
+  // split workload: 198M doubles -> 16 planes
+  const int64_t rows = 14080, cols = 14080;
+  double* src;
+  int8_t* q;
+  int* ex;
+  CK(cudaMalloc(&src, rows * cols * 8));
+  CK(cudaMemset(src, 0, rows * cols * 8));
+  CK(cudaMalloc(&q, rows * cols * 16));
+  CK(cudaMalloc(&ex, rows * 4));
+  CK(cudaMemset(ex, 0, rows * 4));
+  CK(cudaFuncSetAttribute(igemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IG_SMEM));
+  cudaStream_t s1, s2;
+  CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  RowMap rm{INT_MAX, 0, 0, nullptr};
+  auto gemm = [&](cudaStream_t s) { igemm_tc_kernel<<<148, IG_THREADS, IG_SMEM, s>>>(mx, my, P); };
+  auto split = [&](cudaStream_t s, dim3 sg) {
+    oz_split_kernel<16><<<sg, 256, 0, s>>>(src, cols, rm, rm, (int)rows, (int)cols, ex, q, cols, rows * cols);
+  };
+  CK(cudaFuncSetAttribute(oz_split_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  for (int bps : {2, 3, 4}) {
+  dim3 sg(148 * bps);
+  printf("split grid %d blocks\n", 148 * bps);
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  float t;
+  for (int w = 0; w < 2; ++w) { gemm(s1); split(s1, sg); }
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a, s1)); gemm(s1); CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&t, a, b)); printf("igemm alone: %.3f ms\n", t);
+  CK(cudaEventRecord(a, s1)); split(s1, sg); CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&t, a, b)); printf("split alone: %.3f ms\n", t);
+  CK(cudaEventRecord(a, s1)); gemm(s1); split(s1, sg); CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&t, a, b)); printf("serial: %.3f ms\n", t);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a, s1)); CK(cudaStreamWaitEvent(s2, a, 0));
+  gemm(s1); split(s2, sg);
+  cudaEvent_t c2; CK(cudaEventCreate(&c2)); CK(cudaEventRecord(c2, s2)); CK(cudaStreamWaitEvent(s1, c2, 0));
+  CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&t, a, b)); printf("concurrent (gemm first): %.3f ms\n", t);
+  CK(cudaDeviceSynchronize());
+  CK(cudaEventRecord(a, s1)); CK(cudaStreamWaitEvent(s2, a, 0));
+  split(s2, sg); gemm(s1);
+  CK(cudaEventRecord(c2, s2)); CK(cudaStreamWaitEvent(s1, c2, 0));
+  CK(cudaEventRecord(b, s1)); CK(cudaEventSynchronize(b));
+  CK(cudaEventElapsedTime(&t, a, b)); printf("concurrent (split first): %.3f ms\n", t);
+  CK(cudaDeviceSynchronize());
+  }
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1) { cudaDriverEntryPointQueryResult q0; CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q0)); concurrency(); return 0; }
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q));
   int bad = 0;
+  for (g_pair = 0; g_pair < 2; ++g_pair) {
   bad += run(128, 256, 128, 1, 0, true, 0);
   bad += run(256, 512, 1024, 1, 0, true, 0);
   bad += run(300, 700, 1000, 1, 0, true, 0);
@@ -181,5 +263,6 @@ int main(int argc, char** argv) {
   run(2560, 14080, 14080, 4, 251, false, 3);
   run(8192, 8192, 8192, 1, 0, false, 5);
   run(8192, 8192, 8192, 1, 251, false, 5);
+  }
   return bad ? 1 : 0;
 }

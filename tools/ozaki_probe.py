@@ -108,6 +108,32 @@ if __name__ == "__main__":
     if "timing" in what:
         timing()
     for w in what:
+        if w.startswith("chunks:"):
+            from paper_2502_06377_b200 import configs
+            from paper_2502_06377_b200.device import DeviceSolver
+            nm = w.split(":")[1]
+            cfg = configs.get_config(nm)
+            a = torch.as_tensor(configs.make_matrix(nm), device=dev)
+            for ch, pair in ((1, 0), (1, 1), (4, 1)):
+                _abi.check(L.ibmi_tune(10, ch))
+                _abi.check(L.ibmi_tune(11, pair))
+                ds = DeviceSolver(a, partition=cfg.partition())
+                ds.set_emulation(16)
+                ds.setup()
+                ds.init_sigma(0)
+                for _ in range(2):
+                    ds.sweep(1e-9, 5000)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for _ in range(4):
+                    ds.sweep(1e-9, 5000)
+                torch.cuda.synchronize()
+                dt = (time.perf_counter() - t0) / 4
+                tm = ds.sweep_timed(1e-9, 5000)[3]
+                print(f"chunks={ch} pair={pair}: {1/dt:.2f} sweeps/s (graph), timed {dict((k, round(v, 2)) for k, v in tm.items())}", flush=True)
+                ds.close()
+            _abi.check(L.ibmi_tune(10, 1))
+            _abi.check(L.ibmi_tune(11, 1))
         if w.startswith("profile:"):
             _, nm, mod = w.split(":")
             from paper_2502_06377_b200 import configs
