@@ -1546,6 +1546,8 @@ struct NormBufs {
   double* ws;           // split-K workspace for the Gram GEMM (may be null)
   int64_t ws_cap;
   int sms;
+  OzWork* oz = nullptr;  // Ozaki-II emulation of the Gram GEMM (context with emulation on)
+  int oz_n = 0;
 };
 
 int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, double rtol, int max_iters,
@@ -1566,13 +1568,25 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
   gg.M = n; gg.N = n;
   gg.C = nb.G; gg.ldc = nb.ldG;
   gg.lower = true; gg.mirror = true;
-  if (nb.ws && mode == 0) {
-    const int bk = g_variant == 2 ? 32 : 16;
-    gg.splits = g_split_gram > 0 ? g_split_gram : auto_split(gemm_tiles(gg), (int)((cc + bk - 1) / bk), nb.sms);
-    if ((int64_t)gemm_tiles(gg) * gg.splits * GB_M * GB_N > nb.ws_cap) gg.splits = 1;
-    gg.ws = nb.ws;
+  // emulated Gram product (context in emulation mode, workspace large enough)
+  const bool emu = mode == 0 && nb.oz && nb.oz_n > 0 && n <= 65535 && n <= nb.oz->ex_cap &&
+                   (int64_t)nb.oz_n * n * round_up(n, 16) <= nb.oz->rq_cap &&
+                   (int64_t)nb.oz_n * n * round_up(cc, 16) <= nb.oz->xq_cap;
+  if (emu) {
+    // G = B Bᵀ: X and Y are the same rows, one conversion serves both
+    OzPre same;
+    same.q = nb.oz->xq;
+    same.e = nb.oz->ex;
+    CUDA_TRY(oz_gemm(gg, *nb.oz, nb.oz_n, nb.sms, st, OzPre(), same));
+  } else {
+    if (nb.ws && mode == 0) {
+      const int bk = g_variant == 2 ? 32 : 16;
+      gg.splits = g_split_gram > 0 ? g_split_gram : auto_split(gemm_tiles(gg), (int)((cc + bk - 1) / bk), nb.sms);
+      if ((int64_t)gemm_tiles(gg) * gg.splits * GB_M * GB_N > nb.ws_cap) gg.splits = 1;
+      gg.ws = nb.ws;
+    }
+    CUDA_TRY(launch_gemm(gg, st));
   }
-  CUDA_TRY(launch_gemm(gg, st));
   if (mode == 0) {
     const int threads = 256;
     const int blocks = (int)((b * 32 + threads - 1) / threads);
@@ -1663,6 +1677,10 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
   NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
               c->power_smem_cap, c->splitws, c->splitws_cap, c->sms};
+  if (c->oz_n > 0 && !s.general) {
+    nb.oz = &c->oz;
+    nb.oz_n = c->oz_n;
+  }
   rc = enqueue_two_norm(c->Bm, c->ldB, b, cc, rtol, max_iters, nb, c->stream, ev ? ev[1] : nullptr);
   if (rc) return rc;
   if (copy_out) CUDA_TRY(cudaMemcpyAsync(c->hpin, c->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
