@@ -114,6 +114,7 @@ bool tma_encoder() {
 }
 
 bool encode_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  if (!tma_encoder()) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
   cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
@@ -443,6 +444,7 @@ int oz_bits(int n, int64_t K) {
 }
 
 bool encode_map_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  if (!tma_encoder()) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld};
   cuuint32_t box[2] = {(cuuint32_t)IG_BK, (cuuint32_t)box_rows};
@@ -530,7 +532,8 @@ RowMap map_shift(const RowMap& m, int64_t j0) {
 }
 
 cudaError_t oz_convert(const double* X, int64_t ld, RowMap rm, RowMap km, int64_t R, int64_t K, int t, int* ex,
-                       int n, int8_t* Q, int64_t ldq, cudaStream_t s) {
+                       int n, int8_t* Q, int64_t ldq, cudaStream_t s, int64_t qplane = -1) {
+  if (qplane < 0) qplane = R * ldq;
   // bounded grids (2 blocks per SM) only when the conversion should co-reside with an INT8 GEMM
   const int gmul = g_oz_chunks > 1 ? 2 : 32;
   const int64_t rx = std::min<int64_t>((R * 32 + 255) / 256, (int64_t)gmul * g_sms_hint);
@@ -540,7 +543,7 @@ cudaError_t oz_convert(const double* X, int64_t ld, RowMap rm, RowMap km, int64_
   // persistent split: two 256-thread blocks per SM at most (co-resident with the INT8 GEMM)
   const int64_t items = R * ((ldq + OZ_SPLIT_V * 256 - 1) / (OZ_SPLIT_V * 256));
   dim3 grid((unsigned)std::min<int64_t>(items, (int64_t)gmul * g_sms_hint));
-  OZ_DISPATCH(n, oz_split_launch, grid, s, X, ld, rm, km, (int)R, (int)K, ex, Q, ldq, R * ldq);
+  OZ_DISPATCH(n, oz_split_launch, grid, s, X, ld, rm, km, (int)R, (int)K, ex, Q, ldq, qplane);
   note_launch();
   return cudaGetLastError();
 }
@@ -559,8 +562,26 @@ GemmParams oz_epilogue(const GemmOp& op) {
   return P;
 }
 
+// Residue planes of one GEMM operand as the INT8 GEMM addresses them:
+// plane l, row r, column k at q[(l*rows + r)*ldq + k]; the tensor map spans
+// `rows` x `cols`; ig_gap mappings (IgemmParams) for rows and K columns; e
+// (exponent per row) indexed through emap (all-zero = identity).
+struct OzOperand {
+  const int8_t* q = nullptr;
+  const int* e = nullptr;
+  RowMap emap{0, 0, 0, nullptr};
+  int64_t ldq = 0, rows = 0, cols = 0;
+  int row_off = 0, split = 0, off1 = 0;     // X: row_off; Y: row gap
+  int ksplit = 0, koff1 = 0;
+};
+inline OzOperand oz_plain(const int8_t* q, const int* e, int64_t ldq, int64_t rows, int64_t cols) {
+  OzOperand o;
+  o.q = q; o.e = e; o.ldq = ldq; o.rows = rows; o.cols = cols;
+  return o;
+}
+
 // INT8 residue GEMMs of one N chunk [j0, j0 + nc) into rq.
-cudaError_t oz_igemm(const GemmOp& op, int n, const int8_t* xq, const int8_t* yq, int64_t K, int64_t ldq, int64_t j0,
+cudaError_t oz_igemm(const GemmOp& op, int n, const OzOperand& X, const OzOperand& Y, int64_t K, int64_t j0,
                      int64_t nc, uint8_t* rq, int sms, cudaStream_t s) {
   static bool attr = false;
   cudaError_t e;
@@ -573,8 +594,7 @@ cudaError_t oz_igemm(const GemmOp& op, int n, const int8_t* xq, const int8_t* yq
   }
   const bool pair = g_oz_pair != 0;
   CUtensorMap mx, my;
-  if (!encode_map_u8(&mx, xq, n * op.M, K, ldq, IG_BM) ||
-      !encode_map_u8(&my, yq, n * nc, K, ldq, pair ? 128 : IG_BN))
+  if (!encode_map_u8(&mx, X.q, n * X.rows, X.cols, X.ldq, IG_BM) || !encode_map_u8(&my, Y.q, n * Y.rows, Y.cols, Y.ldq, 128))
     return cudaErrorInvalidValue;
   const int64_t ldr = round_up(nc, 16);
   IgemmParams G;
@@ -585,9 +605,13 @@ cudaError_t oz_igemm(const GemmOp& op, int n, const int8_t* xq, const int8_t* yq
   G.planes = n;
   G.R = rq; G.ldr = ldr; G.r_plane = op.M * ldr;
   for (int l = 0; l < n; ++l) G.mod[l] = g_oz_host[n - OZ_MINN].m[l];
-  G.rows_per_plane_x = (int)op.M;
-  G.rows_per_plane_y = (int)nc;
+  G.rows_per_plane_x = (int)X.rows;
+  G.rows_per_plane_y = (int)Y.rows;
   G.lower = (op.lower && j0 == 0) ? 1 : 0;
+  G.x_row_off = X.row_off;
+  G.y_split = Y.split; G.y_off1 = Y.off1;
+  G.xk_split = X.ksplit; G.xk_off1 = X.koff1;
+  G.yk_split = Y.ksplit; G.yk_off1 = Y.koff1;
   int total = G.tiles_m * G.tiles_n * n;
   if (pair) total = 2 * (int)((op.M + IG2_BM - 1) / IG2_BM) * (int)((nc + IG2_BN - 1) / IG2_BN) * n;
   int grid = std::min(total, sms);
@@ -623,12 +647,14 @@ cudaError_t oz_igemm(const GemmOp& op, int n, const int8_t* xq, const int8_t* yq
 }
 
 // CRT + fused epilogue of one N chunk.
-cudaError_t oz_crt(const GemmOp& op, const GemmParams& P, int n, const int* ex, const int* ey, int64_t j0, int64_t nc,
-                   const uint8_t* rq, cudaStream_t s) {
+cudaError_t oz_crt(const GemmOp& op, const GemmParams& P, int n, const OzOperand& X, const OzOperand& Y, int64_t j0,
+                   int64_t nc, const uint8_t* rq, cudaStream_t s) {
   const int64_t ldr = round_up(nc, 16);
   OzCrt E;
+  memset(&E, 0, sizeof(E));
   E.R = rq; E.ldr = ldr; E.rplane = op.M * ldr;
-  E.ex = ex; E.ey = ey; E.n = n; E.M = (int)op.M; E.ncols = (int)nc; E.j_off = (int)j0;
+  E.ex = X.e; E.ey = Y.e; E.exm = X.emap; E.eym = Y.emap;
+  E.n = n; E.M = (int)op.M; E.ncols = (int)nc; E.j_off = (int)j0;
   const int64_t ctiles = ((nc + 127) / 128) * ((op.M + 15) / 16);
   dim3 cg((unsigned)std::min<int64_t>(ctiles, (int64_t)(g_oz_chunks > 1 ? 2 : 32) * g_sms_hint));
   OZ_DISPATCH(n, oz_crt_launch, cg, s, P, E);
@@ -639,9 +665,10 @@ cudaError_t oz_crt(const GemmOp& op, const GemmParams& P, int n, const int* ex, 
 cudaError_t oz_chunk(const GemmOp& op, const GemmParams& P, int n, const int8_t* xq, const int* ex, const int8_t* yq,
                      const int* ey, int64_t K, int64_t ldq, int64_t j0, int64_t nc, uint8_t* rq, int sms,
                      cudaStream_t s) {
-  cudaError_t e = oz_igemm(op, n, xq, yq, K, ldq, j0, nc, rq, sms, s);
+  const OzOperand X = oz_plain(xq, ex, ldq, op.M, K), Y = oz_plain(yq, ey, ldq, nc, K);
+  cudaError_t e = oz_igemm(op, n, X, Y, K, j0, nc, rq, sms, s);
   if (e != cudaSuccess) return e;
-  return oz_crt(op, P, n, ex, ey, j0, nc, rq, s);
+  return oz_crt(op, P, n, X, Y, j0, nc, rq, s);
 }
 
 bool oz_fits(const GemmOp& op, const OzWork& w, int n) {
@@ -762,14 +789,16 @@ cudaError_t oz_gemm(const GemmOp& op, OzWork& w, int n, int sms, cudaStream_t s,
       if ((e = cudaStreamWaitEvent(s, evc[j], 0)) != cudaSuccess) return e;
       if (j >= 2 && (e = cudaStreamWaitEvent(s, evr[j - 2], 0)) != cudaSuccess) return e;
       mark("main gemm" + std::to_string(j) + " start", s);
-      e = oz_igemm(op, n, xp.q, w.yq + b * ybuf, pl.K, pl.ldq, j0, nc, w.rq + b * rbuf, sms, s);
+      const OzOperand Xo = oz_plain(xp.q, xp.e, pl.ldq, op.M, pl.K);
+      const OzOperand Yo = oz_plain(w.yq + b * ybuf, w.ey + b * pl.nc, pl.ldq, nc, pl.K);
+      e = oz_igemm(op, n, Xo, Yo, pl.K, j0, nc, w.rq + b * rbuf, sms, s);
       if (e != cudaSuccess || (e = cudaEventRecord(evg[j], s)) != cudaSuccess) return e;
       mark("main gemm" + std::to_string(j) + " done", s);
       if (j + 1 < pl.nch && (e = conv(j + 1)) != cudaSuccess) return e;
       mark("aux conv" + std::to_string(j + 1) + " done", a);
       if ((e = cudaStreamWaitEvent(a, evg[j], 0)) != cudaSuccess) return e;
       mark("aux crt" + std::to_string(j) + " start", a);
-      e = oz_crt(op, P, n, xp.e, w.ey + b * pl.nc, j0, nc, w.rq + b * rbuf, a);
+      e = oz_crt(op, P, n, Xo, Yo, j0, nc, w.rq + b * rbuf, a);
       if (e != cudaSuccess || (e = cudaEventRecord(evr[j], a)) != cudaSuccess) return e;
       mark("aux crt" + std::to_string(j) + " done", a);
     }
@@ -808,6 +837,27 @@ struct OzCache {
     bytes = 0;
   }
   OzPre pre() const { OzPre p; p.q = q; p.e = e; return p; }
+};
+
+// Residue planes of the whole Σ (p x p, one exponent per row), kept in step
+// with Σ by the emulated block updates: each step re-converts the set's rows
+// and rewrites the set's columns of the other rows (oz_update_cols_kernel);
+// a full conversion refreshes every row's exponent at the start of a sweep.
+struct OzSigma {
+  int8_t* q = nullptr;
+  int* e = nullptr;
+  int* flags = nullptr;
+  int64_t ldq = 0;
+  int n = 0, t = 0;
+  bool valid = false;
+  size_t bytes = 0;
+  void release() {
+    if (q) cudaFree(q);
+    if (e) cudaFree(e);
+    if (flags) cudaFree(flags);
+    q = nullptr; e = nullptr; flags = nullptr;
+    n = 0; valid = false; bytes = 0;
+  }
 };
 
 // Convert op's X (y = false) or Y (y = true) operand into a cache if the
@@ -1230,6 +1280,7 @@ struct ibmi_ctx {
   OzCache oz_a;                   // residue planes of A[c_K, :] (error estimate of the last set)
   int oz_a_set = -1;
   OzStreams ozs;                  // aux stream + events of the chunk pipeline
+  OzSigma oz_s;                   // residue planes of Σ (incremental block updates)
   int graph_gen = -1;
   long long graph_launches = 0;   // kernel nodes in the captured sweep
   double* dscal = nullptr;        // [0..2] power out, [3..4] frob, [8..9] symcheck (u64)
@@ -1267,6 +1318,8 @@ void oz_drop_caches(ibmi_ctx* c) {
   c->bytes -= c->oz_a.bytes;
   c->oz_a.release();
   c->oz_a_set = -1;
+  c->bytes -= c->oz_s.bytes;
+  c->oz_s.release();
 }
 
 void invalidate_graph(ibmi_ctx* c) {
@@ -1308,7 +1361,79 @@ int plan_split(const ibmi_ctx* c, const GemmOp& op, int forced, int64_t* ws_need
 
 // ---- one block update: the hot path (solver.py:122-129)
 // `mid` (optional) is recorded between the two GEMMs (for ibmi_sweep_timed).
+// Contiguous sets whose start is a multiple of 128 (no TMA box of the
+// planes straddles the set) and whose end is 16-byte aligned.
+bool oz_global_set_ok(const SetDev& s) { return !s.general && s.lo % 128 == 0 && s.hi % 16 == 0; }
+
+// Emulated block update on the residue planes of Σ (OzSigma): no per-step
+// conversion of Σ[c, c]; see OzSigma.
+int enqueue_block_update_ozg(ibmi_ctx* c, int k, cudaEvent_t mid) {
+  const SetDev& s = c->sets[k];
+  OzSigma& G = c->oz_s;
+  const OzCache& W = c->oz_w[k];
+  const int n = c->oz_n;
+  const int64_t p = c->p, lo = s.lo, hi = s.hi, b = s.b, cc = p - b;
+  const int64_t qplane = p * G.ldq;
+  cudaStream_t st = c->stream;
+  CUDA_TRY(oz_upload_tables());
+  if (k == 0 || !G.valid) {
+    CUDA_TRY(oz_convert(c->S, c->ld, contig_map(0), contig_map(0), p, p, G.t, G.e, n, G.q, G.ldq, st, qplane));
+    G.valid = true;
+  }
+  const int64_t ldw = round_up(cc, 16);
+  // K1: Σ[I, c] = −W Σ[c, c] (mirrored), Y = the planes' rows c over columns c
+  GemmOp k1;
+  k1.M = b; k1.N = cc;
+  k1.C = c->S; k1.ldc = c->ld; k1.cm = contig_map(lo); k1.cn = complement_map(lo, hi);
+  k1.alpha = -1.0; k1.mirror = true;
+  const OzOperand X1 = oz_plain(W.q, W.e, ldw, b, cc);
+  OzOperand Y1;
+  Y1.q = G.q; Y1.e = G.e; Y1.emap = complement_map(lo, hi);
+  Y1.ldq = G.ldq; Y1.rows = p; Y1.cols = p;
+  Y1.split = (int)lo; Y1.off1 = (int)hi; Y1.ksplit = (int)lo; Y1.koff1 = (int)hi;
+  CUDA_TRY(oz_igemm(k1, n, X1, Y1, cc, 0, cc, c->oz.rq, c->sms, st));
+  CUDA_TRY(oz_crt(k1, oz_epilogue(k1), n, X1, Y1, 0, cc, c->oz.rq, st));
+  if (mid) CUDA_TRY(cudaEventRecord(mid, st));
+  // the set's rows of the planes (fresh exponents; their own columns follow K2)
+  CUDA_TRY(oz_convert(c->S, c->ld, contig_map(lo), contig_map(0), b, p, G.t, G.e + lo, n, G.q + lo * G.ldq, G.ldq,
+                      st, qplane));
+  // K2: Σ[I, I] = A_II⁻¹ − Σ[I, c] Wᵀ, X = the planes' rows I over columns c
+  GemmOp k2;
+  k2.M = b; k2.N = b;
+  k2.C = c->S; k2.ldc = c->ld; k2.cm = contig_map(lo); k2.cn = contig_map(lo);
+  k2.alpha = -1.0; k2.beta = 1.0; k2.D = s.ainv; k2.ldd = s.ldb;
+  k2.lower = true; k2.mirror = true;
+  OzOperand X2;
+  X2.q = G.q; X2.e = G.e + lo;
+  X2.ldq = G.ldq; X2.rows = p; X2.cols = p;
+  X2.row_off = (int)lo; X2.ksplit = (int)lo; X2.koff1 = (int)hi;
+  const OzOperand Y2 = oz_plain(W.q, W.e, ldw, b, cc);
+  CUDA_TRY(oz_igemm(k2, n, X2, Y2, cc, 0, b, c->oz.rq, c->sms, st));
+  CUDA_TRY(oz_crt(k2, oz_epilogue(k2), n, X2, Y2, 0, b, c->oz.rq, st));
+  // the set's columns in every row, then full re-conversion of rows whose
+  // exponent no longer covers them
+  const int64_t items = p * ((b + 7) / 8);
+  dim3 ug((unsigned)std::min<int64_t>((items + 255) / 256, 32LL * c->sms));
+  OZ_DISPATCH(n, oz_update_cols_launch, ug, st, c->S, c->ld, (int)p, lo, (int)b, G.e, G.t, G.q, G.ldq, qplane,
+              G.flags);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  dim3 fg((unsigned)std::min<int64_t>(p, 4LL * c->sms));
+  OZ_DISPATCH(n, oz_fix_rows_launch, fg, st, c->S, c->ld, (int)p, (int)p, G.e, G.t, G.q, G.ldq, qplane, G.flags);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return IBMI_OK;
+}
+
+bool ozg_ready(const ibmi_ctx* c, int k) {
+  return c->oz_n > 0 && c->oz_s.q && c->oz_s.n == c->oz_n && k < (int)c->oz_w.size() && c->oz_w[k].q &&
+         c->oz_w[k].n == c->oz_n && oz_global_set_ok(c->sets[k]) &&
+         (int64_t)c->oz_n * c->sets[k].b * round_up(c->p - c->sets[k].b, 16) <= c->oz.rq_cap;
+}
+
 int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
+  if (ozg_ready(c, k)) return enqueue_block_update_ozg(c, k, mid);
+  c->oz_s.valid = false;             // Σ changes outside the planes' bookkeeping
   const SetDev& s = c->sets[k];
   const int64_t p = c->p, lo = s.lo, hi = s.hi, b = s.b, cc = p - b;
   if (s.general) {
@@ -1521,6 +1646,39 @@ int plan_workspace(ibmi_ctx* c) {
       gb.add_seg(0, 0, c->p);
       if (oz_cache_build(c->oz_a, gb, true, n, margin, c->stream, &c->bytes)) c->oz_a_set = last;
     }
+    // residue planes of Σ for the incremental block updates (all sets eligible,
+    // W planes cached, room for n·p² bytes)
+    bool all_ok = c->p <= 65535;
+    for (size_t k = 0; k < c->sets.size(); ++k)
+      all_ok = all_ok && oz_global_set_ok(c->sets[k]) && k < c->oz_w.size() && c->oz_w[k].q;
+    if (all_ok && !(c->oz_s.q && c->oz_s.n == n)) {
+      c->bytes -= c->oz_s.bytes;
+      c->oz_s.release();
+      const int64_t ldq = round_up(c->p, 16);
+      const size_t need = (size_t)n * c->p * ldq + 2 * (size_t)c->p * sizeof(int);
+      size_t fr = 0, tot_mem = 0;
+      if (cudaMemGetInfo(&fr, &tot_mem) == cudaSuccess && fr >= need + margin &&
+          cudaMalloc(&c->oz_s.q, (size_t)n * c->p * ldq) == cudaSuccess &&
+          cudaMalloc(&c->oz_s.e, (size_t)c->p * sizeof(int)) == cudaSuccess &&
+          cudaMalloc(&c->oz_s.flags, (size_t)c->p * sizeof(int)) == cudaSuccess &&
+          cudaMemset(c->oz_s.flags, 0, (size_t)c->p * sizeof(int)) == cudaSuccess) {
+        c->oz_s.ldq = ldq;
+        c->oz_s.n = n;
+        c->oz_s.t = oz_bits(n, c->p);     // valid for every GEMM of the solve (K <= p)
+        c->oz_s.valid = false;
+        c->oz_s.bytes = need;
+        c->bytes += need;
+      } else {
+        cudaGetLastError();
+        c->oz_s.release();
+      }
+    }
+    if (c->oz_s.q) {   // K1 of the planes path runs as one N chunk: residues b × c
+      OzPlan more;
+      for (const SetDev& s : c->sets) more.rq = std::max(more.rq, n * s.b * round_up(c->p - s.b, 16));
+      rc = oz_reserve(c->oz, more, &c->bytes);
+      if (rc) return rc;
+    }
     if (c->oz_a.q) {   // the cached estimate runs as one N chunk: residues b × c
       const SetDev& s = c->sets[last];
       OzPlan more;
@@ -1662,9 +1820,19 @@ int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaE
   gb.add_seg(0, 0, p);
   gb.C = c->Bm; gb.ldc = c->ldB;
   gb.tma_ok = true; gb.xrows = p; gb.xcols = p; gb.yrows = p; gb.ycols = p;
-  if (c->oz_n > 0 && !s.general && oz_fits(gb, c->oz, c->oz_n)) {
-    const bool acache = c->oz_a_set == k && c->oz_a.q && c->oz_a.n == c->oz_n &&
-                        c->oz_n * b * round_up(cc, 16) <= c->oz.rq_cap;
+  const bool acache_ok = c->oz_n > 0 && !s.general && c->oz_a_set == k && c->oz_a.q && c->oz_a.n == c->oz_n &&
+                         c->oz_n * b * round_up(cc, 16) <= c->oz.rq_cap;
+  if (acache_ok && c->oz_s.q && c->oz_s.valid && c->oz_s.n == c->oz_n && b <= 65535 && cc <= 65535) {
+    // X = the planes' rows I (all columns), Y = cached planes of A[c, :]
+    OzOperand X;
+    X.q = c->oz_s.q; X.e = c->oz_s.e + s.lo;
+    X.ldq = c->oz_s.ldq; X.rows = p; X.cols = p; X.row_off = (int)s.lo;
+    const OzOperand Y = oz_plain(c->oz_a.q, c->oz_a.e, round_up(p, 16), cc, p);
+    CUDA_TRY(oz_upload_tables());
+    CUDA_TRY(oz_igemm(gb, c->oz_n, X, Y, p, 0, cc, c->oz.rq, c->sms, c->stream));
+    CUDA_TRY(oz_crt(gb, oz_epilogue(gb), c->oz_n, X, Y, 0, cc, c->oz.rq, c->stream));
+  } else if (c->oz_n > 0 && !s.general && oz_fits(gb, c->oz, c->oz_n)) {
+    const bool acache = acache_ok;
     CUDA_TRY(oz_gemm(gb, c->oz, c->oz_n, c->sms, c->stream, OzPre(), acache ? c->oz_a.pre() : OzPre(), false,
                      &c->ozs));
   } else {
@@ -1772,6 +1940,7 @@ int ibmi_destroy(ibmi_ctx* c) {
   c->oz.release();
   for (auto& w : c->oz_w) w.release();
   c->oz_a.release();
+  c->oz_s.release();
   c->ozs.release();
   for (double* q : {c->A, c->S, c->Bm, c->Gm, c->vec, c->part, c->vr, c->frob_part, c->dscal, c->splitws})
     if (q) cudaFree(q);
@@ -1884,6 +2053,7 @@ int ibmi_set_partition_general(ibmi_ctx* c, int k, const int64_t* set_ptr, const
 
 int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_pivot) {
   if (!c) return fail(IBMI_ERR_INVALID, "null context");
+  if (c) c->oz_s.valid = false;   // Σ (or W) changes outside the residue planes' bookkeeping
   if (!c->a_set) return fail(IBMI_ERR_STATE, "matrix not set");
   if (c->sets.empty()) return fail(IBMI_ERR_STATE, "partition not set");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -2033,6 +2203,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
 
 int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int on_device) {
   int rc = check_ready(c);
+  if (c) c->oz_s.valid = false;   // Σ (or W) changes outside the residue planes' bookkeeping
   if (rc) return rc;
   const int64_t p = c->p;
   const SetDev& s0 = c->sets[0];
@@ -2134,6 +2305,7 @@ int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int
 
 int ibmi_set_sigma(ibmi_ctx* c, const double* s, int64_t lds, int on_device) {
   if (!c || !s) return fail(IBMI_ERR_INVALID, "null argument");
+  if (c) c->oz_s.valid = false;   // Σ (or W) changes outside the residue planes' bookkeeping
   if (lds < c->p) return fail(IBMI_ERR_DIM, "lds < p");
   CUDA_TRY(cudaSetDevice(c->device));
   if (int rc = ensure_sigma(c)) return rc;

@@ -46,7 +46,16 @@ struct IgemmParams {
   int rows_per_plane_x;      // TMA row offset of plane l in the stacked X map
   int rows_per_plane_y;
   int lower;                 // only tiles whose columns start at or before the rows end (symmetric C)
+  // Operand addressing inside a plane (all-zero = identity): X rows start at
+  // x_row_off; logical Y row r sits at r < y_split ? r : r - y_split + y_off1
+  // (the complement of a set, skipping its rows); logical K column k of X / Y
+  // sits at k < *_ksplit ? k : k - *_ksplit + *_koff1 (the set's columns
+  // skipped).  Splits are multiples of 128 so no TMA box straddles a gap.
+  int x_row_off;
+  int y_split, y_off1;
+  int xk_split, xk_off1, yk_split, yk_off1;
 };
+__device__ __forceinline__ int ig_gap(int v, int split, int off1) { return v < split ? v : v - split + off1; }
 
 __device__ __forceinline__ void ig_mbar_init(uint32_t a, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
@@ -175,8 +184,9 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int l, tm, tn;
         if (!ig_tile(P, t, l, tm, tn)) continue;
-        const int ya = l * P.rows_per_plane_y + tn * IG_BN;
-        const int xa = l * P.rows_per_plane_x + tm * IG_BM;
+        const int xa = l * P.rows_per_plane_x + P.x_row_off + tm * IG_BM;
+        const int ya0 = l * P.rows_per_plane_y + ig_gap(tn * IG_BN, P.y_split, P.y_off1);
+        const int ya1 = l * P.rows_per_plane_y + ig_gap(tn * IG_BN + 128, P.y_split, P.y_off1);
         for (int kt = 0; kt < KT; ++kt, ++it) {
           const uint32_t s = it % IG_ST;
           const uint32_t round = it / IG_ST;
@@ -184,8 +194,12 @@ __global__ void __launch_bounds__(IG_THREADS, 1)
           const uint32_t fb = bar_full + 8 * s;
           ig_expect_tx(fb, IG_STAGE);
           const uint32_t dst = base + s * IG_STAGE;
-          ig_tma_2d(dst, &mx, kt * IG_BK, xa, fb);
-          ig_tma_2d(dst + IG_A_BYTES, &my, kt * IG_BK, ya, fb);
+          const int kl = kt * IG_BK;
+          ig_tma_2d(dst, &mx, ig_gap(kl, P.xk_split, P.xk_off1), xa, fb);
+          // the 256-row Y tile as two 128-row boxes (either may sit past the row gap)
+          const int ky = ig_gap(kl, P.yk_split, P.yk_off1);
+          ig_tma_2d(dst + IG_A_BYTES, &my, ky, ya0, fb);
+          ig_tma_2d(dst + IG_A_BYTES + IG_B_BYTES / 2, &my, ky, ya1, fb);
         }
       }
     }
@@ -396,16 +410,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(IG_THREADS, 1)
       for (int t = cid; t < total; t += ncl) {
         int l, tm, tn;
         if (!ig2_tile(P, t, l, tm, tn)) continue;
-        const int xa = l * P.rows_per_plane_x + tm * IG2_BM + (int)rank * 128;
-        const int ya = l * P.rows_per_plane_y + tn * IG2_BN + (int)rank * 128;
+        const int xa = l * P.rows_per_plane_x + P.x_row_off + tm * IG2_BM + (int)rank * 128;
+        const int ya = l * P.rows_per_plane_y + ig_gap(tn * IG2_BN + (int)rank * 128, P.y_split, P.y_off1);
         for (int kt = 0; kt < KT; ++kt, ++it) {
           const uint32_t s = it % IG2_ST;
           const uint32_t round = it / IG2_ST;
           if (round > 0) ig_wait(bar_empty + 8 * s, (round - 1) & 1);
           if (rank == 0) ig_expect_tx(bar_full + 8 * s, 2 * IG2_STAGE);
           const uint32_t dst = base + s * IG2_STAGE;
-          ig_tma_2d_pair(dst, &mx, kt * IG_BK, xa, full_leader + 8 * s);
-          ig_tma_2d_pair(dst + IG2_A_BYTES, &my, kt * IG_BK, ya, full_leader + 8 * s);
+          const int kl = kt * IG_BK;
+          ig_tma_2d_pair(dst, &mx, ig_gap(kl, P.xk_split, P.xk_off1), xa, full_leader + 8 * s);
+          ig_tma_2d_pair(dst + IG2_A_BYTES, &my, ig_gap(kl, P.yk_split, P.yk_off1), ya, full_leader + 8 * s);
         }
       }
     }

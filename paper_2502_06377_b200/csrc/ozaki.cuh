@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(256, 4) oz_split_kernel(const double* __restri
 struct OzCrt {
   const uint8_t* R; int64_t ldr, rplane;    // residues [l][i][j]
   const int* ex; const int* ey;
+  RowMap exm, eym;  // row i / chunk column j -> exponent index (all-zero map = identity)
   int n;            // moduli
   int M, ncols;     // rows of the output, columns of this chunk
   int j_off;        // logical column of chunk column 0
@@ -231,14 +232,14 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
       const uint8_t* src = E.R + (int64_t)i * E.ldr + jl;
 #pragma unroll
       for (int l = 0; l < NM; ++l) rs[l] = __ldcs(reinterpret_cast<const unsigned int*>(src + (int64_t)l * E.rplane));
-      const int exi = E.ex[i];
+      const int exi = E.ex[map_idx(E.exm, i)];
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int j = jl + b;
         if (j >= E.ncols) break;
         const int n = E.j_off + j;
         if (P.lower && i < n) continue;
-        double v = P.alpha * oz_crt_value<NM>(T, rs, b, exi + E.ey[j]);
+        double v = P.alpha * oz_crt_value<NM>(T, rs, b, exi + E.ey[map_idx(E.eym, j)]);
         if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, i) * P.ldd + map_idx(P.dn, n)];
         v4[b] = v;
         ok4[b] = true;
@@ -267,6 +268,108 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
       P.C2[map_idx(P.c2n, E.j_off + j) * P.ldc2 + mc] = v;
     }
   }
+  }
+}
+
+// ---- incremental maintenance of the residue planes of Σ (full rows,
+// exponent per row, plane stride qplane): after a block step only the set's
+// columns changed in the other rows.  Rewrite their residues with the row's
+// existing exponent; a value that no longer fits in t bits flags its row for
+// a full re-conversion (oz_fix_rows_kernel).
+template <int NM>
+__global__ void __launch_bounds__(256) oz_update_cols_kernel(const double* __restrict__ S, int64_t ld, int rows,
+                                                             int64_t lo, int b, const int* __restrict__ E, int t,
+                                                             int8_t* __restrict__ Q, int64_t ldq, int64_t qplane,
+                                                             int* __restrict__ flags) {
+  constexpr int V = 8;
+  const OzTable& T = c_oz[NM - OZ_MINN];
+  const int per = (b + V - 1) / V;
+  for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < (int64_t)rows * per;
+       item += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(item / per);
+    const int c0 = (int)(item - (int64_t)j * per) * V;
+    const double* src = S + (int64_t)j * ld + lo + c0;
+    const int e = E[j];
+    int r0[V], r1[V], r2[V];
+    bool over = false;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const double x = c0 + i < b ? src[i] : 0.0;
+      // |x|·2^e must stay below 2^t; test the exponent (a shifted mantissa
+      // would overflow 64 bits long before the test could see it)
+      const int ex = (int)((__double_as_longlong(x) >> 52) & 0x7ff);
+      const bool big = ex != 0 && ex - 1023 + e >= t;
+      over |= big;
+      const uint64_t a = big ? 0 : oz_scaled_mag(x, e);
+      const int sg = x < 0.0 ? -1 : 1;
+      r0[i] = sg * (int)((uint32_t)a & 0x1fffffu);
+      r1[i] = sg * (int)((uint32_t)(a >> 21) & 0x1fffffu);
+      r2[i] = sg * (int)(a >> 42);
+    }
+    if (over) flags[j] = 1;
+    int8_t* dst = Q + (int64_t)j * ldq + lo + c0;
+#pragma unroll
+    for (int l = 0; l < NM; ++l) {
+      int v[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) v[i] = oz_sym_residue(T, l, r0[i], r1[i], r2[i]);
+      if (c0 + V <= b) {
+        const uint32_t w0 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+        const uint32_t w1 = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+        *reinterpret_cast<uint2*>(dst + (int64_t)l * qplane) = make_uint2(w0, w1);
+      } else {
+        for (int i = 0; c0 + i < b; ++i) dst[(int64_t)l * qplane + i] = (int8_t)v[i];
+      }
+    }
+  }
+}
+
+// Re-convert every flagged row in full (fresh exponent), one block per row.
+template <int NM>
+__global__ void __launch_bounds__(256) oz_fix_rows_kernel(const double* __restrict__ S, int64_t ld, int rows, int K,
+                                                          int* __restrict__ E, int t, int8_t* __restrict__ Q,
+                                                          int64_t ldq, int64_t qplane, int* __restrict__ flags) {
+  constexpr int V = 8;
+  __shared__ double red[8];
+  const OzTable& T = c_oz[NM - OZ_MINN];
+  for (int j = blockIdx.x; j < rows; j += gridDim.x) {
+    if (flags[j] == 0) continue;
+    const double* row = S + (int64_t)j * ld;
+    double mx = 0.0;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) mx = fmax(mx, fabs(row[k]));
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    const int e = mx > 0.0 ? t - 1 - ilogb(mx) : 0;
+    for (int k0 = threadIdx.x * V; k0 < ldq; k0 += blockDim.x * V) {
+      int r0[V], r1[V], r2[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const double x = k0 + i < K ? row[k0 + i] : 0.0;
+        const uint64_t a = oz_scaled_mag(x, e);
+        const int sg = x < 0.0 ? -1 : 1;
+        r0[i] = sg * (int)((uint32_t)a & 0x1fffffu);
+        r1[i] = sg * (int)((uint32_t)(a >> 21) & 0x1fffffu);
+        r2[i] = sg * (int)(a >> 42);
+      }
+      int8_t* dst = Q + (int64_t)j * ldq + k0;
+#pragma unroll
+      for (int l = 0; l < NM; ++l) {
+        int v[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) v[i] = oz_sym_residue(T, l, r0[i], r1[i], r2[i]);
+        const uint32_t w0 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+        const uint32_t w1 = __byte_perm(__byte_perm(v[4], v[5], 0x0040), __byte_perm(v[6], v[7], 0x0040), 0x5410);
+        *reinterpret_cast<uint2*>(dst + (int64_t)l * qplane) = make_uint2(w0, w1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      E[j] = e;
+      flags[j] = 0;
+    }
   }
 }
 
@@ -304,6 +407,16 @@ void oz_split_launch(dim3 grid, cudaStream_t s, const double* X, int64_t ld, Row
                      const int* ex, int8_t* Q, int64_t ldq, int64_t qplane) {
   oz_carveout(oz_split_kernel<NM>);
   oz_split_kernel<NM><<<grid, 256, 0, s>>>(X, ld, rm, km, R, K, ex, Q, ldq, qplane);
+}
+template <int NM>
+void oz_update_cols_launch(dim3 grid, cudaStream_t s, const double* S, int64_t ld, int rows, int64_t lo, int b,
+                           const int* E, int t, int8_t* Q, int64_t ldq, int64_t qplane, int* flags) {
+  oz_update_cols_kernel<NM><<<grid, 256, 0, s>>>(S, ld, rows, lo, b, E, t, Q, ldq, qplane, flags);
+}
+template <int NM>
+void oz_fix_rows_launch(dim3 grid, cudaStream_t s, const double* S, int64_t ld, int rows, int K, int* E, int t,
+                        int8_t* Q, int64_t ldq, int64_t qplane, int* flags) {
+  oz_fix_rows_kernel<NM><<<grid, 256, 0, s>>>(S, ld, rows, K, E, t, Q, ldq, qplane, flags);
 }
 template <int NM>
 void oz_crt_launch(dim3 grid, cudaStream_t s, const GemmParams& P, const OzCrt& E) {

@@ -145,3 +145,30 @@ def test_emulation_switch_on_context():
         with pytest.raises(ValueError):
             ds.set_emulation(30)
     assert np.allclose(e_oz, e_dm, rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("moduli", [16, 18])
+def test_residue_planes_overflow_repair(moduli):
+    """Σ0 = 1e-6·I: the first Σ_II blocks are ~1e6 times their rows' exponents,
+    so the incremental residue planes must flag and re-convert those rows
+    (oz_fix_rows_kernel).  Set starts are multiples of 128 (planes path)."""
+    import paper_2502_06377_b200 as pkg
+    from paper_2502_06377_b200.device import DeviceSolver
+
+    p = 2048
+    a = random_spd(p, 11) / p
+    part = pkg.contiguous_partition(p, 4, 0.25)
+    assert all(s[0] % 128 == 0 for s in part.sets)
+    sig0 = 1e-6 * np.eye(p)
+    out = {}
+    for mode in (0, moduli):
+        with DeviceSolver(a, partition=part) as ds:
+            ds.set_emulation(mode)
+            ds.setup()
+            ds.set_sigma(sig0)
+            errs = [ds.sweep(1e-9, 5000)[0] for _ in range(4)]
+            out[mode] = (errs, ds.sigma())
+    e0, s0 = out[0]
+    e1, s1 = out[moduli]
+    assert np.linalg.norm(s1 - s0) <= 1e-12 * np.linalg.norm(s0)
+    assert np.allclose(e1, e0, rtol=1e-9, atol=0)

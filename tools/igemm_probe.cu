@@ -87,7 +87,7 @@ int run(int M, int N, int K, int planes, int mod, bool check, int reps) {
   }
   CUtensorMap mx, my;
   make_map(&mx, x, rx * planes, K, ld, IG_BM);
-  make_map(&my, y, ry * planes, K, ld, g_pair ? 128 : IG_BN);
+  make_map(&my, y, ry * planes, K, ld, 128);
   IgemmParams P{};
   P.M = M;
   P.N = N;
