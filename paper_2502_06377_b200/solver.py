@@ -217,8 +217,20 @@ def solve(a, part: Partition, cfg: IbmiConfig | None = None, *, device: int = 0,
     if cfg.initial_guess not in _GUESS_KIND:
         raise NotImplementedError(f"initial guess {cfg.initial_guess!r} is not available on the B200 path yet")
 
-    with DeviceSolver(a, partition=part, device=device) as ds:
+    prof = os.environ.get("IBMI_PROFILE") is not None
+    t0 = time.perf_counter()
+    ds = DeviceSolver(a, partition=part, device=device)
+    t1 = time.perf_counter()
+    try:
         return run_solve(ds, part, cfg, a=a, result_on_device=result_on_device, callback=callback)
+    finally:
+        t2 = time.perf_counter()
+        ds.close()
+        if prof:
+            import sys
+
+            print(f"[ibmi] context + A upload {t1 - t0:.3f}s, solve {t2 - t1:.3f}s, release {time.perf_counter() - t2:.3f}s",
+                  file=sys.stderr)
 
 
 def run_solve(ds: DeviceSolver, part: Partition, cfg: IbmiConfig, *, a=None, result_on_device: bool = False,
