@@ -160,37 +160,43 @@ struct OzCrt {
 };
 
 // Exact C' from n residues; returns C' · 2^-shift as FP64.
+// Limbs of the CRT arithmetic: |C'| <= P/4 < 2^(32·L - 1) suffices, the sum
+// S = Σ r_l w_l being evaluated modulo 2^(32·L).  16 moduli (P < 2^126): 4.
+template <int NM>
+constexpr int oz_limbs() { return NM <= 16 ? 4 : 5; }
+
 template <int NM>
 __device__ __forceinline__ double oz_crt_value(const OzTable& T, const uint32_t* rs, int byte, int shift) {
-  int64_t acc[OZ_LIMBS];
+  constexpr int LB = oz_limbs<NM>();
+  int64_t acc[LB];
 #pragma unroll
-  for (int k = 0; k < OZ_LIMBS; ++k) acc[k] = 0;
+  for (int k = 0; k < LB; ++k) acc[k] = 0;
   float fq = 0.0f;
 #pragma unroll
   for (int l = 0; l < NM; ++l) {
     {
       const uint32_t r = (rs[l] >> (8 * byte)) & 0xffu;
 #pragma unroll
-      for (int k = 0; k < OZ_LIMBS; ++k) acc[k] += (int64_t)((uint64_t)r * T.w[l][k]);
+      for (int k = 0; k < LB; ++k) acc[k] += (int64_t)((uint64_t)r * T.w[l][k]);
       fq = fmaf((float)r, T.f[l], fq);
     }
   }
   const int64_t q = (int64_t)rintf(fq);
 #pragma unroll
-  for (int k = 0; k < OZ_LIMBS; ++k) acc[k] -= q * (int64_t)T.P[k];
+  for (int k = 0; k < LB; ++k) acc[k] -= q * (int64_t)T.P[k];
 #pragma unroll
-  for (int k = 0; k < OZ_LIMBS - 1; ++k) {
+  for (int k = 0; k < LB - 1; ++k) {
     acc[k + 1] += acc[k] >> 32;            // arithmetic shift: signed carry
     acc[k] &= 0xffffffffll;
   }
-  uint32_t L[OZ_LIMBS];
+  uint32_t L[LB];
 #pragma unroll
-  for (int k = 0; k < OZ_LIMBS; ++k) L[k] = (uint32_t)acc[k];
-  const bool neg = (int32_t)L[OZ_LIMBS - 1] < 0;
+  for (int k = 0; k < LB; ++k) L[k] = (uint32_t)acc[k];
+  const bool neg = (int32_t)L[LB - 1] < 0;
   if (neg) {   // two's-complement negate the 192-bit value
     uint32_t carry = 1;
 #pragma unroll
-    for (int k = 0; k < OZ_LIMBS; ++k) {
+    for (int k = 0; k < LB; ++k) {
       const uint64_t s = (uint64_t)(~L[k]) + carry;
       L[k] = (uint32_t)s;
       carry = (uint32_t)(s >> 32);
@@ -198,7 +204,7 @@ __device__ __forceinline__ double oz_crt_value(const OzTable& T, const uint32_t*
   }
   double d = 0.0;
 #pragma unroll
-  for (int k = OZ_LIMBS - 1; k >= 0; --k) d = fma(d, 4294967296.0, (double)L[k]);
+  for (int k = LB - 1; k >= 0; --k) d = fma(d, 4294967296.0, (double)L[k]);
   d = neg ? -d : d;
   const int be = 1023 - shift;                 // 2^-shift as a normal double when in range
   if (be >= 1 && be <= 2046) return d * __longlong_as_double((int64_t)be << 52);
