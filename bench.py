@@ -219,6 +219,28 @@ def executed_flops(cfg):
 INT8_PEAK_TOPS = 4500.0   # B200 dense INT8 tensor peak (nominal, B200_PROFILING.md: fp8/int8 4.5 P dense)
 
 
+def probe_int8_peak(n: int = 8192, reps: int = 10):
+    """Measured INT8 tensor throughput on this box: cuBLASLt int8 GEMM
+    (torch._int_mm, n^3, best of `reps`, CUDA events) — the denominator of
+    the emulated path's roofline (MEASURED_PEAKS.json has no INT8 entry)."""
+    import torch
+
+    a = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-128, 127, (n, n), dtype=torch.int8, device="cuda").t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
 def measure_single(solver, cfg, args, stream, guess, mode, moduli, setup_s0):
     """Timed sweeps, per-kernel-class breakdown and time to tolerance of one
     GEMM mode ("dmma" or "ozaki") on a prepared single-GPU DeviceSolver."""
@@ -307,6 +329,12 @@ def run_ours(args):
         a_dev = configs.make_matrix_c5_device(0, device=f"cuda:{dev}")
     torch.cuda.synchronize()
     peak = probe_fp64_peak(dev)
+    int8_peak = None
+    if args.gemm == "ozaki" or not args.no_alt:
+        try:
+            int8_peak = probe_int8_peak()
+        except Exception:           # torch without int8 cuBLASLt: fall back to the nominal figure
+            int8_peak = None
     flops = configs.sweep_flops(cfg)
     sizes = [len(s) for s in part.sets]
     guess = "jacobi" if cfg.guess == "jacobi" else "identity"
@@ -418,14 +446,18 @@ def run_ours(args):
             return None
         if mode == "ozaki":
             ach = igemm_["int8_ops"] / (igemm_["ms"] * 1e-3) / 1e12 if igemm_ and igemm_["ms"] > 0 else None
-            return {"bound": "tensor", "kernel": "igemm_tc_kernel (INT8 residue GEMMs of the Ozaki-II emulation, "
-                                                 "tcgen05.mma kind::i8, TMA, TMEM)",
-                    "achieved": ach, "peak": INT8_PEAK_TOPS, "unit": "TOPS",
-                    "frac": ach / INT8_PEAK_TOPS if ach else None, "traffic": None,
+            pk = int8_peak or INT8_PEAK_TOPS
+            return {"bound": "tensor", "kernel": "igemm_tc2_kernel (INT8 residue GEMMs of the Ozaki-II emulation, "
+                                                 "tcgen05.mma.cta_group::2 kind::i8, TMA, TMEM)",
+                    "achieved": ach, "peak": pk, "unit": "TOPS",
+                    "frac": ach / pk if ach else None,
+                    "frac_of_nominal": ach / INT8_PEAK_TOPS if ach else None,
+                    "traffic": None,
                     "launches_per_sweep": igemm_["launches"] if igemm_ else None,
                     "kernel_ms_per_sweep": igemm_["ms"] if igemm_ else None,
-                    "peak_source": "nominal B200 dense INT8/FP8 tensor peak (B200_PROFILING.md); "
-                                   "achieved = algorithmic INT8 ops / CUDA-event time of every igemm launch of a sweep"}
+                    "peak_source": ("measured on this box: cuBLASLt int8 GEMM 8192^3 (torch._int_mm), best of 10"
+                                    if int8_peak else "nominal B200 dense INT8 (B200_PROFILING.md)") +
+                                   "; achieved = algorithmic INT8 ops / CUDA-event time of every igemm launch of a sweep"}
         panel_flops = sum(2.0 * b * (p - b) ** 2 for b in sizes)
         panel_tf = panel_flops / (kt_["panel_gemm"] * 1e-3) / 1e12
         return {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
@@ -454,6 +486,7 @@ def run_ours(args):
             "tflops_frac_of_peak": tf / world / peak,
             "tflops_executed": executed_flops(cfg) * sweeps_s / 1e12,
             "fp64_peak_tflops": peak,
+            "int8_peak_tops_measured": int8_peak,
             "setup_s": setup_s,
             "ranks_consistent": consistent,
             "exchange": getattr(solver, "exchange", None) if world > 1 else None,
