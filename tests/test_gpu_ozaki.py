@@ -32,6 +32,11 @@ from test_gpu_parity import (  # noqa: E402,F401  (re-collected here, under emul
     test_solve_shapes_match_oracle,
     test_solve_small_cases_match_reference,
     test_block_update_and_error_estimate_match_reference,
+    test_block_update_noncontiguous_set,
+    test_initial_guesses_match_reference,
+    test_solve_mixed_runs_and_lists_local_guess,
+    test_solve_overlapping_noncontiguous_matches_oracle,
+    test_solve_with_guess_matches_oracle,
 )
 
 MODULI = 16
