@@ -13,9 +13,12 @@ from paper_2502_06377_b200.device import DeviceSolver  # noqa: E402
 name = sys.argv[1]
 n = int(sys.argv[2])
 every = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+moduli = int(sys.argv[4]) if len(sys.argv) > 4 else 0   # 0: FP64 DMMA, else Ozaki-II moduli
 cfg = configs.get_config(name)
 a = torch.as_tensor(configs.make_matrix(name), device="cuda")
 ds = DeviceSolver(a, partition=cfg.partition())
+if moduli:
+    ds.set_emulation(moduli)
 t0 = time.perf_counter()
 ds.setup()
 ds.init_sigma(1 if cfg.guess == "jacobi" else 0)
