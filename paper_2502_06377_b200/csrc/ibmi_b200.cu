@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -204,6 +205,27 @@ cudaError_t launch_nn(const GemmParams& P, int grid, int epi, cudaStream_t s) {
 }
 
 cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path);
+
+// IBMI_PROFILE=1: device-synchronised phase timings of the host entry points
+// on stderr (diagnostic only; the syncs change nothing but timing).
+struct PhaseTimer {
+  bool on;
+  const char* fn;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTimer(const char* f) : fn(f) {
+    static int en = -1;
+    if (en < 0) en = getenv("IBMI_PROFILE") ? 1 : 0;
+    on = en != 0;
+    if (on) { cudaDeviceSynchronize(); t = std::chrono::steady_clock::now(); }
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[ibmi] %s: %s %.1f ms\n", fn, what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // IBMI_DEBUG_SYNC=1: synchronise after every GEMM and report the failing one.
 cudaError_t launch_gemm(const GemmOp& op, cudaStream_t s) {
@@ -1895,6 +1917,7 @@ int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
   *out = nullptr;
   if (p < 2) return fail(IBMI_ERR_DIM, "matrix order must be >= 2");
   CUDA_TRY(cudaSetDevice(device));
+  PhaseTimer pt("create");
   ibmi_ctx* c = new ibmi_ctx();
   c->device = device;
   c->p = p;
@@ -1922,14 +1945,17 @@ int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
   }
   c->bytes = mat + 16 * 8;
   *out = c;
+  pt.mark("context + A allocation");
   return IBMI_OK;
 }
 
 int ibmi_destroy(ibmi_ctx* c) {
   if (!c) return IBMI_OK;
   cudaSetDevice(c->device);
+  PhaseTimer pt("destroy");
   if (c->stream) cudaStreamSynchronize(c->stream);
   invalidate_graph(c);
+  pt.mark("sync + graph");
   for (auto& s : c->sets) {
     if (s.W) cudaFree(s.W);
     if (s.ainv) cudaFree(s.ainv);
@@ -1947,6 +1973,7 @@ int ibmi_destroy(ibmi_ctx* c) {
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  pt.mark("free");
   return IBMI_OK;
 }
 
@@ -1955,6 +1982,7 @@ int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
   if (lda < c->p) return fail(IBMI_ERR_DIM, "lda < p");
   CUDA_TRY(cudaSetDevice(c->device));
   const int64_t p = c->p;
+  PhaseTimer pt("set_matrix");
   CUDA_TRY(cudaMemsetAsync(c->A, 0, (size_t)p * c->ld * sizeof(double), c->stream));
   if (on_device) {
     CUDA_TRY(cudaMemcpy2DAsync(c->A, c->ld * sizeof(double), a, lda * sizeof(double), p * sizeof(double), p,
@@ -1970,8 +1998,10 @@ int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
   c->bytes -= c->oz_a.bytes;
   c->oz_a.release();
   c->oz_a_set = -1;
+  pt.mark("upload");
   int rc = symcheck(c, contig_map(0), p, "matrix");
   if (rc) { c->a_set = false; return rc; }
+  pt.mark("symmetry check");
   return IBMI_OK;
 }
 
@@ -2065,6 +2095,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   if (count == 0) return IBMI_OK;
   const int64_t p = c->p;
   cudaStream_t st = c->stream;
+  PhaseTimer pt("setup");
   for (int j = first; j < first + count && j < (int)c->oz_w.size(); ++j) {
     c->bytes -= c->oz_w[j].bytes;
     c->oz_w[j].release();
@@ -2085,6 +2116,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaFree(dsym);
   if (e != cudaSuccess) return fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+  pt.mark("block symmetry checks");
 
   // 2. factor / invert / W for all sets, up to 8 sets in flight on their own streams
   for (int j = 0; j < count; ++j) {
@@ -2095,6 +2127,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
       c->bytes += (size_t)s.b * c->ld * 8 + (size_t)s.b * s.ldb * 8;
     }
   }
+  pt.mark("W / ainv allocation");
   const int S = std::min(count, 8);
   std::vector<cudaStream_t> ss(S, nullptr);
   std::vector<CholScratch> scr(S);
@@ -2130,6 +2163,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
     rc = ensure_scratch(scr[q], bmax);
     if (rc) { cleanup(); return rc; }
   }
+  pt.mark("streams + scratch");
   for (int j = 0; j < count; ++j) {
     const int q = j % S;
     SetDev& s = c->sets[first + j];
@@ -2177,7 +2211,9 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
   for (int q = 0; q < S; ++q) SETUP_TRY(cudaStreamSynchronize(ss[q]));
   SETUP_TRY(cudaMemcpy(infos.data(), dinfo, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost));
 #undef SETUP_TRY
+  pt.mark("factor + inverse + W");
   cleanup();
+  pt.mark("scratch release");
 
   // 3. errors in the reference's order: set by set, symmetry before the pivot
   for (int j = 0; j < count; ++j) {
@@ -2326,6 +2362,7 @@ int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
   if (ldo < c->p) return fail(IBMI_ERR_DIM, "ldo < p");
   CUDA_TRY(cudaSetDevice(c->device));
   if (int rc = ensure_sigma(c)) return rc;
+  PhaseTimer pt("get_sigma");
   if (on_device) {
     CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, c->S, c->ld * 8, c->p * 8, c->p, cudaMemcpyDeviceToDevice, c->stream));
   } else {
@@ -2334,6 +2371,7 @@ int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
     if (rc) return rc;
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  pt.mark("download");
   return IBMI_OK;
 }
 
