@@ -397,6 +397,7 @@ def run_ours(args):
                 errs.append(sweep())
             e1.record(stream)
             torch.cuda.synchronize()
+        torch.distributed.barrier()
         ms = e0.elapsed_time(e1)
         launches = abi_mod.lib().ibmi_launch_count() - launches0
         if world > 1:
