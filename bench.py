@@ -463,9 +463,13 @@ def run_ours(args):
         panel_tf = panel_flops / (kt_["panel_gemm"] * 1e-3) / 1e12
         return {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
                 "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s", "frac": panel_tf / peak,
-                "traffic": 6.50e9,
-                "traffic_note": "ncu dram read+write bytes of one interior-set panel GEMM launch "
-                                "(profiles/r01_c4_sweep.md); algorithmic minimum 2.38e9",
+                "traffic": 6.50e9 if args.config == "c4" else None,
+                "traffic_note": ("ncu dram read+write bytes of one interior-set panel GEMM launch "
+                                 "(profiles/r01_c4_sweep.md); algorithmic minimum 2.38e9 (W + Sigma_cc read once, "
+                                 "M written twice). W (288 MB) and Sigma_cc (1.58 GB) exceed the 126 MB L2, so each "
+                                 "148-tile wave re-streams all of W from HBM (15 waves): ~5.9 GB read at 2% of HBM "
+                                 "bandwidth, while the kernel is DMMA-bound") if args.config == "c4"
+                else "measured for c4 only",
                 "peak_source": "measured on this box: DMMA m8n8k4 throughput probe (ibmi_probe_fp64_peak)"}
 
     if rank == 0:
