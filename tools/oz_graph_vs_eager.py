@@ -1,5 +1,5 @@
-"""Graph-replayed vs eagerly launched emulated c4 sweeps in one process
-(device time per sweep, SM clock sampled during each phase)."""
+"""Graph-replayed vs eagerly launched sweeps in one process (device time per
+sweep, SM clock sampled during each phase).  usage: moduli sweeps [config]"""
 import os
 import sys
 import time
@@ -13,14 +13,15 @@ from bench import ClockSampler  # noqa: E402
 
 moduli = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-cfg = configs.get_config("c4")
-a = torch.as_tensor(configs.make_matrix("c4"), device="cuda")
+name = sys.argv[3] if len(sys.argv) > 3 else "c4"
+cfg = configs.get_config(name)
+a = torch.as_tensor(configs.make_matrix(name), device="cuda")
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ds = DeviceSolver(a, partition=cfg.partition(), stream=stream.cuda_stream)
 ds.set_emulation(moduli)
 ds.setup()
-ds.init_sigma(0)
+ds.init_sigma(1 if cfg.guess == "jacobi" else 0)
 for _ in range(3):
     ds.sweep(1e-9, 5000)
 torch.cuda.synchronize()
