@@ -101,6 +101,14 @@ int ibmi_init_sigma(ibmi_ctx* ctx, int guess_kind, const double* guess, int64_t 
 int ibmi_set_sigma(ibmi_ctx* ctx, const double* s, int64_t lds, int on_device);
 int ibmi_get_sigma(ibmi_ctx* ctx, double* out, int64_t ldo, int on_device);
 
+/* Host <-> device row copy through the pinned staging pool (several threads),
+ * device row r <-> host row host_rows[r] (NULL: r).  Used by the sharded solve
+ * to gather Σ's block-cyclic row panels straight into SolveReport.result
+ * (solver.py:277) without a host-side permutation pass.  Synchronises `stream`
+ * first (the rows are produced on it). */
+int ibmi_copy_rows(int device, double* dev, int64_t ldd, double* host, int64_t ldh, int64_t rows, int64_t cols,
+                   const int64_t* host_rows, int to_device, void* stream);
+
 /* The normalised default_rng(0x5EED) restart vector of length n used when the
  * power iteration collapses to σ = 0 (linalg.py:237-244). */
 int ibmi_set_restart_vector(ibmi_ctx* ctx, int64_t n, const double* v);

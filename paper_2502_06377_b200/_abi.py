@@ -41,6 +41,7 @@ SIGNATURES = [
     ("ibmi_init_sigma", C.c_int, [_P, C.c_int, _P, _I64, C.c_int]),
     ("ibmi_set_sigma", C.c_int, [_P, _P, _I64, C.c_int]),
     ("ibmi_get_sigma", C.c_int, [_P, _P, _I64, C.c_int]),
+    ("ibmi_copy_rows", C.c_int, [C.c_int, _P, _I64, _P, _I64, _I64, _I64, _P, C.c_int, _P]),
     ("ibmi_set_restart_vector", C.c_int, [_P, _I64, _D]),
     ("ibmi_block_update", C.c_int, [_P, C.c_int]),
     ("ibmi_error_estimate", C.c_int, [_P, C.c_int, C.c_double, C.c_int, _D, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

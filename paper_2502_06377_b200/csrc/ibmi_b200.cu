@@ -322,7 +322,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
       else if (epi == EPI_FROB) err = launch_tma_inst<EPI_FROB>(P, maps, grid, s);
       else err = launch_tma_inst<EPI_STORE>(P, maps, grid, s);
       if (err != cudaSuccess || !split) return err;
-      splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P); note_launch();
+      splitk_reduce_kernel<<<tiles * (GB_M / 32), 256, 0, s>>>(P); note_launch();
       return cudaGetLastError();
     }
   }
@@ -342,7 +342,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
               : launch_inst<CfgA, true, false, false, EPI_STORE>(P, grid, s);
   }
   if (err != cudaSuccess || !split) return err;
-  splitk_reduce_kernel<<<tiles, 256, 0, s>>>(P); note_launch();
+  splitk_reduce_kernel<<<tiles * (GB_M / 32), 256, 0, s>>>(P); note_launch();
   return cudaGetLastError();
 }
 
@@ -922,11 +922,14 @@ struct PinnedPool {
 PinnedPool g_pool;
 constexpr size_t STAGE_SLOT = 16u << 20;   // 16 MiB per slot, 2 slots per thread
 
+// `hrows` (optional): host row of each device row (a row permutation applied
+// while the rows pass through the pinned slots; the sharded Σ gather uses it).
 int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t rows, int64_t cols, bool to_device,
-                int device, cudaStream_t stream) {
+                int device, cudaStream_t stream, const int64_t* hrows = nullptr) {
   const size_t row_bytes = (size_t)cols * 8;
   const size_t total = row_bytes * (size_t)rows;
-  if (total < (64u << 20) || row_bytes > STAGE_SLOT) {
+  if (row_bytes > STAGE_SLOT && hrows) return fail(IBMI_ERR_INVALID, "staged copy: row too long for a row map");
+  if (!hrows && (total < (64u << 20) || row_bytes > STAGE_SLOT)) {
     // async on the caller's stream + sync: a pageable cudaMemcpy may return
     // before its DMA lands, and the context stream does not wait for stream 0
     CUDA_TRY(cudaMemcpy2DAsync(to_device ? (void*)dev : (void*)host, (to_device ? ldd : ldh) * 8,
@@ -962,8 +965,10 @@ int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t row
       cudaEventSynchronize(ev[slot]);
       if (!to_device) {
         const char* src = (const char*)g_pool.slots[2 * t + slot];
-        for (int64_t r = 0; r < pending_n[slot]; ++r)
-          memcpy(host + (pending_r0[slot] + r) * ldh, src + r * row_bytes, row_bytes);
+        for (int64_t r = 0; r < pending_n[slot]; ++r) {
+          const int64_t hr = hrows ? hrows[pending_r0[slot] + r] : pending_r0[slot] + r;
+          memcpy(host + hr * ldh, src + r * row_bytes, row_bytes);
+        }
       }
       used[slot] = false;
     };
@@ -973,7 +978,8 @@ int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t row
       char* slot = (char*)g_pool.slots[2 * t + s];
       cudaError_t e;
       if (to_device) {
-        for (int64_t r = 0; r < n; ++r) memcpy(slot + r * row_bytes, host + (r0 + r) * ldh, row_bytes);
+        for (int64_t r = 0; r < n; ++r)
+          memcpy(slot + r * row_bytes, host + (hrows ? hrows[r0 + r] : r0 + r) * ldh, row_bytes);
         e = cudaMemcpy2DAsync(dev + r0 * ldd, ldd * 8, slot, row_bytes, row_bytes, n, cudaMemcpyHostToDevice, st);
       } else {
         e = cudaMemcpy2DAsync(slot, row_bytes, dev + r0 * ldd, ldd * 8, row_bytes, n, cudaMemcpyDeviceToHost, st);
@@ -2373,6 +2379,17 @@ int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   pt.mark("download");
   return IBMI_OK;
+}
+
+int ibmi_copy_rows(int device, double* dev, int64_t ldd, double* host, int64_t ldh, int64_t rows, int64_t cols,
+                   const int64_t* host_rows, int to_device, void* stream) {
+  if (!dev || !host || rows < 0 || cols < 0) return fail(IBMI_ERR_INVALID, "bad copy arguments");
+  if (ldd < cols || ldh < cols) return fail(IBMI_ERR_DIM, "leading dimension < cols");
+  if (rows == 0 || cols == 0) return IBMI_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamSynchronize(st));   // the rows are produced on the caller's stream
+  return staged_copy(dev, ldd, host, ldh, rows, cols, to_device != 0, device, st, host_rows);
 }
 
 int ibmi_set_restart_vector(ibmi_ctx* c, int64_t n, const double* v) {

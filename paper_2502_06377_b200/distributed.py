@@ -40,7 +40,7 @@ from . import _abi
 from .device import DeviceSolver, restart_vector
 from .partition import Partition, block_permutation, contiguous_ranges
 
-__all__ = ["RowPanels", "GemmSpec", "CudaBackend", "ShardedSolver"]
+__all__ = ["RowPanels", "GemmSpec", "CudaBackend", "ShardedSolver", "solve_sharded"]
 
 
 # --------------------------------------------------------------------------- layout
@@ -229,6 +229,16 @@ class CudaBackend:
         self._opened = getattr(self, "_opened", []) + [ptr.value]
         return ptr.value
 
+    def rows_to_host(self, t, out: np.ndarray, host_rows: np.ndarray):
+        """out[host_rows[r], :] = t[r, :] through the library's pinned staging pool."""
+        torch = self.torch
+        rows = np.ascontiguousarray(host_rows, dtype=np.int64)
+        assert out.dtype == np.float64 and out.flags.c_contiguous and t.stride(1) == 1
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _abi.check(self.L.ibmi_copy_rows(self.device.index, C.c_void_p(t.data_ptr()), t.stride(0),
+                                         out.ctypes.data_as(C.c_void_p), out.shape[1], t.shape[0], t.shape[1],
+                                         rows.ctypes.data_as(C.c_void_p), 0, stream), "copy_rows")
+
     def two_norm(self, b, rtol, max_iters):
         torch = self.torch
         v = restart_vector(b.shape[1])
@@ -416,7 +426,8 @@ class ShardedSolver:
         """W_k restricted to this rank's columns, compact (zeros stay on I)."""
         cache = self.__dict__.setdefault("_wloc", {})
         if k not in cache:
-            cache[k] = self.W[k].index_select(1, self.own_t).contiguous()
+            # one rank owns every column: W itself (its padding columns are never read)
+            cache[k] = self.W[k] if self.n_loc == self.p else self.W[k].index_select(1, self.own_t).contiguous()
         return cache[k]
 
     # ------------------------------------------------------------ Σ₀
@@ -549,7 +560,10 @@ class ShardedSolver:
         allrows = self.comm.all_gather_rows(self.S[: self.n_loc, : self.p], counts)
         order = np.concatenate(self.layout.rows)
         full = np.empty((self.p, self.p))
-        full[order] = allrows.cpu().numpy()
+        if allrows.is_cuda and hasattr(self.be, "rows_to_host"):
+            self.be.rows_to_host(allrows, full, order)     # panels land in their global rows directly
+        else:
+            full[order] = allrows.cpu().numpy()
         if self.perm is not None:
             inv = np.argsort(self.perm)
             full = full[np.ix_(inv, inv)]
@@ -557,3 +571,64 @@ class ShardedSolver:
 
     def close(self):
         self.be.close()
+
+
+# --------------------------------------------------------------------------- public entry point
+def solve_sharded(a, part: Partition, cfg=None, *, group=None, panel: int = 128, device: int | None = None,
+                  exchange: str = "auto", backend=None, gather_result: bool = True, callback=None):
+    """``solve`` (reference solver.py:225-278) with Σ sharded over the process group.
+
+    Call it on every rank with the same ``a`` (host array or a device copy) and
+    partition.  Same loop and stop rules as the single-GPU ``solve``: K block
+    updates, the reference's error estimate on the last set, stop when it is
+    ≤ ``cfg.tol`` (``stopping="frobenius"``: ‖I − AΣ‖_F < tol, evaluated only
+    once the estimate is below 1.01·tol, since ‖I − AΣ‖_F ≥ the estimate).
+    Every rank returns the same trace; ``result`` is the full Σ (host numpy,
+    original index order) on every rank when ``gather_result``, else None.
+    Supported guesses: identity and jacobi; FP64 DMMA GEMMs only.
+    """
+    import time
+    import warnings
+
+    from .exceptions import NoConvergenceWarning
+    from .partition import validate
+    from .solver import IbmiConfig, SolveReport
+
+    cfg = cfg or IbmiConfig()
+    if getattr(cfg, "gemm", None) == "ozaki":
+        raise NotImplementedError("the sharded sweep runs FP64 DMMA GEMMs only (gemm='ozaki' is single-GPU)")
+    if cfg.initial_guess not in ("identity", "jacobi"):
+        raise NotImplementedError(f"guess {cfg.initial_guess!r} on the sharded path")
+    validate(part)
+    stopping = getattr(cfg, "stopping", "estimate")
+    t0 = time.perf_counter()
+    ss = ShardedSolver(a, part, group=group, panel=panel, backend=backend, device=device, exchange=exchange)
+    try:
+        ss.init_sigma(cfg.initial_guess)
+        setup_s = time.perf_counter() - t0
+        errs, walls, pits, resid = [], [], [], []
+        converged = False
+        for _ in range(cfg.max_iterations):
+            t1 = time.perf_counter()
+            err, it, ok = ss.sweep(cfg.norm_rtol, cfg.norm_max_iters)
+            if not ok:
+                warnings.warn(f"two_norm: power iteration did not stabilize in {cfg.norm_max_iters} "
+                              "iterations; returning last estimate", NoConvergenceWarning, stacklevel=2)
+            fr = None
+            if stopping == "frobenius":      # the same exact skip as the single-GPU loop (solver.run_solve)
+                fr = ss.frobenius() if (getattr(cfg, "residual_every_sweep", False) or err < 1.01 * cfg.tol) \
+                    else float("nan")
+                resid.append(fr)
+            walls.append(time.perf_counter() - t1)
+            errs.append(err)
+            pits.append(it)
+            if callback is not None:
+                callback(len(errs), err, fr)
+            if (fr < cfg.tol) if fr is not None else (err <= cfg.tol):   # nan < tol is False
+                converged = True
+                break
+        result = ss.gather_sigma() if gather_result else None
+        return SolveReport(iterations=len(errs), converged=converged, error_trace=errs, wall_times=walls,
+                           result=result, power_iterations=pits, residual_trace=resid, setup_seconds=setup_s)
+    finally:
+        ss.close()

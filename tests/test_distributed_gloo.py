@@ -91,3 +91,62 @@ def test_sharded_matches_oracle(world, case):
         assert np.linalg.norm(sig - o["result"]) <= 1e-12 * np.linalg.norm(o["result"]), rank
         np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-14)
         assert abs(fr - orc.frobenius_residual(a, o["result"])) <= 1e-9 * max(1.0, fr)
+
+
+def _solve_worker(rank, world, port, case, out):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from torch_backend import TorchCPUBackend
+
+        from paper_2502_06377_b200 import IbmiConfig, contiguous_partition
+        from paper_2502_06377_b200.distributed import solve_sharded
+
+        p, k, f, tol, guess, stopping = case
+        m = np.random.default_rng(p + k).standard_normal((p, p))
+        a = m.T @ m + 0.05 * p * np.eye(p)
+        rep = solve_sharded(a, contiguous_partition(p, k, f),
+                            IbmiConfig(tol=tol, initial_guess=guess, stopping=stopping, max_iterations=300),
+                            panel=8, backend=TorchCPUBackend())
+        out.put((rank, rep.iterations, rep.converged, rep.error_trace, rep.result, rep.residual_trace))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [(72, 3, 0.1, 1e-10, "identity", "estimate"),
+                                  (64, 2, 0.0, 1e-9, "jacobi", "frobenius")])
+def test_solve_sharded_matches_oracle(case):
+    """solve_sharded (the public N-rank solve) stops on the same sweep as the oracle's solve."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import contiguous_partition
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p, k, f, tol, guess, stopping = case
+    m = np.random.default_rng(p + k).standard_normal((p, p))
+    a = m.T @ m + 0.05 * p * np.eye(p)
+    o = orc.solve(a, contiguous_partition(p, k, f).sets, tol=tol, guess=guess, stopping=stopping,
+                  max_iterations=300)
+    assert o["converged"]
+    for rank, iters, conv, errs, sig, resid in res:
+        assert conv and iters == o["iterations"], (rank, iters, o["iterations"])
+        np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-2 * tol)
+        assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
+        if stopping == "frobenius":
+            assert resid[-1] < tol and len(resid) == iters
