@@ -375,9 +375,14 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
 // 32-row chunks: partial sums and the direct store are coalesced along the
 // row; the mirrored (transposed) store and the peer store go through a shared
 // memory transpose so they are written as contiguous 32-element runs too.
+// One CTA per (tile, 32-row chunk): grid = tiles * GB_M / 32.  Each thread
+// keeps 16 row accumulators and streams the split partials with the split
+// loop outside, so 16 independent loads are in flight per thread; every
+// element is still summed in split order 0..s-1 (deterministic, unchanged bits).
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) {
   __shared__ double tr[32][129];
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.x / (GB_M / 32);
+  const int rc = (blockIdx.x % (GB_M / 32)) * 32;
   int tm, tn;
   if (P.lower) {
     int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
@@ -397,35 +402,39 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) 
   const bool ncol_ok = n < P.N;
   const int64_t colc = ncol_ok ? map_idx(P.cn, n) : 0;
   const int64_t cold = (ncol_ok && P.beta != 0.0) ? map_idx(P.dn, n) : 0;
-  for (int rc = 0; rc < GB_M; rc += 32) {
-#pragma unroll 4
-    for (int q = 0; q < 16; ++q) {
-      const int r = rc + (tid >> 7) + 2 * q;
-      const int m = tm * GB_M + r;
-      double acc = 0.0;
-      for (int sp = 0; sp < P.splits; ++sp) acc += src[(size_t)sp * GB_M * GB_N + r * GB_N + c];
-      double v = P.alpha * acc;
-      const bool ok = ncol_ok && m < P.M && !(diag_tile && m < n);
-      if (ok) {
-        if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + cold];
-        if (P.direct) P.C[(P.cidx ? P.cidx[m] : map_idx(P.cm, m)) * P.ldc + colc] = v;
-      }
-      tr[r - rc][c] = v;
+  const int r0 = rc + (tid >> 7);
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int sp = 0; sp < P.splits; ++sp) {
+    const double* base = src + (size_t)sp * GB_M * GB_N + (size_t)r0 * GB_N + c;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] += __ldcs(base + 2 * q * GB_N);
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int r = r0 + 2 * q;
+    const int m = tm * GB_M + r;
+    double v = P.alpha * acc[q];
+    const bool ok = ncol_ok && m < P.M && !(diag_tile && m < n);
+    if (ok) {
+      if (P.beta != 0.0) v += P.beta * P.D[map_idx(P.dm, m) * P.ldd + cold];
+      if (P.direct) P.C[(P.cidx ? P.cidx[m] : map_idx(P.cm, m)) * P.ldc + colc] = v;
     }
+    tr[r - rc][c] = v;
+  }
+  if (P.mirror || P.peers) {
     __syncthreads();
-    if (P.mirror || P.peers) {
-      const int m = tm * GB_M + rc + lane;
-      const bool mrow_ok = m < P.M;
-      const int64_t mcol2 = mrow_ok ? map_idx(P.c2m, m) : 0;
-      for (int cc = warp; cc < GB_N; cc += 8) {
-        const int nn = tn * GB_N + cc;
-        if (!mrow_ok || nn >= P.N || (diag_tile && m < nn)) continue;
-        const double v = tr[lane][cc];
-        if (P.mirror) P.C2[map_idx(P.c2n, nn) * P.ldc2 + mcol2] = v;
-        if (P.peers) peer_store(P, m, nn, v);
-      }
+    const int m = tm * GB_M + rc + lane;
+    const bool mrow_ok = m < P.M;
+    const int64_t mcol2 = mrow_ok ? map_idx(P.c2m, m) : 0;
+    for (int cc = warp; cc < GB_N; cc += 8) {
+      const int nn = tn * GB_N + cc;
+      if (!mrow_ok || nn >= P.N || (diag_tile && m < nn)) continue;
+      const double v = tr[lane][cc];
+      if (P.mirror) P.C2[map_idx(P.c2n, nn) * P.ldc2 + mcol2] = v;
+      if (P.peers) peer_store(P, m, nn, v);
     }
-    __syncthreads();
   }
   if (P.peers) __threadfence_system();
 }
