@@ -211,21 +211,6 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
   }
 }
 
-// Fixed-order reduce of the per-CTA partials (same result in every CTA).
-__device__ __forceinline__ void grid_sum2(const double* part, int nb, double& a, double& b, double* bc) {
-  if (threadIdx.x < 32) {
-    double sa = 0.0, sb = 0.0;
-    for (int i = threadIdx.x; i < nb; i += 32) { sa += part[2 * i]; sb += part[2 * i + 1]; }
-    sa = warp_sum(sa);
-    sb = warp_sum(sb);
-    if (threadIdx.x == 0) { bc[0] = sa; bc[1] = sb; }
-  }
-  __syncthreads();
-  a = bc[0];
-  b = bc[1];
-  __syncthreads();
-}
-
 __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double ys[];           // n doubles (the current iterate, scaled)
@@ -303,8 +288,18 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
   double* gres = ys + (stage ? n : 0);
   const int nres = stage ? min(P.resident, rb1 - rb0) : 0;
   for (int e = threadIdx.x; e < nres * n; e += blockDim.x) gres[e] = P.G[(int64_t)(rb0 + e / n) * P.ldg + (e % n)];
+  // `pre`: publish() already pulled the raw iterate into ys (its L2 reads
+  // overlapped the partial-sum reads after the grid barrier); each thread
+  // scales the entries it loaded itself -- the same xs·x product as the direct
+  // load, so the iterate is bit-identical either way.
+  bool pre = false;
   auto gmatvec = [&](const double* xin, double xs, double* zout, double& pyz, double& pzz) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) ys[j] = xs * __ldcg(xin + j);
+    if (pre) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) ys[j] = xs * ys[j];
+      pre = false;
+    } else {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) ys[j] = xs * __ldcg(xin + j);
+    }
     __syncthreads();
     pyz = 0.0;
     pzz = 0.0;
@@ -352,15 +347,37 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
     __syncthreads();
   };
 
-  auto publish = [&](double a, double b) {   // block partial -> part[phase]
+  // block partial -> part[phase]; after the barrier, optionally prefetch the
+  // next raw iterate `pf` into ys while warp 0 reduces the partials.
+  auto publish = [&](double a, double b, const double* pf) {
     block_sum2(a, b, red);
     if (threadIdx.x == 0) {
       P.part[(size_t)(phase & 1) * 2 * gridDim.x + 2 * blockIdx.x] = a;
       P.part[(size_t)(phase & 1) * 2 * gridDim.x + 2 * blockIdx.x + 1] = b;
     }
     grid.sync();
-    double ra, rb;
-    grid_sum2(P.part + (size_t)(phase & 1) * 2 * gridDim.x, gridDim.x, ra, rb, bc);
+    const double* pp = P.part + (size_t)(phase & 1) * 2 * gridDim.x;
+    if (threadIdx.x < 32) {
+      double sa = 0.0, sb = 0.0;
+      for (int i = threadIdx.x; i < (int)gridDim.x; i += 32) { sa += pp[2 * i]; sb += pp[2 * i + 1]; }
+      sa = warp_sum(sa);
+      sb = warp_sum(sb);
+      if (threadIdx.x == 0) { bc[0] = sa; bc[1] = sb; }
+    }
+    if (pf != nullptr && stage) {
+      const int bd = blockDim.x;
+      int j = threadIdx.x;
+      for (; j + 3 * bd < n; j += 4 * bd) {
+        const double v0 = __ldcg(pf + j), v1 = __ldcg(pf + j + bd), v2 = __ldcg(pf + j + 2 * bd),
+                     v3 = __ldcg(pf + j + 3 * bd);
+        ys[j] = v0; ys[j + bd] = v1; ys[j + 2 * bd] = v2; ys[j + 3 * bd] = v3;
+      }
+      for (; j < n; j += bd) ys[j] = __ldcg(pf + j);
+      pre = true;
+    }
+    __syncthreads();
+    const double ra = bc[0], rb = bc[1];
+    __syncthreads();
     ++phase;
     return make_double2(ra, rb);
   };
@@ -371,7 +388,7 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
     double pz = 0.0;
     for (int r = gw; r < n; r += tw)
       if (lane == 0) pz = fma(__ldcg(P.vec + r), __ldcg(P.vec + r), pz);
-    double2 s = publish(0.0, pz);
+    double2 s = publish(0.0, pz, P.vec + (size_t)cur * n);
     sigma = sqrt(s.y);
     for (;;) {
       if (sigma == 0.0) {
@@ -380,7 +397,7 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
         double pyz, pzz;
         matvec(P.B, P.ldb, P.brows, P.bcols, P.vr, 1.0, false, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
         cur ^= 1;
-        s = publish(0.0, pzz);
+        s = publish(0.0, pzz, P.vec + (size_t)cur * n);
         restarted = true;
         prev = -1.0;
         if (it >= P.max_iters) { sigma = 0.0; conv = 0.0; it = P.max_iters; break; }
@@ -394,7 +411,7 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
       double pyz, pzz;
       if (stage) gmatvec(P.vec + (size_t)cur * n, sc, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
       else matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
-      s = publish(pyz, pzz);
+      s = publish(pyz, pzz, P.vec + (size_t)(cur ^ 1) * n);
       const double nw = sqrt(s.x);
       if (nw == 0.0) { conv = 1.0; break; }
       if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
@@ -412,7 +429,7 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
       double pyz, pzz;
       if (stage) gmatvec(P.vec + (size_t)cur * n, sc, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
       else matvec(P.G, P.ldg, n, n, P.vec + (size_t)cur * n, sc, stage, P.vec + (size_t)(cur ^ 1) * n, pyz, pzz);
-      double2 s = publish(pyz, pzz);
+      double2 s = publish(pyz, pzz, P.vec + (size_t)(cur ^ 1) * n);
       sigma = sqrt(fmax(s.x, 0.0));
       if (sigma == 0.0) {
         if (restarted) { conv = 1.0; break; }
@@ -420,6 +437,7 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
         for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
           P.vec[(size_t)cur * n + j] = P.vr[j];
         grid.sync();
+        pre = false;   // the prefetched z is not the restart vector
         restarted = true;
         prev = -1.0;
         sc = 1.0;
