@@ -255,6 +255,16 @@ int ibmi_ipc_handle(void* ptr, void* handle64);
 int ibmi_ipc_open(int device, const void* handle64, void** ptr);
 int ibmi_ipc_close(void* ptr);
 
+/* Device block cache (the library's allocator): buffers freed by destroyed
+ * contexts stay reserved per device and are reused by the next context of a
+ * similar shape, instead of paying cudaFree/cudaMalloc of GB-sized blocks per
+ * solve.  Capped at a quarter of device memory (env IBMI_MEM_CACHE_MB; 0 turns
+ * it off).  No reference counterpart: the reference allocates with NumPy
+ * (solver.py:250, :120).  release: return device `device`'s cached blocks to
+ * the driver (device < 0: all devices); cached: bytes currently held. */
+int ibmi_release_cached_memory(int device);
+int ibmi_cached_bytes(int device, int64_t* bytes);
+
 /* Number of kernels this library has launched in the process (graph replays
  * count their kernel nodes) — the `gpu_launches` of bench.py. */
 long long ibmi_launch_count(void);

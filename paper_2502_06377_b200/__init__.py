@@ -53,3 +53,22 @@ def load_library():
     from . import _abi
 
     return _abi.lib()
+
+
+def release_cached_memory(device: int = -1) -> None:
+    """Return the device blocks the library keeps between solves to the driver
+    (``device < 0``: every device).  See ``ibmi_release_cached_memory``."""
+    from . import _abi
+
+    _abi.check(_abi.lib().ibmi_release_cached_memory(int(device)), "release_cached_memory")
+
+
+def cached_bytes(device: int = -1) -> int:
+    """Bytes of device memory held in the library's block cache."""
+    import ctypes
+
+    from . import _abi
+
+    out = ctypes.c_int64()
+    _abi.check(_abi.lib().ibmi_cached_bytes(int(device), ctypes.byref(out)), "cached_bytes")
+    return int(out.value)

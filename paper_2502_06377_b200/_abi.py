@@ -70,6 +70,8 @@ SIGNATURES = [
     ("ibmi_ipc_handle", C.c_int, [_P, C.c_char_p]),
     ("ibmi_ipc_open", C.c_int, [C.c_int, C.c_char_p, C.POINTER(_P)]),
     ("ibmi_ipc_close", C.c_int, [_P]),
+    ("ibmi_release_cached_memory", C.c_int, [C.c_int]),
+    ("ibmi_cached_bytes", C.c_int, [C.c_int, C.POINTER(_I64)]),
     ("ibmi_launch_count", C.c_longlong, []),
     ("ibmi_tune", C.c_int, [C.c_int, C.c_int]),
     ("ibmi_probe_fp64_peak", C.c_int, [C.c_int, _D]),

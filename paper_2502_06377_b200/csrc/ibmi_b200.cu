@@ -54,6 +54,147 @@ int fail(int code, const std::string& msg) {
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// ------------------------------------------------------ device block cache
+// Every device buffer of a context (A, Σ, W_k, workspaces, residue planes) is
+// a multi-GB cudaMalloc, and cudaMalloc/cudaFree of that size cost 10–700 ms
+// each depending on what the driver has to map or unmap.  Freed blocks are
+// therefore kept per device and handed to the next request of a similar size
+// (a repeated solve of the same shape reuses every block), up to a cap of a
+// quarter of the device's memory (IBMI_MEM_CACHE_MB overrides; 0 disables).
+// release() synchronises the device first, as cudaFree does, so a cached block
+// is never reused while kernels still touch it.  When cudaMalloc fails the
+// device's cache is returned to the driver and the request retried;
+// ibmi_release_cached_memory() does that on demand.
+struct DevBlock { size_t bytes; int dev; };
+std::mutex g_mem_mu;
+struct MemCache {
+  std::vector<std::pair<void*, DevBlock>> live;    // small: tens of blocks per context
+  std::vector<std::pair<void*, DevBlock>> free;
+  size_t free_bytes[64] = {};
+};
+MemCache g_mem;
+
+size_t mem_cache_cap(int dev) {
+  static long long env = [] {
+    const char* v = getenv("IBMI_MEM_CACHE_MB");
+    return v ? atoll(v) : -1ll;
+  }();
+  if (env >= 0) return (size_t)env << 20;
+  static size_t caps[64] = {};
+  if (dev < 0 || dev >= 64) return 0;
+  if (!caps[dev]) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); return 0; }
+    caps[dev] = tot / 4;
+  }
+  return caps[dev];
+}
+
+// Return every cached block of `dev` (or of all devices, dev < 0) to the driver.
+void mem_flush_locked(int dev) {
+  auto& fl = g_mem.free;
+  for (size_t i = 0; i < fl.size();) {
+    if (dev < 0 || fl[i].second.dev == dev) {
+      (cudaFree)(fl[i].first);
+      g_mem.free_bytes[fl[i].second.dev & 63] -= fl[i].second.bytes;
+      fl[i] = fl.back();
+      fl.pop_back();
+    } else {
+      ++i;
+    }
+  }
+}
+
+// IBMI_MEM_POISON=1: fill every block handed out with 0xFF bytes (NaN), so a
+// kernel that reads memory it never wrote shows up in the parity tests.
+cudaError_t mem_poison(void* p, size_t bytes) {
+  static int on = getenv("IBMI_MEM_POISON") ? 1 : 0;
+  if (!on) return cudaSuccess;
+  cudaError_t e = cudaMemset(p, 0xFF, bytes);
+  return e == cudaSuccess ? cudaDeviceSynchronize() : e;
+}
+
+cudaError_t mem_alloc_raw(void** out, size_t bytes);
+cudaError_t mem_alloc(void** out, size_t bytes) {
+  cudaError_t pe = mem_alloc_raw(out, bytes);
+  if (pe == cudaSuccess && *out) pe = mem_poison(*out, bytes);
+  return pe;
+}
+
+cudaError_t mem_alloc_raw(void** out, size_t bytes) {
+  if (bytes == 0) return (cudaMalloc)(out, 0);
+  const size_t need = (size_t)round_up((int64_t)bytes, 512);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  // best fit among cached blocks of this device no more than 1/8 larger
+  int best = -1;
+  for (int i = 0; i < (int)g_mem.free.size(); ++i) {
+    const DevBlock& b = g_mem.free[i].second;
+    if (b.dev == dev && b.bytes >= need && b.bytes - need <= need / 8 &&
+        (best < 0 || b.bytes < g_mem.free[best].second.bytes))
+      best = i;
+  }
+  if (best >= 0) {
+    *out = g_mem.free[best].first;
+    g_mem.free_bytes[dev & 63] -= g_mem.free[best].second.bytes;
+    g_mem.live.push_back(g_mem.free[best]);
+    g_mem.free[best] = g_mem.free.back();
+    g_mem.free.pop_back();
+    return cudaSuccess;
+  }
+  e = (cudaMalloc)(out, need);
+  if (e == cudaErrorMemoryAllocation && g_mem.free_bytes[dev & 63] > 0) {
+    cudaGetLastError();
+    mem_flush_locked(dev);
+    e = (cudaMalloc)(out, need);
+  }
+  if (e != cudaSuccess) return e;
+  g_mem.live.push_back({*out, DevBlock{need, dev}});
+  return cudaSuccess;
+}
+
+cudaError_t mem_release(void* p) {
+  if (!p) return cudaSuccess;
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  int idx = -1;
+  for (int i = (int)g_mem.live.size() - 1; i >= 0; --i)
+    if (g_mem.live[i].first == p) { idx = i; break; }
+  if (idx < 0) return (cudaFree)(p);        // not ours
+  const DevBlock b = g_mem.live[idx].second;
+  g_mem.live[idx] = g_mem.live.back();
+  g_mem.live.pop_back();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != b.dev) cudaSetDevice(b.dev);
+  cudaError_t e = cudaDeviceSynchronize();   // cudaFree's implicit synchronisation
+  if (e == cudaSuccess && g_mem.free_bytes[b.dev & 63] + b.bytes <= mem_cache_cap(b.dev)) {
+    g_mem.free.push_back({p, b});
+    g_mem.free_bytes[b.dev & 63] += b.bytes;
+  } else {
+    e = (cudaFree)(p);
+  }
+  if (cur != b.dev) cudaSetDevice(cur);
+  return e;
+}
+
+// cudaMemGetInfo that counts this device's cached blocks as free.
+cudaError_t mem_info(size_t* fr, size_t* tot) {
+  cudaError_t e = cudaMemGetInfo(fr, tot);
+  if (e != cudaSuccess) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  *fr += g_mem.free_bytes[dev & 63];
+  return cudaSuccess;
+}
+
+// Everything below allocates through the cache.  The IPC-exported panels
+// (ibmi_device_alloc) call the driver directly as (cudaMalloc)/(cudaFree).
+#define cudaMalloc(P, N) mem_alloc(reinterpret_cast<void**>(P), (size_t)(N))
+#define cudaFree(P) mem_release((void*)(P))
+
 // Every kernel this library launches bumps the counter (graph replays add the
 // number of kernel nodes captured), so callers can report `gpu_launches`.
 std::atomic<long long> g_launches{0};
@@ -889,7 +1030,7 @@ bool oz_cache_build(OzCache& cc, const GemmOp& op, bool y, int n, size_t margin,
   const int64_t rows = y ? op.N : op.M;
   const size_t need = (size_t)n * rows * pl.ldq + (size_t)rows * sizeof(int);
   size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || fr < need + margin) { cudaGetLastError(); return false; }
+  if (mem_info(&fr, &tot) != cudaSuccess || fr < need + margin) { cudaGetLastError(); return false; }
   if (cudaMalloc(&cc.q, (size_t)n * rows * pl.ldq) != cudaSuccess) { cudaGetLastError(); cc.q = nullptr; return false; }
   if (cudaMalloc(&cc.e, (size_t)rows * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
@@ -941,7 +1082,11 @@ int staged_copy(double* dev, int64_t ldd, double* host, int64_t ldh, int64_t row
   const int64_t chunk_rows = std::max<int64_t>(1, (int64_t)(STAGE_SLOT / row_bytes));
   const int64_t nchunks = (rows + chunk_rows - 1) / chunk_rows;
   unsigned hc = std::thread::hardware_concurrency();
-  const int nthreads = (int)std::min<int64_t>(nchunks, std::max(1u, std::min(8u, hc ? hc : 1u)));
+  static const unsigned cap = [] {
+    const char* v = getenv("IBMI_STAGE_THREADS");
+    return v ? (unsigned)std::max(1, atoi(v)) : 12u;
+  }();
+  const int nthreads = (int)std::min<int64_t>(nchunks, std::max(1u, std::min(cap, hc ? hc : 1u)));
   std::lock_guard<std::mutex> lock(g_pool.mu);
   while ((int)g_pool.slots.size() < 2 * nthreads) {
     void* p = nullptr;
@@ -1685,7 +1830,7 @@ int plan_workspace(ibmi_ctx* c) {
       const int64_t ldq = round_up(c->p, 16);
       const size_t need = (size_t)n * c->p * ldq + 2 * (size_t)c->p * sizeof(int);
       size_t fr = 0, tot_mem = 0;
-      if (cudaMemGetInfo(&fr, &tot_mem) == cudaSuccess && fr >= need + margin &&
+      if (mem_info(&fr, &tot_mem) == cudaSuccess && fr >= need + margin &&
           cudaMalloc(&c->oz_s.q, (size_t)n * c->p * ldq) == cudaSuccess &&
           cudaMalloc(&c->oz_s.e, (size_t)c->p * sizeof(int)) == cudaSuccess &&
           cudaMalloc(&c->oz_s.flags, (size_t)c->p * sizeof(int)) == cudaSuccess &&
@@ -2993,16 +3138,32 @@ int ibmi_export(ibmi_ctx* c, int which, int k, double** ptr, int64_t* rows, int6
   return fail(IBMI_ERR_INVALID, "unknown buffer");
 }
 
+int ibmi_release_cached_memory(int device) {
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  mem_flush_locked(device);
+  return IBMI_OK;
+}
+
+int ibmi_cached_bytes(int device, int64_t* bytes) {
+  if (!bytes) return fail(IBMI_ERR_INVALID, "null argument");
+  std::lock_guard<std::mutex> lock(g_mem_mu);
+  size_t t = 0;
+  for (int d = 0; d < 64; ++d)
+    if (device < 0 || d == device) t += g_mem.free_bytes[d];
+  *bytes = (int64_t)t;
+  return IBMI_OK;
+}
+
 int ibmi_device_alloc(int device, int64_t bytes, void** ptr) {
   if (!ptr || bytes < 0) return fail(IBMI_ERR_INVALID, "bad argument");
   CUDA_TRY(cudaSetDevice(device));
-  CUDA_TRY(cudaMalloc(ptr, bytes > 0 ? bytes : 8));
+  CUDA_TRY((cudaMalloc)(ptr, bytes > 0 ? bytes : 8));   // not cached: exported over CUDA IPC
   CUDA_TRY(cudaMemset(*ptr, 0, bytes > 0 ? bytes : 8));
   return IBMI_OK;
 }
 
 int ibmi_device_free(void* ptr) {
-  if (ptr) CUDA_TRY(cudaFree(ptr));
+  if (ptr) CUDA_TRY((cudaFree)(ptr));
   return IBMI_OK;
 }
 
