@@ -511,12 +511,13 @@ def run_ours(args):
         panel_tf = panel_flops / (kt_["panel_gemm"] * 1e-3) / 1e12
         return {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
                 "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s", "frac": panel_tf / peak,
-                "traffic": 6.50e9 if args.config == "c4" else None,
-                "traffic_note": ("ncu dram read+write bytes of one interior-set panel GEMM launch "
-                                 "(profiles/r01_c4_sweep.md); algorithmic minimum 2.38e9 (W + Sigma_cc read once, "
-                                 "M written twice). W (288 MB) and Sigma_cc (1.58 GB) exceed the 126 MB L2, so each "
-                                 "148-tile wave re-streams all of W from HBM (15 waves): ~5.9 GB read at 2% of HBM "
-                                 "bandwidth, while the kernel is DMMA-bound") if args.config == "c4"
+                "traffic": 15.78e9 if args.config == "c4" else None,
+                "traffic_note": ("ncu dram read+write bytes of one interior-set panel GEMM launch, split-K 3 "
+                                 "(profiles/r01_final2_c4_sweep.md): 14.94e9 read + 0.84e9 written (the partial "
+                                 "tiles; splitk_reduce_kernel writes M and its mirror). Algorithmic minimum 2.38e9 "
+                                 "(W + Sigma_cc read once, M written twice). W (283 MB) and Sigma_cc (1.53 GB) "
+                                 "exceed the 126 MB L2, so the resident CTAs re-stream them: 0.55 TB/s, 8% of HBM "
+                                 "bandwidth, while the DMMA pipe is 97.6% busy") if args.config == "c4"
                 else "measured for c4 only",
                 "peak_source": "measured on this box: DMMA m8n8k4 throughput probe (ibmi_probe_fp64_peak)"}
 

@@ -283,7 +283,9 @@ long long ibmi_launch_count(void);
  * key 10: N chunks of the two-stream emulated GEMM pipeline (default 1 = no overlap:
  *         the conversion shares the L1/shared-memory datapath with the INT8
  *         GEMM's operand reads, so overlapping them gained nothing);
- * key 11: INT8 GEMM on CTA pairs (cta_group::2, default 1) or single CTAs (0). */
+ * key 11: INT8 GEMM on CTA pairs (cta_group::2, default 1) or single CTAs (0);
+ * key 12: FP64 GEMM tile raster: bands of this many 128-row tile rows walked column by
+ *         column (default 8; 0 = tile-row-major). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

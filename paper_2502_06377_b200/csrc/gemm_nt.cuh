@@ -81,8 +81,35 @@ struct GemmParams {
   int bc_world, bc_rank;
   int lower;                                 // only tiles tm >= tn; in diagonal tiles only m >= n
   int tiles_m, tiles_n;
+  int group_m = 0;                           // raster: bands of group_m tile rows, tn-major inside (0: tm-major)
   double* partial;                           // EPI_FROB: one partial sum per CTA; EPI_PARTIAL: split tiles
 };
+
+// Output tile of linear tile index `tile` (the GEMM kernels and the split-K
+// reduction must agree).  lower: row-major over the lower triangle.  group_m:
+// the M tiles are cut into bands of group_m rows and each band is walked
+// column by column, so the CTAs resident at once share a few X row blocks and
+// a few Y row blocks (L2 hits) instead of all of X.  Otherwise tm-major.
+__device__ __forceinline__ void tile_coords(const GemmParams& P, int tile, int& tm, int& tn) {
+  if (P.lower) {
+    int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+    while (r * (r + 1) / 2 > tile) --r;
+    tm = r;
+    tn = tile - r * (r + 1) / 2;
+  } else if (P.group_m > 0 && P.group_m < P.tiles_m) {
+    const int per = P.group_m * P.tiles_n;
+    const int band = tile / per;
+    const int first = band * P.group_m;
+    const int gm = min(P.group_m, P.tiles_m - first);
+    const int r = tile - band * per;
+    tm = first + r % gm;
+    tn = r / gm;
+  } else {
+    tm = tile % P.tiles_m;
+    tn = tile / P.tiles_m;
+  }
+}
 
 // Direct-store address of element (m, n) (rowc = cidx/cm row already mapped).
 __device__ __forceinline__ double* direct_addr(const GemmParams& P, int64_t rowc, int n) {
@@ -207,16 +234,7 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
     tile /= P.splits;
   }
   int tm, tn;
-  if (P.lower) {
-    int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
-    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
-    while (r * (r + 1) / 2 > tile) --r;
-    tm = r;
-    tn = tile - r * (r + 1) / 2;
-  } else {
-    tm = tile % P.tiles_m;
-    tn = tile / P.tiles_m;
-  }
+  tile_coords(P, tile, tm, tn);
   const int m0 = tm * GB_M;
   const int n0 = tn * GB_N;
 
@@ -384,16 +402,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) 
   const int tile = blockIdx.x / (GB_M / 32);
   const int rc = (blockIdx.x % (GB_M / 32)) * 32;
   int tm, tn;
-  if (P.lower) {
-    int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
-    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
-    while (r * (r + 1) / 2 > tile) --r;
-    tm = r;
-    tn = tile - r * (r + 1) / 2;
-  } else {
-    tm = tile % P.tiles_m;
-    tn = tile / P.tiles_m;
-  }
+  tile_coords(P, tile, tm, tn);
   const bool diag_tile = P.lower && tm == tn;
   const double* src = P.partial + (size_t)tile * P.splits * GB_M * GB_N;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

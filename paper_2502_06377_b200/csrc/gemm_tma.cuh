@@ -103,16 +103,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
     tile /= P.splits;
   }
   int tm, tn;
-  if (P.lower) {
-    int r = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
-    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
-    while (r * (r + 1) / 2 > tile) --r;
-    tm = r;
-    tn = tile - r * (r + 1) / 2;
-  } else {
-    tm = tile % P.tiles_m;
-    tn = tile / P.tiles_m;
-  }
+  tile_coords(P, tile, tm, tn);
   const int m0 = tm * GB_M;
   const int n0 = tn * GB_N;
   int kt_begin = 0, kt_end = P.kt_total;

@@ -236,6 +236,7 @@ int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
 int g_split_min_kt = 4;     // split-K keeps at least this many k-tiles per split
+int g_raster_group = 0;     // GEMM tile raster: bands of this many tile rows (0 = tm-major)
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
 int g_use_tma = 1;          // TMA/mbarrier kernel for eligible hot GEMMs
 
@@ -414,6 +415,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
   P.peers = op.peers; P.bc_panel = op.bc_panel; P.bc_world = op.bc_world; P.bc_rank = op.bc_rank;
   P.tiles_m = (P.M + GB_M - 1) / GB_M;
   P.tiles_n = (P.N + GB_N - 1) / GB_N;
+  P.group_m = g_raster_group;
   const int tiles = gemm_tiles(op);
   // 16-byte cp.async only when every operand address it forms is 16B aligned
   bool v16 = aligned16(op.X) && aligned16(op.Y) && (op.ldx % 2 == 0) && (op.ldy % 2 == 0);
@@ -3278,6 +3280,10 @@ int ibmi_tune(int key, int value) {
       break;
     case 11:
       g_oz_pair = value ? 1 : 0;
+      break;
+    case 12:
+      if (value < 0 || value > 1024) return fail(IBMI_ERR_INVALID, "raster group must be in [0, 1024]");
+      g_raster_group = value;
       break;
     case 10:
       if (value < 1 || value > 16) return fail(IBMI_ERR_INVALID, "Ozaki pipeline chunks must be in [1, 16]");

@@ -14,7 +14,14 @@ from paper_2502_06377_b200.device import DeviceSolver  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--sweeps", type=int, default=1)
+ap.add_argument("--tune", action="append", default=[], help="key=value for ibmi_tune (repeatable)")
 args = ap.parse_args()
+if args.tune:
+    from paper_2502_06377_b200 import _abi
+
+    for kv in args.tune:
+        k, v = kv.split("=")
+        _abi.check(_abi.lib().ibmi_tune(int(k), int(v)), "tune")
 cfg = configs.get_config(args.config)
 a = torch.as_tensor(configs.make_matrix(args.config), device="cuda")
 s = torch.cuda.Stream()
