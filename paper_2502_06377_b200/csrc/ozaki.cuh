@@ -211,13 +211,15 @@ __device__ __forceinline__ double oz_crt_value(const OzTable& T, const uint32_t*
   return ldexp(d, -shift);
 }
 
-// Block: 256 threads = 8 warps; tile 32 rows x 128 columns; thread = 4
-// consecutive columns of 4 rows.  Mirror stores go through a shared-memory
-// transpose so both stores are coalesced.
+// Block: 256 threads = 8 warps; tile 16 rows x 128 columns; thread = 4
+// consecutive columns of 2 rows.  Mirror stores go through a shared-memory
+// transpose so both stores are coalesced.  Column 4·lane + b of a tile row sits
+// at b·33 + lane: each warp store is 32 consecutive doubles (no bank conflicts;
+// 4·lane + b would put lanes 8 banks apart, an 8-way conflict).
 template <int NM>
 __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const OzCrt E) {
   constexpr int TR = 16;          // tile rows (16.5 KB of shared memory: co-resides with the INT8 GEMM)
-  __shared__ double tile[TR][129];
+  __shared__ double tile[TR][4 * 33 + 1];
   const OzTable& T = c_oz[NM - OZ_MINN];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tiles_j = (E.ncols + 127) / 128, tiles_i = (E.M + TR - 1) / TR;
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
     }
     if (P.mirror) {
 #pragma unroll
-      for (int b = 0; b < 4; ++b) tile[il][4 * lane + b] = ok4[b] ? v4[b] : __longlong_as_double(-1ll);
+      for (int b = 0; b < 4; ++b) tile[il][b * 33 + lane] = ok4[b] ? v4[b] : __longlong_as_double(-1ll);
     }
   }
   if (!P.mirror) continue;
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256) oz_crt_kernel(const GemmParams P, const O
     for (int jj = 2 * warp + (lane >> 4); jj < 128; jj += 16) {
       const int j = j0 + jj;
       if (j >= E.ncols) break;
-      const double v = tile[il][jj];
+      const double v = tile[il][(jj & 3) * 33 + (jj >> 2)];
       if (__double_as_longlong(v) == -1ll) continue;   // not computed (lower mask)
       P.C2[map_idx(P.c2n, E.j_off + j) * P.ldc2 + mc] = v;
     }
