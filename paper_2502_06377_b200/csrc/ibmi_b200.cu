@@ -1299,6 +1299,7 @@ int potrf_enqueue(CholScratch& cs, int n, cudaStream_t s, int* info) {
     pn.M = n - j1; pn.N = jb;
     pn.add_seg(j0, 0, jb);
     pn.C = a; pn.ldc = ld; pn.cm = contig_map(j1); pn.cn = contig_map(j0);
+    pn.tma_ok = true; pn.xrows = n; pn.xcols = n; pn.yrows = jb; pn.ycols = jb;
     CUDA_TRY(launch_gemm(pn, s));
     // trailing: A[j1:, j1:] -= P Pᵀ  (lower tiles only)
     GemmOp tr;
@@ -1309,6 +1310,7 @@ int potrf_enqueue(CholScratch& cs, int n, cudaStream_t s, int* info) {
     tr.C = a; tr.ldc = ld; tr.cm = contig_map(j1); tr.cn = contig_map(j1);
     tr.alpha = -1.0; tr.beta = 1.0; tr.D = a; tr.ldd = ld; tr.dm = contig_map(j1); tr.dn = contig_map(j1);
     tr.lower = true;
+    tr.tma_ok = true; tr.xrows = n; tr.xcols = n; tr.yrows = n; tr.ycols = n;
     CUDA_TRY(launch_gemm(tr, s));
   }
   return IBMI_OK;
@@ -2358,6 +2360,8 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
       gw.M = b; gw.N = p - b;
       gw.add_seg(0, lo, b);
       gw.C = s.W; gw.ldc = c->ld; gw.cn = complement_map(lo, hi);
+      // K tails end at the segment ends (the TMA maps stop there and zero-fill)
+      gw.tma_ok = true; gw.xrows = b; gw.xcols = b; gw.yrows = p; gw.ycols = p;
       SETUP_TRY(launch_gemm(gw, sq));
     }
   }
