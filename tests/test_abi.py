@@ -50,3 +50,15 @@ def test_library_is_sm100a():
 
     data = open(_abi.LIB_PATH, "rb").read()
     assert b"sm_100a" in data
+
+
+def test_block_cache_entry_points_without_gpu():
+    """The device block cache's ABI answers on a CPU-only host: nothing cached,
+    release is a no-op (neither entry point touches CUDA when the cache is empty)."""
+    import paper_2502_06377_b200 as pkg
+    from paper_2502_06377_b200 import _abi
+
+    assert pkg.cached_bytes() == 0
+    assert pkg.cached_bytes(0) == 0
+    pkg.release_cached_memory()
+    assert _abi.lib().ibmi_cached_bytes(-1, None) == _abi.ERR_INVALID
