@@ -32,6 +32,8 @@ import time
 
 import numpy as np
 
+_JSON_OUT = sys.stdout   # replaced by a private dup of fd 1 when run as a script
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -198,7 +200,7 @@ def run_reference(args):
                          "sample": sample},
         "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_JSON_OUT, flush=True)
 
 
 def executed_flops(cfg):
@@ -569,12 +571,18 @@ def run_ours(args):
                 "gpu_launches": int(alt["launches"]), "clocks": alt["clocks"],
                 "note": "same context, same Sigma0 and sweep count; Sigma compared after warmup+steps sweeps",
             }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_JSON_OUT, flush=True)
     if world > 1 or args.sharded:
         torch.distributed.destroy_process_group()
 
 
 if __name__ == "__main__":
+    # The driver reads rank 0's stdout as exactly one JSON line, but NCCL (and
+    # anything else in the process) may write to fd 1 -- e.g. "NCCL version ..."
+    # at the first collective.  Keep a private copy of stdout for the JSON line
+    # and point fd 1 at stderr for everything else.
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     a = parse()
     if a.impl == "reference":
         run_reference(a)
