@@ -186,6 +186,31 @@ int ibmi_emulation_timing(double* ms, double* int8_ops, int* launches);
 int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64_t ldo, int64_t* fail_pivot,
                      void* stream);
 
+/* Lower Cholesky factor of SPD A (device n×n) into l (strict upper zeroed);
+ * replaces cholesky (linalg.py:96-109, dpotrf lower clean=1).  Reads only the
+ * lower triangle (the caller checks symmetry, linalg.py:68-77).  On
+ * IBMI_ERR_NOT_SPD *fail_pivot = the failing elimination step (info − 1). */
+int ibmi_cholesky(int64_t n, const double* a, int64_t lda, double* l, int64_t ldl, int64_t* fail_pivot,
+                  void* stream);
+
+/* x = (L Lᵀ)⁻¹ b for a lower factor l (device n×n) and b (device n×nrhs);
+ * replaces chol_solve (linalg.py:112-119, dpotrs): L⁻¹ by blocked trtri, then
+ * two GEMMs. */
+int ibmi_chol_solve(int64_t n, const double* l, int64_t ldl, int64_t nrhs, const double* b, int64_t ldb, double* x,
+                    int64_t ldx, void* stream);
+
+/* out[i][j] = a[rows[i]][cols[j]] (device arrays); replaces gather
+ * (linalg.py:186-191).  Indices are checked by the caller (_check_indices). */
+int ibmi_gather(const double* a, int64_t lda, const int64_t* rows, int64_t nr, const int64_t* cols, int64_t nc,
+                double* out, int64_t ldo, void* stream);
+
+/* target[rows[i]][cols[j]] = (add ? target[..] : 0) + src[i][j] (device arrays);
+ * replaces scatter_add_assign (linalg.py:194-211).  The grid must not repeat an
+ * element: the caller resolves repeated indices to their last occurrence, which
+ * is what NumPy's fancy assignment keeps. */
+int ibmi_scatter(double* target, int64_t ldt, const int64_t* rows, int64_t nr, const int64_t* cols, int64_t nc,
+                 const double* src, int64_t lds, int add, void* stream);
+
 /* Monte Carlo guess block (solver.py:167-181) for any ordering: A (device, p×p),
  * w (host, p×n standard-normal draws of default_rng(mc_seed)), comp (host, c
  * ascending indices); out (device, c×c) = (L⁻ᵀw)_c (L⁻ᵀw)_cᵀ / n. */

@@ -105,6 +105,36 @@ void mem_flush_locked(int dev) {
   }
 }
 
+// Live contexts per device.  While none is left, the cache keeps at most
+// 1/16 of the device's memory (IBMI_MEM_IDLE_CACHE_MB overrides): enough for
+// the next solve of a c4-sized problem to reuse its blocks, without holding a
+// quarter of HBM against torch (or another process) between solves.
+int g_live_ctx[64] = {};
+
+size_t mem_idle_cap(int dev) {
+  static long long env = [] {
+    const char* v = getenv("IBMI_MEM_IDLE_CACHE_MB");
+    return v ? atoll(v) : -1ll;
+  }();
+  if (env >= 0) return (size_t)env << 20;
+  return mem_cache_cap(dev) / 4;
+}
+
+// Return cached blocks of `dev`, largest first, until at most `keep` bytes stay.
+void mem_trim_locked(int dev, size_t keep) {
+  auto& fl = g_mem.free;
+  while (g_mem.free_bytes[dev & 63] > keep) {
+    int big = -1;
+    for (int i = 0; i < (int)fl.size(); ++i)
+      if (fl[i].second.dev == dev && (big < 0 || fl[i].second.bytes > fl[big].second.bytes)) big = i;
+    if (big < 0) break;
+    (cudaFree)(fl[big].first);
+    g_mem.free_bytes[dev & 63] -= fl[big].second.bytes;
+    fl[big] = fl.back();
+    fl.pop_back();
+  }
+}
+
 // IBMI_MEM_POISON=1: fill every block handed out with 0xFF bytes (NaN), so a
 // kernel that reads memory it never wrote shows up in the parity tests.
 cudaError_t mem_poison(void* p, size_t bytes) {
@@ -1438,6 +1468,7 @@ struct ibmi_ctx {
   int64_t p = 0, ld = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  bool counted = false;      // included in g_live_ctx[device]
   double* A = nullptr;
   double* S = nullptr;
   bool a_set = false;
@@ -2084,6 +2115,11 @@ int ibmi_create(ibmi_ctx** out, int device, int64_t p, void* stream) {
     if (e != cudaSuccess) { delete c; return fail(IBMI_ERR_CUDA, cudaGetErrorString(e)); }
     c->own_stream = true;
   }
+  if (device >= 0 && device < 64) {
+    std::lock_guard<std::mutex> lock(g_mem_mu);
+    ++g_live_ctx[device];
+    c->counted = true;
+  }
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   c->oz_n = g_oz_n;
   g_sms_hint = c->sms;
@@ -2127,7 +2163,13 @@ int ibmi_destroy(ibmi_ctx* c) {
     if (q) cudaFree(q);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  const int dev = c->device;
+  const bool counted = c->counted;
   delete c;
+  {
+    std::lock_guard<std::mutex> lock(g_mem_mu);
+    if (counted && dev >= 0 && dev < 64 && --g_live_ctx[dev] == 0) mem_trim_locked(dev, mem_idle_cap(dev));
+  }
   pt.mark("free");
   return IBMI_OK;
 }
@@ -2999,6 +3041,98 @@ int ibmi_spd_inverse(int64_t n, const double* a, int64_t lda, double* out, int64
   cudaStreamSynchronize(st);
   cs.release();
   return rc;
+}
+
+int ibmi_cholesky(int64_t n, const double* a, int64_t lda, double* l, int64_t ldl, int64_t* fail_pivot,
+                  void* stream) {
+  if (n < 1) return fail(IBMI_ERR_DIM, "matrix must be nonempty");
+  if (!a || !l) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (lda < n || ldl < n) return fail(IBMI_ERR_DIM, "leading dimension < n");
+  cudaStream_t st = (cudaStream_t)stream;
+  CholScratch cs;
+  int rc = ensure_scratch(cs, (int)n);
+  if (rc) { cs.release(); return rc; }
+  copy2d_kernel<<<grid2d(n, n), 256, 0, st>>>(a, lda, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)n, (int)n, 1); note_launch();
+  int64_t piv = -1;
+  rc = potrf_blocked(cs, (int)n, st, &piv);
+  if (rc == IBMI_ERR_NOT_SPD && fail_pivot) *fail_pivot = piv;
+  if (!rc) {   // lower factor, strict upper zeroed (dpotrf clean=1, linalg.py:104)
+    copy2d_kernel<<<grid2d(n, n), 256, 0, st>>>(cs.ws, cs.ldw, contig_map(0), contig_map(0), l, ldl, (int)n, (int)n, 1);
+    note_launch();
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  cs.release();
+  if (!rc && e != cudaSuccess) return fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+  return rc;
+}
+
+int ibmi_chol_solve(int64_t n, const double* l, int64_t ldl, int64_t nrhs, const double* b, int64_t ldb, double* x,
+                    int64_t ldx, void* stream) {
+  if (n < 1 || nrhs < 1) return fail(IBMI_ERR_DIM, "empty system");
+  if (!l || !b || !x) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (ldl < n || ldb < nrhs || ldx < nrhs) return fail(IBMI_ERR_DIM, "leading dimension too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  CholScratch cs;
+  int rc = ensure_scratch(cs, (int)n);
+  if (rc) { cs.release(); return rc; }
+  double* y = nullptr;
+  cudaError_t e = cudaMalloc(&y, (size_t)n * nrhs * sizeof(double));
+  if (e != cudaSuccess) { cs.release(); return fail(IBMI_ERR_OOM, cudaGetErrorString(e)); }
+  // L⁻¹ (lower): diagonal blocks by substitution, then the blocked trtri
+  copy2d_kernel<<<grid2d(n, n), 256, 0, st>>>(l, ldl, contig_map(0), contig_map(0), cs.ws, cs.ldw, (int)n, (int)n, 1); note_launch();
+  trti2_blocks_kernel<<<(unsigned)((n + CHOL_NB - 1) / CHOL_NB), 256, 0, st>>>(cs.ws, cs.ldw, (int)n, cs.dinv); note_launch();
+  rc = trtri_blocked(cs, (int)n, st);
+  if (!rc) {
+    GemmOp g1;   // y = L⁻¹ b:  y[m][j] = Σ_k L⁻¹[m][k] b[k][j]
+    g1.X = cs.ws; g1.ldx = cs.ldw;
+    g1.Y = b; g1.ldy = ldb; g1.yt = true;
+    g1.M = n; g1.N = nrhs;
+    g1.add_seg(0, 0, n);
+    g1.C = y; g1.ldc = nrhs;
+    e = launch_gemm(g1, st);
+    GemmOp g2;   // x = L⁻ᵀ y:  x[m][j] = Σ_k L⁻¹[k][m] y[k][j]
+    g2.X = cs.ws; g2.ldx = cs.ldw; g2.xt = true;
+    g2.Y = y; g2.ldy = nrhs; g2.yt = true;
+    g2.M = n; g2.N = nrhs;
+    g2.add_seg(0, 0, n);
+    g2.C = x; g2.ldc = ldx;
+    if (e == cudaSuccess) e = launch_gemm(g2, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(IBMI_ERR_CUDA, cudaGetErrorString(e));
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(y);
+  cs.release();
+  return rc;
+}
+
+int ibmi_gather(const double* a, int64_t lda, const int64_t* rows, int64_t nr, const int64_t* cols, int64_t nc,
+                double* out, int64_t ldo, void* stream) {
+  if (nr < 0 || nc < 0) return fail(IBMI_ERR_DIM, "negative index count");
+  if (nr == 0 || nc == 0) return IBMI_OK;
+  if (!a || !rows || !cols || !out) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (ldo < nc) return fail(IBMI_ERR_DIM, "ldo < number of columns");
+  cudaStream_t st = (cudaStream_t)stream;
+  copy2d_kernel<<<grid2d(nr, nc), 256, 0, st>>>(a, lda, list_map(rows), list_map(cols), out, ldo, (int)nr, (int)nc, 0);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return IBMI_OK;
+}
+
+int ibmi_scatter(double* target, int64_t ldt, const int64_t* rows, int64_t nr, const int64_t* cols, int64_t nc,
+                 const double* src, int64_t lds, int add, void* stream) {
+  if (nr < 0 || nc < 0) return fail(IBMI_ERR_DIM, "negative index count");
+  if (nr == 0 || nc == 0) return IBMI_OK;
+  if (!target || !rows || !cols || !src) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (lds < nc) return fail(IBMI_ERR_DIM, "lds < number of columns");
+  cudaStream_t st = (cudaStream_t)stream;
+  scatter_add2d_kernel<<<grid2d(nr, nc), 256, 0, st>>>(src, lds, target, ldt, list_map(rows), list_map(cols), (int)nr,
+                                                       (int)nc, add ? 1 : 0);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return IBMI_OK;
 }
 
 // Buffers of the stand-alone two_norm, kept per device between calls (the

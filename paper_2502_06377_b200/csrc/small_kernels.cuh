@@ -60,6 +60,56 @@ __global__ void __launch_bounds__(256) potf2_trti2_kernel(double* a, int64_t lda
 }
 
 // ---------------------------------------------------------------------------
+// L⁻¹ of every CHOL_NB×CHOL_NB diagonal block of a lower-triangular n×n L
+// (block `blockIdx.x` at rows/cols [64·b, 64·b + nb)), by the same row-wise
+// forward substitution as potf2_trti2_kernel; feeds trtri_blocked when only
+// the factor is given (chol_solve, linalg.py:112-119).
+__global__ void __launch_bounds__(256) trti2_blocks_kernel(const double* __restrict__ l, int64_t ldl, int n,
+                                                            double* __restrict__ dinv) {
+  __shared__ double T[CHOL_NB][CHOL_NB + 2];
+  const int tid = threadIdx.x;
+  const int j0 = blockIdx.x * CHOL_NB;
+  const int nb = min(CHOL_NB, n - j0);
+  const double* a = l + (int64_t)j0 * ldl + j0;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    if (j <= i) T[i][j] = a[(int64_t)i * ldl + j];
+  }
+  __syncthreads();
+  for (int i = 0; i < nb; ++i) {
+    const int j = tid >> 2;
+    const int q = tid & 3;
+    double s = 0.0;
+    if (j <= i && j < nb) {
+      for (int k = j + q; k < i; k += 4) s += T[i][k] * T[j][k + 1];
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (q == 0 && j <= i && j < nb) T[j][i + 1] = ((i == j ? 1.0 : 0.0) - s) / T[i][i];
+    __syncthreads();
+  }
+  double* out = dinv + (size_t)blockIdx.x * CHOL_NB * CHOL_NB;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int i = e / nb, j = e % nb;
+    out[(int64_t)i * CHOL_NB + j] = j <= i ? T[j][i + 1] : 0.0;
+  }
+}
+
+// dst[rm(i)][cm(j)] = (add ? dst[rm(i)][cm(j)] : 0) + src[i][j]; the index
+// grid must not repeat an element (the host resolves repeats first).
+__global__ void scatter_add2d_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                                     int64_t ldd, RowMap rm, RowMap cmap, int rows, int cols, int add) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const int64_t c = map_idx(cmap, j);
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+    double* d = dst + map_idx(rm, i) * ldd + c;
+    const double v = src[(int64_t)i * lds + j];
+    *d = add ? *d + v : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // 2-D copy through row/column maps: dst[i][j] = src[rm(i)][cm(j)]
 // mode 0: full, mode 1: lower triangle, zero strict upper.
 __global__ void copy2d_kernel(const double* __restrict__ src, int64_t lds, RowMap rm, RowMap cmap,

@@ -38,6 +38,18 @@ def _is_cuda_tensor(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda", False))
 
 
+def _torch_stream_done(t) -> None:
+    """Wait for torch's current stream on ``t``'s device.
+
+    The library works on its own stream; a device tensor handed to it (or a
+    block torch just allocated for it to fill) may still be produced or read
+    by kernels queued on torch's stream, so that stream is drained before the
+    library's device-to-device copy reads or writes the tensor."""
+    import torch
+
+    torch.cuda.current_stream(t.device).synchronize()
+
+
 class DeviceSolver:
     """IBMI state for one solve on one GPU.
 
@@ -113,6 +125,8 @@ class DeviceSolver:
             if from_file:
                 _abi.check(L.ibmi_load_ibmi1(h, a.path.encode()), "load_ibmi1")
             else:
+                if on_dev:
+                    _torch_stream_done(a)
                 _abi.check(L.ibmi_set_matrix(h, C.c_void_p(_abi.dptr(a)), lda, int(on_dev)), "set_matrix")
             k = len(self.ranges)
             if self.general:
@@ -205,6 +219,7 @@ class DeviceSolver:
             if self.perm is not None:
                 idx = torch.as_tensor(self.perm, device=s.device)
                 s = s.index_select(0, idx).index_select(1, idx).contiguous()
+            _torch_stream_done(s)
             _abi.check(self._L.ibmi_set_sigma(self._h, C.c_void_p(s.data_ptr()), s.stride(0), 1), "set_sigma")
             return
         s = np.asarray(s, dtype=np.float64)
@@ -219,6 +234,7 @@ class DeviceSolver:
             import torch
 
             t = torch.empty((self.p, self.p), dtype=torch.float64, device=f"cuda:{self.device}")
+            _torch_stream_done(t)
             _abi.check(self._L.ibmi_get_sigma(self._h, C.c_void_p(t.data_ptr()), self.p, 1), "get_sigma")
             if self.perm is not None:
                 inv = torch.as_tensor(np.argsort(self.perm), device=t.device)

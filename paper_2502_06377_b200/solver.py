@@ -330,43 +330,43 @@ def _single_set(a, sigma, idx, comp):
     return [(0, idx.size)], np.concatenate([idx, comp]).astype(np.int64)
 
 
-def _require_symmetric_sigma(sigma: np.ndarray) -> None:
-    """The device kernels read a column of Σ as the row with the same index, so
-    Σ must be symmetric (every iterate of the reference is); refuse otherwise
-    rather than silently computing with Σᵀ."""
-    scale = float(np.abs(sigma).max()) if sigma.size else 0.0
-    if scale and float(np.abs(sigma - sigma.T).max()) > 1e-12 * scale:
-        raise ValueError("sigma is not symmetric: the B200 block update requires a symmetric approximation")
+def _is_symmetric(sigma: np.ndarray) -> bool:
+    return sigma.size == 0 or bool(np.array_equal(sigma, sigma.T))
 
 
 def block_update(a, sigma, idx, comp) -> None:
     """Apply one block-inverse update to ``sigma`` in place (solver.py:132-144).
 
     Like the reference, only a float64 ndarray ``sigma`` is updated in place;
-    any other input is converted and the result is discarded.
+    any other input is converted and the result is discarded.  ``sigma`` need
+    not be symmetric: the kernels read Σ[c, c] through rows of the device
+    copy, so a non-symmetric Σ is uploaded as Σᵀ.  The update writes only
+    mirrored pairs (Σ_II symmetrised, Σ_Ic = −M, Σ_cI = −Mᵀ), which are the
+    same in Σ and Σᵀ, and leaves Σ[c, c] untouched, so transposing back gives
+    exactly the reference's result.
     """
     a = np.asarray(a, dtype=np.float64)
     sigma = np.asarray(sigma)
     if a.shape != sigma.shape or a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise DimensionMismatch(f"matrix/approximation shapes differ: {a.shape} vs {sigma.shape}")
     target = sigma if sigma.dtype == np.float64 else np.asarray(sigma, dtype=np.float64)
-    _require_symmetric_sigma(target)
     ranges, perm = _single_set(a, target, idx, comp)
+    sym = _is_symmetric(target)
     with DeviceSolver(a, ranges, perm=perm) as ds:
         ds.setup()
-        ds.set_sigma(target)
+        ds.set_sigma(target if sym else target.T)
         ds.block_update(0)
         out = ds.sigma()
-    target[...] = out
+    target[...] = out if sym else out.T
 
 
 def error_estimate(a, sigma, idx, comp, rtol: float = POWER_RTOL, max_iters: int = POWER_MAX_ITERS) -> float:
-    """Spectral norm of ``S_I A_{I,c} + S_{I,c} A_c`` (solver.py:147-155)."""
+    """Spectral norm of ``S_I A_{I,c} + S_{I,c} A_c`` (solver.py:147-155), any float64 Σ."""
     a = np.asarray(a, dtype=np.float64)
     sigma = np.asarray(sigma, dtype=np.float64)
     if a.shape != sigma.shape or a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise DimensionMismatch(f"matrix/approximation shapes differ: {a.shape} vs {sigma.shape}")
-    _require_symmetric_sigma(sigma)
+    # B = Σ[I, :]·A[:, c] reads rows of Σ, so any (also non-symmetric) Σ is used as given
     ranges, perm = _single_set(a, sigma, idx, comp)
     if ranges[0][1] - ranges[0][0] == a.shape[0]:
         raise DimensionMismatch("matrix must be nonempty, got shape (%d, 0)" % a.shape[0])

@@ -6,6 +6,8 @@ Run in the build container only (it imports the read-only reference from
     python tests/golden/make_golden.py pins          # oracle == reference, small cases
     python tests/golden/make_golden.py c1            # full BASELINE c1 solve
     python tests/golden/make_golden.py c2|c3|c4      # long; c4 limited to 3 sweeps
+    python tests/golden/make_golden.py c4long        # c4 through the FP64 floor (30 sweeps, ~1 h)
+    python tests/golden/make_golden.py sketch c2|c3  # full solve again, Σ·R sketches of the result
 
 Every sweep here calls the reference's own ``_BlockOp`` (solver.py:109-129),
 ``error_estimate`` matrix (solver.py:154) and ``_power_sigma_max``
@@ -39,6 +41,15 @@ from paper_2502_06377_b200 import configs  # noqa: E402
 
 SAMPLE_SEED = 12345
 N_SAMPLES = 4096
+SKETCH_SEED = 2025
+SKETCH_COLS = {"c1": 16, "c2": 16, "c3": 16, "c4": 8, "c5": 4}
+
+
+def sketch_matrix(p, cols):
+    """Seeded Gaussian R (p × cols).  ‖(Σ₁ − Σ₂)R‖_F / ‖Σ₁R‖_F estimates the
+    relative Frobenius distance of the full matrices (E‖XR‖²_F = cols·‖X‖²_F)
+    from fixtures small enough to commit."""
+    return np.random.default_rng(SKETCH_SEED).standard_normal((p, cols))
 
 
 def ref_estimate(a, sigma, idx, comp, rtol=rlin.POWER_RTOL, max_iters=rlin.POWER_MAX_ITERS):
@@ -50,7 +61,7 @@ def ref_estimate(a, sigma, idx, comp, rtol=rlin.POWER_RTOL, max_iters=rlin.POWER
     return s, it, conv
 
 
-def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), log=None):
+def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), log=None, snap_fn=None):
     comps = [ibmi.complement(part, j) for j in range(part.k)]
     t0 = time.perf_counter()
     ops = [rsol._BlockOp(a, part.sets[j], comps[j]) for j in range(part.k)]
@@ -64,6 +75,7 @@ def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), 
         raise ValueError(guess)
     rlin.scatter_add_assign(sigma, comps[0], comps[0], g)
     errs, pits, frob, walls, snaps = [], [], [], [], {}
+    snap_fn = snap_fn or (lambda s: s.copy())
     conv, it = False, 0
     while it < max_iterations:
         t = time.perf_counter()
@@ -79,7 +91,7 @@ def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), 
             fr = orc.frobenius_residual(a, sigma)
             frob.append(fr)
         if it in checkpoints:
-            snaps[it] = sigma.copy()
+            snaps[it] = snap_fn(sigma)
         if log:
             print(f"[{log}] sweep {it} err {e:.4e} pit {pi} frob {fr} {walls[-1]:.2f}s", flush=True)
         if (fr < tol) if stopping == "frobenius" else (e <= tol):
@@ -174,6 +186,23 @@ def pins():
     out["an_lemma"] = np.array([ran.lemma_error_recurrence_check(a, i1, i2, g0, 3)])
     fc = ran.flop_cost(1000, 4, 0.1)
     out["an_flop"] = np.array([fc.m, fc.h, float(fc.total_flops), float(fc.direct_flops)])
+    # block_update / error_estimate on a NON-symmetric Σ (solver.py:132-155 accept any float64 Σ)
+    r2 = np.random.default_rng(11)
+    a = out["case2_a"]                     # p = 128
+    part = ibmi.contiguous_partition(128, 4, 0.125)
+    idx, comp = part.sets[1], ibmi.complement(part, 1)
+    sig = np.eye(128) + 0.05 * r2.standard_normal((128, 128))
+    out["nonsym_sigma0"] = sig.copy()
+    ibmi.block_update(a, sig, idx, comp)
+    out["nonsym_bu"] = sig
+    out["nonsym_ee"] = np.array([ibmi.error_estimate(a, out["nonsym_sigma0"], idx, comp)])
+    # linalg seam: cholesky / chol_solve (linalg.py:96-119)
+    spd = out["case1_a"]
+    f = rlin.cholesky(spd)
+    out["chol_l"] = f.l
+    rhs = r2.standard_normal((96, 5))
+    out["chol_rhs"] = rhs
+    out["chol_x"] = rlin.chol_solve(f, rhs)
     np.savez_compressed(os.path.join(HERE, "pins.npz"), **out)
     print("pins OK:", len(cases), "cases")
 
@@ -234,9 +263,81 @@ def run_config(name):
     print(name, "done:", meta)
 
 
+def _snapshot(a, sigma, r, si, sj, frob=False):
+    d = dict(sketch=sigma @ r, sample=sigma[si, sj], rowsum=sigma.sum(axis=1),
+             fro=np.array([np.linalg.norm(sigma)]),
+             asym=np.array([float(np.max(np.abs(sigma - sigma.T)))]))
+    if frob:
+        d["frobenius"] = np.array([orc.frobenius_residual(a, sigma)])
+    return d
+
+
+def run_c4_long(max_it=30, checkpoints=(3, 10, 18, 25, 30)):
+    """c4 with the reference's own tol 1e-8 (solver.py:73), run past the sweep
+    where the GPU paths stall (~22) to show whether the reference's FP64 run
+    stalls at the same floor.  Freezes the error trace, power-iteration counts
+    and Σ snapshots (sketch Σ·R, sampled entries, row sums, ‖Σ‖_F,
+    ‖I − AΣ‖_F) at ``checkpoints``."""
+    cfg = configs.get_config("c4")
+    a = configs.make_matrix("c4", 0)
+    part = cfg.partition()
+    r = sketch_matrix(cfg.p, SKETCH_COLS["c4"])
+    si, sj = sample_index(cfg.p)
+    rep = ref_solve(a, part, tol=1e-8, max_iterations=max_it, guess="identity", stopping="estimate",
+                    checkpoints=checkpoints, log="c4long",
+                    snap_fn=lambda s: _snapshot(a, s, r, si, sj, frob=True))
+    out = dict(error_trace=np.array(rep["error_trace"]), power_iters=np.array(rep["power_iters"]),
+               wall_times=np.array(rep["wall_times"]),
+               iterations=np.array([rep["iterations"], int(rep["converged"])]),
+               sample_i=si, sample_j=sj, checkpoints=np.array(sorted(rep["snaps"])))
+    for it, d in rep["snaps"].items():
+        for key, val in d.items():
+            out[f"snap{it}_{key}"] = val
+    meta = {"config": "c4", "reference_tol": 1e-8, "max_iterations": max_it,
+            "iterations": rep["iterations"], "converged": rep["converged"],
+            "error_trace": rep["error_trace"], "power_iters": rep["power_iters"],
+            "frobenius_at": {str(k): float(v["frobenius"][0]) for k, v in rep["snaps"].items()},
+            "setup_seconds": rep["setup_seconds"], "mean_sweep_seconds": float(np.mean(rep["wall_times"])),
+            "sketch_cols": SKETCH_COLS["c4"], "sketch_seed": SKETCH_SEED,
+            "host_threads": os.cpu_count(), "numpy": np.__version__}
+    np.savez_compressed(os.path.join(HERE, "c4long.npz"), **out)
+    with open(os.path.join(HERE, "c4long.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print("c4long done:", meta)
+
+
+def run_sketch(name):
+    """Full reference solve of c1/c2/c3 again, freezing Σ·R of the result (and
+    of the first sweeps) so the GPU test measures a relative-Frobenius distance
+    over the whole Σ, not only sampled entries.  The error trace is asserted
+    equal to the committed fixture (same BLAS, same thread count)."""
+    cfg = configs.get_config(name)
+    a = configs.make_matrix(name, 0)
+    part = cfg.partition()
+    r = sketch_matrix(cfg.p, SKETCH_COLS[name])
+    si, sj = sample_index(cfg.p)
+    rep = ref_solve(a, part, tol=cfg.tol, max_iterations=cfg.max_iterations, guess=cfg.guess,
+                    stopping=cfg.stopping, checkpoints=(1, 5), log=f"{name}-sketch",
+                    snap_fn=lambda s: _snapshot(a, s, r, si, sj))
+    old = np.load(os.path.join(HERE, f"{name}.npz"))
+    same = np.array_equal(np.array(rep["error_trace"]), old["error_trace"])
+    out = dict(error_trace=np.array(rep["error_trace"]),
+               iterations=np.array([rep["iterations"], int(rep["converged"])]),
+               **{f"final_{k}": v for k, v in _snapshot(a, rep["sigma"], r, si, sj).items()})
+    for it, d in rep["snaps"].items():
+        for key, val in d.items():
+            out[f"snap{it}_{key}"] = val
+    np.savez_compressed(os.path.join(HERE, f"{name}_sketch.npz"), **out)
+    print(name, "sketch done; trace identical to committed fixture:", same, "iterations", rep["iterations"])
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "pins":
         pins()
+    elif what == "c4long":
+        run_c4_long()
+    elif what == "sketch":
+        run_sketch(sys.argv[2])
     else:
         run_config(what)

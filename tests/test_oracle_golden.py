@@ -72,3 +72,16 @@ def test_flop_cost_matches_reference():
     pins = golden("pins.npz")
     fc = flop_cost(1000, 4, 0.1)
     assert [fc.m, fc.h, float(fc.total_flops), float(fc.direct_flops)] == pins["an_flop"].tolist()
+
+
+def test_oracle_nonsymmetric_sigma_against_reference():
+    """block_update / error_estimate accept any float64 Σ (solver.py:132-155)."""
+    pins = golden("pins.npz")
+    a = pins["case2_a"]
+    part = contiguous_partition(128, 4, 0.125)
+    idx, comp = part.sets[1], orc.complement(128, part.sets[1])
+    s = pins["nonsym_sigma0"].copy()
+    assert not np.array_equal(s, s.T)
+    assert orc.error_estimate(a, s, idx, comp)[0] == pins["nonsym_ee"][0]
+    orc.BlockOp(a, idx, comp).apply(s)
+    assert np.array_equal(s, pins["nonsym_bu"])
