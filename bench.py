@@ -16,7 +16,15 @@ the SM clocks sampled during the timed region.
 
 ``--impl reference`` times the CPU oracle port (oracle/ibmi_oracle.py, the
 reference algorithm on NumPy/SciPy OpenBLAS, all host threads) on the same
-config, each step one block update (sets cycled), and reports the same metric.
+config: each timed step is one FULL sweep in the reference's order (K block
+updates + the error estimate, solver.py:257-266), from the reference's Σ₀;
+warm-up steps are single block updates (then Σ is reset), and the timed sweeps
+stop early, with ``steps`` reporting the sweeps actually run, if the next one
+would pass ``--ref-budget-s``.
+
+``--gpus N`` without torchrun re-launches this script under
+``torch.distributed.run`` with N ranks when the node has N GPUs, and exits
+non-zero when it has fewer: a multi-GPU line is never measured on one GPU.
 """
 
 from __future__ import annotations
@@ -54,7 +62,46 @@ def parse():
                     help="headline GEMM path: FP64 DMMA (default) or Ozaki-II INT8 emulation")
     ap.add_argument("--moduli", type=int, default=16, help="Ozaki-II moduli (8..20)")
     ap.add_argument("--no-alt", action="store_true", help="skip measuring the other GEMM path")
+    ap.add_argument("--ref-budget-s", type=float, default=1500.0,
+                    help="reference arm: stop the timed sweeps before this many seconds")
     return ap.parse_args()
+
+
+def bench_config(cfg, part) -> dict:
+    """The workload description both arms print (so the driver sees the same config)."""
+    sizes = [len(s) for s in part.sets]
+    mat = cfg.p * cfg.p * 8
+    l2 = ("inputs (A, Sigma: %.2f GB each) exceed the 126 MB L2; no flush" % (mat / 1e9) if mat > 126e6 else
+          "inputs (A, Sigma: %.0f MB each) fit in L2; not flushed (every sweep rewrites all of Sigma)" % (mat / 1e6))
+    return {"workload": f"{cfg.name}: {cfg.description}", "p": cfg.p, "sets": part.k, "overlap": cfg.overlap,
+            "set_sizes": sorted(set(sizes)), "l2": l2}
+
+
+def host_info() -> dict:
+    """CPU model and the BLAS/LAPACK builds NumPy and SciPy run on."""
+    import platform
+
+    import scipy
+    import scipy.linalg  # noqa: F401  (loads SciPy's OpenBLAS)
+
+    model = platform.processor()
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), model)
+    except OSError:
+        pass
+    blas = []
+    try:
+        from threadpoolctl import threadpool_info
+
+        for d in threadpool_info():
+            blas.append({"api": d.get("internal_api"), "version": d.get("version"),
+                         "threads": d.get("num_threads"), "arch": d.get("architecture"),
+                         "lib": os.path.basename(d.get("filepath") or "")})
+    except Exception as exc:  # noqa: BLE001 - informational only
+        blas.append({"error": repr(exc)})
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "numpy": np.__version__, "scipy": scipy.__version__,
+            "blas": blas}
 
 
 def dist_env():
@@ -62,20 +109,38 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+    """SM clocks + throttle reasons sampled while running: NVML every 20 ms
+    (so even a sub-second timed region gets samples), else nvidia-smi -lms 200."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h)
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []          # (sm_mhz, max_mhz, reasons)
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index())
+            self._sample_nvml()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:           # noqa: BLE001 - no NVML: nvidia-smi
+            self._nv = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self._physical_index()), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -84,11 +149,45 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _physical_index(self) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[self.index])
+            except (ValueError, IndexError):
+                pass
+        return self.index
+
+    def _sample_nvml(self):
+        nv = self._nv
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:           # noqa: BLE001 - older binding name
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.samples.append((float(sm), float(mx), {n for n, b in self.BITS.items() if bits & b}))
+
+    def _nvml_loop(self):
+        while not self._stop.wait(0.02):
+            try:
+                self._sample_nvml()
+            except Exception:       # noqa: BLE001
+                return
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            try:
+                self._sample_nvml()
+            except Exception:       # noqa: BLE001
+                pass
+            if self.t:
+                self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -98,6 +197,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
+        for a, b, r in self.samples:
+            sm.append(a)
+            mx.append(b)
+            reasons |= r
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -114,7 +217,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml 20 ms" if self.samples else "nvidia-smi 200 ms"}
 
 
 def cpu_sample(cfg, a, n_blocks=1):
@@ -154,6 +257,9 @@ def cpu_sample(cfg, a, n_blocks=1):
 
 
 def run_reference(args):
+    """The reference's CPU path (oracle port, bit-identical to the reference on
+    the pinned cases) timed in whole sweeps: solver.py:257-266 order, K block
+    updates then the error estimate on the last set, from the reference Σ₀."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -161,43 +267,63 @@ def run_reference(args):
     from paper_2502_06377_b200 import configs
 
     cfg = configs.get_config(args.config)
+    if args.config == "c5":
+        print(json.dumps({"impl": "reference", "unavailable": "c5's reference sweep needs ~140 GB of host RAM and "
+                          "~21 min per sweep; run tools/c5_oracle_check.py instead"}), file=_JSON_OUT, flush=True)
+        return
     a = configs.make_matrix(args.config)
     part = cfg.partition()
     p = cfg.p
     comps = [orc.complement(p, s) for s in part.sets]
-    ops = {}
-    sigma = np.eye(p)
-    step_t = []
-    for step in range(args.warmup + args.steps):
-        k = step % part.k
-        if k not in ops:
-            ops[k] = orc.BlockOp(a, part.sets[k], comps[k])
-        t0 = time.perf_counter()
-        ops[k].apply(sigma)
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            step_t.append((k, dt))
     t0 = time.perf_counter()
-    orc.error_estimate(a, sigma, part.sets[-1], comps[-1])
-    t_err = time.perf_counter() - t0
-    per_flop = []
-    for k, dt in step_t:
-        b = len(part.sets[k])
-        per_flop.append(dt / (2.0 * b * (p - b) ** 2 + 2.0 * b * b * (p - b)))
-    pf = statistics.median(per_flop)
-    t_sweep = sum(pf * (2.0 * len(s) * (p - len(s)) ** 2 + 2.0 * len(s) ** 2 * (p - len(s))) for s in part.sets) + t_err
-    value = 1.0 / t_sweep
-    sample = (f"{args.steps} timed block updates (sets cycled, {args.warmup} warm-up) + 1 error estimate; "
-              f"sweep time = FLOP-weighted block time x {part.k} sets + estimate")
+    ops = [orc.BlockOp(a, part.sets[k], comps[k]) for k in range(part.k)]
+    setup_s = time.perf_counter() - t0
+
+    def sigma0():
+        sig = np.eye(p)
+        if cfg.guess == "jacobi":
+            c0 = comps[0]
+            sig[c0, c0] = 1.0 / np.diag(a)[c0]
+        return sig
+
+    sigma = sigma0()
+    t_warm = time.perf_counter()
+    for step in range(args.warmup):          # warm-up: single block updates (BLAS threads, page-in)
+        ops[step % part.k].apply(sigma)
+    warm_s = time.perf_counter() - t_warm
+    sigma = sigma0()
+    sweep_t, errs, pits = [], [], []
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        for op in ops:
+            op.apply(sigma)
+        e, it, _ = orc.error_estimate(a, sigma, part.sets[-1], comps[-1])
+        sweep_t.append(time.perf_counter() - t1)
+        errs.append(e)
+        pits.append(it)
+        elapsed = time.perf_counter() - t_start
+        if elapsed + max(sweep_t) > args.ref_budget_s and len(sweep_t) < args.steps:
+            break
+    n = len(sweep_t)
+    total = sum(sweep_t)
+    value = n / total
+    info = host_info()
+    sample = (f"{n} full sweeps timed (each: {part.k} block updates + the error estimate on set {part.k - 1}, "
+              f"solver.py:257-266 order, from the reference Sigma0)"
+              + (f"; capped at {n} of {args.steps} by --ref-budget-s {args.ref_budget_s:.0f}" if n < args.steps else "")
+              + f"; {args.warmup} warm-up steps = single block updates ({warm_s:.1f} s), then Sigma reset")
     line = {
-        "impl": "reference", "metric": "IBMI sweeps/s (FP64) at p=16384" if args.config == "c4" else f"IBMI sweeps/s ({args.config})",
-        "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_sweep * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg.description}", "p": p, "sets": part.k, "overlap": cfg.overlap},
+        "impl": "reference",
+        "metric": "IBMI sweeps/s (FP64) at p=16384" if args.config == "c4" else f"IBMI sweeps/s ({args.config})",
+        "value": value, "unit": "sweeps/s", "n_gpus": world if world > 1 else args.gpus, "steps": n,
+        "warmup": args.warmup, "ms_per_step": total / n * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(cfg, part),
         "tflops": configs.sweep_flops(cfg) * value / 1e12,
+        "sweep_seconds": sweep_t, "error_trace": errs, "power_iterations": pits, "setup_s": setup_s,
         "cpu_baseline": {"value": value, "unit": "sweeps/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **info},
         "e2e": {"value": value, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=_JSON_OUT, flush=True)
@@ -490,7 +616,7 @@ def run_ours(args):
     if not args.no_cpu_baseline and rank == 0 and world == 1 and a_host is not None:
         s = cpu_sample(cfg, a_host)
         cpu = {"value": 1.0 / s["sweep_s"], "unit": "sweeps/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": s["sample"], "setup_one_set_s": s["setup_one_set_s"]}
+               "sample": s["sample"], "setup_one_set_s": s["setup_one_set_s"], **host_info()}
 
     def roofline(mode, kt_, igemm_):
         if kt_ is None:
@@ -533,11 +659,9 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64" if mode == "dmma" else f"f64 via int8 (Ozaki-II, {args.moduli} moduli)",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg.description}", "p": p, "sets": part.k,
-                       "overlap": cfg.overlap, "set_sizes": sorted(set(sizes)),
-                       "l2": "inputs (A, Sigma) exceed L2; no flush",
-                       "parallelism": f"row-panel sharded x{world}" if world > 1 else "single",
-                       "gemm": mode},
+            "config": bench_config(cfg, part),
+            "parallelism": f"row-panel sharded x{world}" if world > 1 else "single",
+            "gemm": mode,
             "tflops": tf,
             "tflops_frac_of_peak": tf / world / peak,
             "tflops_executed": executed_flops(cfg) * sweeps_s / 1e12,
@@ -576,6 +700,27 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def relaunch(args) -> int:
+    """``--gpus N`` outside torchrun: run N ranks under torch.distributed.run on
+    this node, or fail (exit 3) when it has fewer than N GPUs."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs on this node, found {have}; "
+              "not running (a multi-GPU number is never measured on fewer GPUs)", file=sys.stderr)
+        return 3
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, stdout=_JSON_OUT.fileno(), stderr=2).returncode
+
+
 if __name__ == "__main__":
     # The driver reads rank 0's stdout as exactly one JSON line, but NCCL (and
     # anything else in the process) may write to fd 1 -- e.g. "NCCL version ..."
@@ -584,7 +729,14 @@ if __name__ == "__main__":
     _JSON_OUT = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
     a = parse()
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None and int(ws) != a.gpus:
+        print(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={ws}; launch with torchrun --nproc-per-node {a.gpus}",
+              file=sys.stderr)
+        sys.exit(2)
     if a.impl == "reference":
         run_reference(a)
+    elif ws is None and a.gpus > 1:
+        sys.exit(relaunch(a))
     else:
         run_ours(a)

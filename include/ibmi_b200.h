@@ -251,7 +251,7 @@ typedef struct {
   double* c; int64_t ldc; ibmi_map cm, cn; const int64_t* cidx; int direct;
   double* c2; int64_t ldc2; ibmi_map c2m, c2n; int mirror;
   double alpha, beta; const double* d; int64_t ldd; ibmi_map dm, dn;
-  int lower, tma_safe, splits;
+  int lower, tma_safe, splits;   /* splits: split-K factor, <= 0 = automatic (wave model) */
   double* frob_out;
   double* ws; int64_t ws_len;
   /* fused exchange (sharded sweep): when peers != NULL every element (m, n) is
@@ -267,6 +267,10 @@ typedef struct {
 
 int ibmi_gemm(const ibmi_gemm_desc* desc, void* stream);
 int ibmi_gemm_workspace(const ibmi_gemm_desc* desc, int64_t* doubles);
+
+/* The CUDA stream the context's work is ordered on (its own non-blocking
+ * stream, or the one passed to ibmi_create). */
+int ibmi_context_stream(ibmi_ctx* ctx, void** stream);
 
 /* Device pointer, shape and leading dimension of a context buffer:
  * which = 0 A, 1 Σ, 2 W_k (b_k × ld, global columns), 3 A_II⁻¹ of set k. */

@@ -67,6 +67,7 @@ SIGNATURES = [
                                 C.POINTER(C.c_int), _P]),
     ("ibmi_gemm", C.c_int, [_P, _P]),
     ("ibmi_gemm_workspace", C.c_int, [_P, C.POINTER(_I64)]),
+    ("ibmi_context_stream", C.c_int, [_P, C.POINTER(_P)]),
     ("ibmi_export", C.c_int, [_P, C.c_int, C.c_int, C.POINTER(_P), C.POINTER(_I64), C.POINTER(_I64),
                               C.POINTER(_I64)]),
     ("ibmi_device_alloc", C.c_int, [C.c_int, _I64, C.POINTER(_P)]),

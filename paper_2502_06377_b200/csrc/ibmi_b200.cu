@@ -3139,8 +3139,8 @@ int ibmi_scatter(double* target, int64_t ldt, const int64_t* rows, int64_t nr, c
 // sharded sweep calls it once per sweep; no cudaMalloc on that path).
 struct NormCache {
   std::mutex mu;
-  double *G = nullptr, *vec = nullptr, *part = nullptr, *out = nullptr, *vr = nullptr;
-  int64_t g_cap = 0, vec_cap = 0, vr_cap = 0;
+  double *G = nullptr, *vec = nullptr, *part = nullptr, *out = nullptr, *vr = nullptr, *ws = nullptr;
+  int64_t g_cap = 0, vec_cap = 0, vr_cap = 0, ws_cap = 0;
   int blocks = 0, threads = 0;
   size_t smem_cap = 0;
   double* host = nullptr;
@@ -3170,7 +3170,18 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
   if (ensure_buf(&nc.vec, &nc.vec_cap, 2 * std::max(rows, cols), &dummy)) return IBMI_ERR_OOM;
   if (ensure_buf(&nc.vr, &nc.vr_cap, cols, &dummy)) return IBMI_ERR_OOM;
   CUDA_TRY(cudaMemcpyAsync(nc.vr, restart_v, (size_t)cols * sizeof(double), cudaMemcpyHostToDevice, st));
-  NormBufs nb{nc.G, ldG, nc.vec, nc.part, nc.out, nc.vr, nc.blocks, nc.threads, nc.smem_cap, nullptr, 0, 148};
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (rows <= cols) {   // split-K workspace of the Gram GEMM G = B Bᵀ (same plan as enqueue_two_norm)
+    GemmOp gg;
+    gg.M = n; gg.N = n; gg.lower = true;
+    gg.add_seg(0, 0, cols);
+    const int bk = g_variant == 2 ? 32 : 16;
+    const int sp = g_split_gram > 0 ? g_split_gram : auto_split(gemm_tiles(gg), (int)((cols + bk - 1) / bk), sms);
+    if (sp > 1 && ensure_buf(&nc.ws, &nc.ws_cap, (int64_t)gemm_tiles(gg) * sp * GB_M * GB_N, &dummy))
+      return IBMI_ERR_OOM;
+  }
+  NormBufs nb{nc.G, ldG, nc.vec, nc.part, nc.out, nc.vr, nc.blocks, nc.threads, nc.smem_cap, nc.ws, nc.ws_cap, sms};
   int rc = enqueue_two_norm(b, ldb, rows, cols, rtol, max_iters, nb, st);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(nc.host, nc.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -3215,17 +3226,36 @@ static int desc_to_op(const ibmi_gemm_desc* d, GemmOp& op) {
   op.lower = d->lower != 0;
   op.tma_ok = d->tma_safe != 0;
   op.xrows = d->xrows; op.xcols = d->xcols; op.yrows = d->yrows; op.ycols = d->ycols;
-  op.splits = d->splits > 1 ? d->splits : 1;
   op.xt = d->xt != 0;
   op.yt = d->yt != 0;
   if ((op.xt && (op.xm.idx || op.xm.split != INT_MAX)) || (op.yt && (op.yn.idx || op.yn.split != INT_MAX)))
     return fail(IBMI_ERR_INVALID, "transposed operands take contiguous maps only");
-  if (op.xt || op.yt) { op.tma_ok = false; op.splits = 1; }
   if (d->peers) {
     if (d->bc_panel < 1 || d->bc_world < 1 || d->bc_rank < 0 || d->bc_rank >= d->bc_world || op.cidx)
       return fail(IBMI_ERR_INVALID, "bad peer-store layout");
     op.peers = d->peers; op.bc_panel = d->bc_panel; op.bc_world = d->bc_world; op.bc_rank = d->bc_rank;
+  }
+  // split-K: explicit factor, or (splits <= 0) the same wave model as the
+  // context's own GEMMs; the fixed-order reduction kernel also runs the
+  // mirrored and peer-store epilogues.  Not for transposed operands or the
+  // Frobenius epilogue.
+  if (op.xt || op.yt) op.tma_ok = false;
+  if (op.xt || op.yt || d->frob_out) {
     op.splits = 1;
+  } else if (d->splits > 0) {
+    op.splits = d->splits;
+  } else {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    static int sm_of[64] = {0};
+    if (dev >= 0 && dev < 64) {
+      if (!sm_of[dev]) cudaDeviceGetAttribute(&sm_of[dev], cudaDevAttrMultiProcessorCount, dev);
+      sms = sm_of[dev] > 0 ? sm_of[dev] : 148;
+    }
+    int64_t klen = 0;
+    for (int i = 0; i < op.nseg; ++i) klen += op.seg[i].len;
+    const int bk = g_variant == 2 ? 32 : 16;
+    op.splits = auto_split(gemm_tiles(op), (int)((klen + bk - 1) / bk), sms);
   }
   return IBMI_OK;
 }
@@ -3276,6 +3306,12 @@ int ibmi_export(ibmi_ctx* c, int which, int k, double** ptr, int64_t* rows, int6
   if (which == 2) { *ptr = s.W; if (rows) *rows = s.b; if (cols) *cols = c->p; if (ld) *ld = c->ld; return IBMI_OK; }
   if (which == 3) { *ptr = s.ainv; if (rows) *rows = s.b; if (cols) *cols = s.b; if (ld) *ld = s.ldb; return IBMI_OK; }
   return fail(IBMI_ERR_INVALID, "unknown buffer");
+}
+
+int ibmi_context_stream(ibmi_ctx* c, void** stream) {
+  if (!c || !stream) return fail(IBMI_ERR_INVALID, "null argument");
+  *stream = (void*)c->stream;
+  return IBMI_OK;
 }
 
 int ibmi_release_cached_memory(int device) {

@@ -164,6 +164,12 @@ class DeviceSolver:
         except Exception:
             pass
 
+    def stream_handle(self) -> int:
+        """The context's CUDA stream (``cudaStream_t`` as an int)."""
+        st = C.c_void_p()
+        _abi.check(self._L.ibmi_context_stream(self._h, C.byref(st)), "context_stream")
+        return st.value or 0
+
     # -- pieces
     def _set_restart(self, n: int):
         if n >= 1 and n != self._restart_n:

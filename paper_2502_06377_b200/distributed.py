@@ -190,7 +190,7 @@ class CudaBackend:
         if s.d is not None:
             d.d, d.ldd = s.d.data_ptr(), s.d.stride(0)
             d.dm, d.dn = _cmap(s.dm), _cmap(s.dn)
-        d.lower, d.tma_safe, d.splits = int(s.lower), int(s.tma_safe), 1
+        d.lower, d.tma_safe, d.splits = int(s.lower), int(s.tma_safe), 0     # 0: automatic split-K
         d.xt = int(s.xt)
         if s.peers is not None:
             d.peers, d.bc_panel, d.bc_world, d.bc_rank = s.peers.data_ptr(), s.bc_panel, s.bc_world, s.bc_rank

@@ -334,6 +334,48 @@ def _is_symmetric(sigma: np.ndarray) -> bool:
     return sigma.size == 0 or bool(np.array_equal(sigma, sigma.T))
 
 
+def _export(ds: DeviceSolver, which: int, k: int = 0):
+    import ctypes as C
+
+    ptr, r, c, ld = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+    _abi.check(_abi.lib().ibmi_export(ds._h, which, k, C.byref(ptr), C.byref(r), C.byref(c), C.byref(ld)), "export")
+    return ptr.value, ld.value
+
+
+def _diag_block_nonsymmetric(ds: DeviceSolver) -> None:
+    """Σ_II = A_II⁻¹ + ½(M Wᵀ + W Mᵀ) after K1 has stored Σ[I, c] = −M.
+
+    solver.py:125-127 symmetrises ``ainv + M Wᵀ``; with a symmetric Σ the
+    library's K2 takes the lower triangle of ``M Wᵀ`` (symmetric up to
+    rounding), but with a non-symmetric Σ_cc that product is not symmetric,
+    so the average is formed by two GEMMs on the device:
+    ``Σ_II = ainv + ½·M Wᵀ`` then ``Σ_II += ½·W Mᵀ``."""
+    import ctypes as C
+
+    lo, hi = ds.ranges[0]
+    p, b = ds.p, hi - lo
+    s_ptr, lds = _export(ds, 1)
+    w_ptr, ldw = _export(ds, 2, 0)
+    ai_ptr, ldai = _export(ds, 3, 0)
+    run = _abi.Map.run
+    for x, ldx, xm, y, ldy, yn, d, ldd, dm in (
+            (s_ptr, lds, run(lo), w_ptr, ldw, run(0), ai_ptr, ldai, run(0)),     # ainv − ½(−M)Wᵀ
+            (w_ptr, ldw, run(0), s_ptr, lds, run(lo), s_ptr, lds, run(lo))):     # + (−½)·W(−M)ᵀ
+        g = _abi.GemmDesc()
+        g.x, g.ldx, g.xm, g.xrows, g.xcols = x, ldx, xm, 0, 0
+        g.y, g.ldy, g.yn, g.yrows, g.ycols = y, ldy, yn, 0, 0
+        g.m, g.n = b, b
+        segs = [(0, 0, lo), (hi, hi, p - hi)]
+        segs = [sg for sg in segs if sg[2] > 0]
+        g.nseg = len(segs)
+        for i, (x0, y0, ln) in enumerate(segs):
+            g.seg_x0[i], g.seg_y0[i], g.seg_len[i] = x0, y0, ln
+        g.c, g.ldc, g.cm, g.cn, g.direct = s_ptr, lds, run(lo), run(lo), 1
+        g.alpha, g.beta, g.d, g.ldd, g.dm, g.dn = -0.5, 1.0, d, ldd, dm, run(0) if d == ai_ptr else run(lo)
+        g.splits = 1
+        _abi.check(_abi.lib().ibmi_gemm(C.byref(g), C.c_void_p(ds.stream_handle())), "gemm")
+
+
 def block_update(a, sigma, idx, comp) -> None:
     """Apply one block-inverse update to ``sigma`` in place (solver.py:132-144).
 
@@ -341,9 +383,9 @@ def block_update(a, sigma, idx, comp) -> None:
     any other input is converted and the result is discarded.  ``sigma`` need
     not be symmetric: the kernels read Σ[c, c] through rows of the device
     copy, so a non-symmetric Σ is uploaded as Σᵀ.  The update writes only
-    mirrored pairs (Σ_II symmetrised, Σ_Ic = −M, Σ_cI = −Mᵀ), which are the
-    same in Σ and Σᵀ, and leaves Σ[c, c] untouched, so transposing back gives
-    exactly the reference's result.
+    mirrored pairs (Σ_Ic = −M, Σ_cI = −Mᵀ, a symmetric Σ_II) and leaves
+    Σ[c, c] untouched, so transposing back gives the reference's result; Σ_II
+    is then the average ``ainv + ½(M Wᵀ + W Mᵀ)`` (:func:`_diag_block_nonsymmetric`).
     """
     a = np.asarray(a, dtype=np.float64)
     sigma = np.asarray(sigma)
@@ -356,6 +398,8 @@ def block_update(a, sigma, idx, comp) -> None:
         ds.setup()
         ds.set_sigma(target if sym else target.T)
         ds.block_update(0)
+        if not sym:
+            _diag_block_nonsymmetric(ds)
         out = ds.sigma()
     target[...] = out if sym else out.T
 

@@ -9,6 +9,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 from conftest import ROOT
@@ -34,6 +35,35 @@ def test_reference_arm_line_on_cpu():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["e2e"]["d2h_bytes_per_step"] == 0
+    # each step is one whole sweep, timed: the claimed time fits the sweeps reported
+    assert d["steps"] == 2 and len(d["sweep_seconds"]) == 2
+    assert abs(d["ms_per_step"] - 1e3 * sum(d["sweep_seconds"]) / 2) < 1e-6 * d["ms_per_step"]
+    assert abs(d["value"] - 2 / sum(d["sweep_seconds"])) < 1e-9 * d["value"]
+    # the same error trace as the reference's first two c1 sweeps (golden fixture)
+    from conftest import golden
+
+    np.testing.assert_array_equal(d["error_trace"], golden("c1.npz")["error_trace"][:2])
+    assert "cpu_model" in cb and "blas" in cb
+    assert set(d["config"]) == {"workload", "p", "sets", "overlap", "set_sizes", "l2"}
+
+
+def test_reference_arm_budget_caps_sweeps():
+    d = _run(["--impl", "reference", "--config", "c1", "--steps", "50", "--warmup", "0", "--ref-budget-s", "0"],
+             timeout=600)
+    assert d["steps"] == 1 and len(d["sweep_seconds"]) == 1 and "capped" in d["cpu_baseline"]["sample"]
+
+
+def test_gpus_flag_never_measures_on_fewer_gpus():
+    """--gpus N outside torchrun either launches N ranks or exits non-zero; a
+    WORLD_SIZE that disagrees with --gpus is an error."""
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert res.returncode == 3 and res.stdout.strip() == "", (res.returncode, res.stdout[-500:])
+    assert "needs 64 GPUs" in res.stderr
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert res.returncode == 2 and res.stdout.strip() == ""
 
 
 @pytest.mark.gpu
