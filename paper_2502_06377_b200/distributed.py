@@ -435,8 +435,18 @@ class ShardedSolver:
         """Σ = I, Σ[c₁,c₁] = identity or diag(1/A_ii) (solver.py:244-251 + BASELINE jacobi)."""
         torch = self.torch
         self.S.zero_()
-        if self.n_loc == 0:
-            return
+        if self.n_loc:
+            self._seed_sigma(guess)
+        elif guess not in ("identity", "jacobi"):
+            raise NotImplementedError(f"guess {guess!r} on the sharded path")
+        # No rank may start its first panel GEMM before every panel is seeded: in the
+        # p2p exchange K1's epilogue stores −M into the OWNERS' panels, and a late
+        # zero_() on a slow rank would wipe those stores.
+        if self.world > 1:
+            self.comm.barrier()
+
+    def _seed_sigma(self, guess):
+        torch = self.torch
         loc = torch.arange(self.n_loc, device=self.S.device)
         vals = torch.ones(self.n_loc, dtype=torch.float64, device=self.S.device)
         if guess == "jacobi":

@@ -61,7 +61,8 @@ def ref_estimate(a, sigma, idx, comp, rtol=rlin.POWER_RTOL, max_iters=rlin.POWER
     return s, it, conv
 
 
-def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), log=None, snap_fn=None):
+def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), log=None, snap_fn=None,
+              progress_fn=None):
     comps = [ibmi.complement(part, j) for j in range(part.k)]
     t0 = time.perf_counter()
     ops = [rsol._BlockOp(a, part.sets[j], comps[j]) for j in range(part.k)]
@@ -92,6 +93,9 @@ def ref_solve(a, part, *, tol, max_iterations, guess, stopping, checkpoints=(), 
             frob.append(fr)
         if it in checkpoints:
             snaps[it] = snap_fn(sigma)
+            if progress_fn:
+                progress_fn(dict(iterations=it, converged=False, error_trace=errs, power_iters=pits,
+                                 wall_times=walls, setup_seconds=setup, snaps=snaps))
         if log:
             print(f"[{log}] sweep {it} err {e:.4e} pit {pi} frob {fr} {walls[-1]:.2f}s", flush=True)
         if (fr < tol) if stopping == "frobenius" else (e <= tol):
@@ -272,7 +276,7 @@ def _snapshot(a, sigma, r, si, sj, frob=False):
     return d
 
 
-def run_c4_long(max_it=30, checkpoints=(3, 10, 18, 25, 30)):
+def run_c4_long(max_it=30, checkpoints=(3, 6, 10, 14, 18, 20, 22, 24, 25, 26, 28, 30)):
     """c4 with the reference's own tol 1e-8 (solver.py:73), run past the sweep
     where the GPU paths stall (~22) to show whether the reference's FP64 run
     stalls at the same floor.  Freezes the error trace, power-iteration counts
@@ -283,27 +287,32 @@ def run_c4_long(max_it=30, checkpoints=(3, 10, 18, 25, 30)):
     part = cfg.partition()
     r = sketch_matrix(cfg.p, SKETCH_COLS["c4"])
     si, sj = sample_index(cfg.p)
+    def save(rep):
+        # written at every checkpoint so an interrupted run still leaves a usable fixture
+        out = dict(error_trace=np.array(rep["error_trace"]), power_iters=np.array(rep["power_iters"]),
+                   wall_times=np.array(rep["wall_times"]),
+                   iterations=np.array([rep["iterations"], int(rep["converged"])]),
+                   sample_i=si, sample_j=sj, checkpoints=np.array(sorted(rep["snaps"])))
+        for it, d in rep["snaps"].items():
+            for key, val in d.items():
+                out[f"snap{it}_{key}"] = val
+        meta = {"config": "c4", "reference_tol": 1e-8, "max_iterations": max_it,
+                "iterations": rep["iterations"], "converged": rep["converged"],
+                "error_trace": list(rep["error_trace"]), "power_iters": list(rep["power_iters"]),
+                "frobenius_at": {str(k): float(v["frobenius"][0]) for k, v in rep["snaps"].items()},
+                "setup_seconds": rep["setup_seconds"],
+                "mean_sweep_seconds": float(np.mean(rep["wall_times"])),
+                "sketch_cols": SKETCH_COLS["c4"], "sketch_seed": SKETCH_SEED,
+                "host_threads": os.cpu_count(), "numpy": np.__version__}
+        np.savez_compressed(os.path.join(HERE, "c4long.npz"), **out)
+        with open(os.path.join(HERE, "c4long.json"), "w") as fh:
+            json.dump(meta, fh, indent=1)
+        return meta
+
     rep = ref_solve(a, part, tol=1e-8, max_iterations=max_it, guess="identity", stopping="estimate",
-                    checkpoints=checkpoints, log="c4long",
+                    checkpoints=checkpoints, log="c4long", progress_fn=save,
                     snap_fn=lambda s: _snapshot(a, s, r, si, sj, frob=True))
-    out = dict(error_trace=np.array(rep["error_trace"]), power_iters=np.array(rep["power_iters"]),
-               wall_times=np.array(rep["wall_times"]),
-               iterations=np.array([rep["iterations"], int(rep["converged"])]),
-               sample_i=si, sample_j=sj, checkpoints=np.array(sorted(rep["snaps"])))
-    for it, d in rep["snaps"].items():
-        for key, val in d.items():
-            out[f"snap{it}_{key}"] = val
-    meta = {"config": "c4", "reference_tol": 1e-8, "max_iterations": max_it,
-            "iterations": rep["iterations"], "converged": rep["converged"],
-            "error_trace": rep["error_trace"], "power_iters": rep["power_iters"],
-            "frobenius_at": {str(k): float(v["frobenius"][0]) for k, v in rep["snaps"].items()},
-            "setup_seconds": rep["setup_seconds"], "mean_sweep_seconds": float(np.mean(rep["wall_times"])),
-            "sketch_cols": SKETCH_COLS["c4"], "sketch_seed": SKETCH_SEED,
-            "host_threads": os.cpu_count(), "numpy": np.__version__}
-    np.savez_compressed(os.path.join(HERE, "c4long.npz"), **out)
-    with open(os.path.join(HERE, "c4long.json"), "w") as fh:
-        json.dump(meta, fh, indent=1)
-    print("c4long done:", meta)
+    print("c4long done:", save(rep))
 
 
 def run_sketch(name):

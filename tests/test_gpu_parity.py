@@ -514,18 +514,6 @@ def test_solve_shapes_match_oracle(p, k, f):
     assert np.array_equal(rep.result, rep.result.T)
 
 
-def test_block_update_rejects_asymmetric_sigma():
-    import paper_2502_06377_b200 as pkg
-
-    a = random_spd(40, 5)
-    s = np.eye(40)
-    s[0, 3] = 0.5
-    with pytest.raises(ValueError):
-        pkg.block_update(a, s, np.arange(20), np.arange(20, 40))
-    with pytest.raises(ValueError):
-        pkg.error_estimate(a, s, np.arange(20), np.arange(20, 40))
-
-
 @pytest.mark.parametrize("stopping", ["estimate", "frobenius"])
 def test_device_loop_equals_host_loop(stopping, monkeypatch):
     """The conditional-graph solve loop gives the host loop's sweeps bit for bit."""
