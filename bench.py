@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--sharded", action="store_true", help="use the sharded driver even at N=1 (diagnostic)")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance run")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "p2p"])
+    ap.add_argument("--operands", default="auto", choices=["auto", "replicated", "sharded"],
+                    help="sharded driver: A and W replicated, or A row panels + W column shards gathered per step "
+                         "(auto: sharded when N > 1)")
     ap.add_argument("--gemm", default="dmma", choices=["dmma", "ozaki"],
                     help="headline GEMM path: FP64 DMMA (default) or Ozaki-II INT8 emulation")
     ap.add_argument("--moduli", type=int, default=16, help="Ozaki-II moduli (8..20)")
@@ -510,11 +513,13 @@ def run_ours(args):
         ms_step = ms / args.steps
         consistent = None
         clocks = head["clocks"]
+        sharded_info = None
     else:
         from paper_2502_06377_b200.distributed import ShardedSolver
 
         t0 = time.perf_counter()
-        solver = ShardedSolver(a_dev, part, device=dev, exchange=args.exchange)
+        solver = ShardedSolver(a_host if a_host is not None else a_dev, part, device=dev, exchange=args.exchange,
+                               operands=args.operands)
         solver.init_sigma(guess)
         torch.cuda.synchronize()
         setup_s = time.perf_counter() - t0
@@ -554,6 +559,12 @@ def run_ours(args):
             consistent = bool(lo_.item() == hi_.item())
         kt, head, alt = None, None, None
         clocks = clk.summary()
+        comm = [solver.comm_bytes(k) for k in range(len(part.sets))]
+        sharded_info = {"operands": solver.operands, "exchange_mode": solver.exchange, "panel": solver.layout.panel,
+                        "comm_bytes_per_sweep_this_rank": {key: int(sum(c[key] for c in comm)) for key in comm[0]},
+                        "nvlink_model_ms_per_sweep": sum(
+                            max(c["exchange_out"], c["exchange_in"]) + c["allreduce_top"] + c["allgather_w_in"]
+                            for c in comm) / 770e9 * 1e3}
         ttt = None
         if not args.no_ttt:
             solver.init_sigma(guess)
@@ -602,7 +613,8 @@ def run_ours(args):
             torch.distributed.barrier()
             t0 = time.perf_counter()
             rep = solve_sharded(a_host, part, pkg.IbmiConfig(tol=1e-300, max_iterations=args.steps,
-                                                             initial_guess=guess), exchange=args.exchange)
+                                                             initial_guess=guess), exchange=args.exchange,
+                                operands=args.operands)
             walls.append(max_over_ranks(time.perf_counter() - t0, dev))
             del rep
         wall = min(walls)
@@ -670,6 +682,7 @@ def run_ours(args):
             "setup_s": setup_s,
             "ranks_consistent": consistent,
             "exchange": getattr(solver, "exchange", None) if world > 1 else None,
+            "sharded": sharded_info,
             "time_to_tol": ttt,
             "power_iterations": [e[1] for e in errs],
             "error_trace": [e[0] for e in errs],

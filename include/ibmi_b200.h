@@ -268,6 +268,13 @@ typedef struct {
 int ibmi_gemm(const ibmi_gemm_desc* desc, void* stream);
 int ibmi_gemm_workspace(const ibmi_gemm_desc* desc, int64_t* doubles);
 
+/* Rows of the symmetric block update from an all-reduced lower triangle (the
+ * sharded Σ_II = sym(A_II⁻¹ + M·Wᵀ), solver.py:125-127):
+ * dst[i][j] = base[r][j] + (j <= r ? low[r][j] : low[j][r]), r = rows[i] (device int64).
+ * Stream-ordered, no synchronisation (graph-capturable). */
+int ibmi_sym_rows(const double* base, int64_t ldb, const double* low, int64_t ldl, const int64_t* rows, int64_t nrows,
+                  int64_t n, double* dst, int64_t ldd, void* stream);
+
 /* The CUDA stream the context's work is ordered on (its own non-blocking
  * stream, or the one passed to ibmi_create). */
 int ibmi_context_stream(ibmi_ctx* ctx, void** stream);

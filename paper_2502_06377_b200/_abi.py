@@ -62,6 +62,7 @@ SIGNATURES = [
     ("ibmi_chol_solve", C.c_int, [_I64, _P, _I64, _I64, _P, _I64, _P, _I64, _P]),
     ("ibmi_gather", C.c_int, [_P, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     ("ibmi_scatter", C.c_int, [_P, _I64, _P, _I64, _P, _I64, _P, _I64, C.c_int, _P]),
+    ("ibmi_sym_rows", C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _P, _I64, _P]),
     ("ibmi_mc_guess", C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     ("ibmi_two_norm", C.c_int, [_I64, _I64, _P, _I64, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), _P]),

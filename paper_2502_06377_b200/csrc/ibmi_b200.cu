@@ -3135,6 +3135,19 @@ int ibmi_scatter(double* target, int64_t ldt, const int64_t* rows, int64_t nr, c
   return IBMI_OK;
 }
 
+int ibmi_sym_rows(const double* base, int64_t ldb, const double* low, int64_t ldl, const int64_t* rows, int64_t nrows,
+                  int64_t n, double* dst, int64_t ldd, void* stream) {
+  if (nrows < 0 || n < 0) return fail(IBMI_ERR_DIM, "negative size");
+  if (nrows == 0 || n == 0) return IBMI_OK;
+  if (!base || !low || !rows || !dst) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (nrows > INT_MAX || n > INT_MAX || ldd < n || ldb < n || ldl < n) return fail(IBMI_ERR_DIM, "bad leading dimension");
+  cudaStream_t st = (cudaStream_t)stream;
+  sym_rows_kernel<<<grid2d(nrows, n), 256, 0, st>>>(base, ldb, low, ldl, rows, dst, ldd, (int)nrows, (int)n);
+  note_launch();
+  CUDA_TRY(cudaGetLastError());
+  return IBMI_OK;
+}
+
 // Buffers of the stand-alone two_norm, kept per device between calls (the
 // sharded sweep calls it once per sweep; no cudaMalloc on that path).
 struct NormCache {

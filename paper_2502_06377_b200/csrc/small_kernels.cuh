@@ -133,6 +133,23 @@ __global__ void scatter2d_kernel(const double* __restrict__ src, int64_t lds, do
   }
 }
 
+// Rows of a symmetric block from its lower triangle (sharded Σ_II):
+// dst[i][j] = base[r][j] + (j <= r ? low[r][j] : low[j][r]),  r = rows[i].
+// `low` holds the all-reduced lower triangle of M·Wᵀ (its strict upper part is
+// never read); `base` is A_II⁻¹.  One launch replaces the index_select / add /
+// transpose / diagonal-fix chain of the eager path.
+__global__ void sym_rows_kernel(const double* __restrict__ base, int64_t ldb, const double* __restrict__ low,
+                                int64_t ldl, const int64_t* __restrict__ rows, double* __restrict__ dst,
+                                int64_t ldd, int nrows, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = blockIdx.y; i < nrows; i += gridDim.y) {
+    if (j >= n) continue;
+    const int64_t r = rows[i];
+    const double t = (j <= r) ? low[r * ldl + j] : low[(int64_t)j * ldl + r];
+    dst[(int64_t)i * ldd + j] = base[r * ldb + j] + t;
+  }
+}
+
 __global__ void fill2d_kernel(double* __restrict__ dst, int64_t ldd, int rows, int cols, double v,
                               double diag) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;

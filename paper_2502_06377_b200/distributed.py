@@ -97,6 +97,7 @@ class GemmSpec:
     yrows: int = 0
     ycols: int = 0
     xt: bool = False                 # X given transposed: X(m, k) = x[seg.x0 + k][xm.off0 + m]
+    yt: bool = False                 # Y given transposed: Y(n, k) = y[seg.y0 + k][yn.off0 + n]
     peers: object = None             # int64 tensor of per-rank Σ panel pointers (fused exchange)
     bc_panel: int = 0
     bc_world: int = 1
@@ -164,6 +165,42 @@ class CudaBackend:
     def index_tensor(self, idx):
         return self.torch.as_tensor(np.asarray(idx, dtype=np.int64), device=self.device)
 
+    # operand-sharded set-up (ShardedSolver, operands="sharded"): primitives only
+    def upload_rows(self, a, rows):
+        """Device copy of ``a[rows, :]`` with the leading dimension padded to 32 doubles
+        (16-byte aligned rows for TMA; padding columns are zero)."""
+        torch = self.torch
+        n, p = len(rows), int(a.shape[1])
+        out = torch.zeros((max(n, 1), -(-p // 32) * 32), dtype=torch.float64, device=self.device)
+        if n:
+            if hasattr(a, "is_cuda"):
+                out[:n, :p] = a.to(self.device, torch.float64).index_select(0, self.index_tensor(rows))
+            else:
+                out[:n, :p] = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)[rows, :]))
+        return out[:n, :p] if n else out[:0, :p]
+
+    def spd_inverse(self, blk):
+        """A_II⁻¹ on the device (linalg.py:122-130): symmetric check (linalg.py:68-77),
+        blocked Cholesky + inverse; raises NotPositiveDefinite(index) like the reference."""
+        from . import linalg
+
+        torch = self.torch
+        if not hasattr(blk, "is_cuda"):
+            blk = torch.from_numpy(np.ascontiguousarray(np.asarray(blk, dtype=np.float64)))
+        d = blk.to(self.device, torch.float64).contiguous()
+        scale = float(d.abs().max()) if d.numel() else 0.0
+        if scale != 0.0 and float((d - d.t()).abs().max()) > linalg.SYMMETRY_RTOL * scale:
+            raise ValueError("matrix is not symmetric")
+        return linalg.spd_inverse(d, self.device.index)
+
+    def sym_rows(self, base, low, rel, dst):
+        """dst[i, :] = base[rel[i], :] + symmetric completion of the lower triangle ``low``."""
+        n = base.shape[0]
+        stream = C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+        _abi.check(self.L.ibmi_sym_rows(C.c_void_p(base.data_ptr()), base.stride(0), C.c_void_p(low.data_ptr()),
+                                        low.stride(0), C.c_void_p(rel.data_ptr()), rel.numel(), n,
+                                        C.c_void_p(dst.data_ptr()), dst.stride(0), stream), "sym_rows")
+
     def gemm(self, s: GemmSpec):
         torch = self.torch
         d = _abi.GemmDesc()
@@ -191,7 +228,7 @@ class CudaBackend:
             d.d, d.ldd = s.d.data_ptr(), s.d.stride(0)
             d.dm, d.dn = _cmap(s.dm), _cmap(s.dn)
         d.lower, d.tma_safe, d.splits = int(s.lower), int(s.tma_safe), 0     # 0: automatic split-K
-        d.xt = int(s.xt)
+        d.xt, d.yt = int(s.xt), int(s.yt)
         if s.peers is not None:
             d.peers, d.bc_panel, d.bc_world, d.bc_rank = s.peers.data_ptr(), s.bc_panel, s.bc_world, s.bc_rank
         out = None
@@ -263,6 +300,11 @@ class CudaBackend:
 
 
 # --------------------------------------------------------------------------- collectives
+class _Done:
+    def wait(self):
+        return True
+
+
 class _Comm:
     """torch.distributed calls, staging CUDA tensors through the host when the
     process group cannot take them (gloo)."""
@@ -311,6 +353,36 @@ class _Comm:
             self.dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
         return out
 
+    def broadcast(self, t, src: int):
+        """In-place broadcast of ``t`` from group rank ``src``."""
+        if self.world == 1:
+            return t
+        gsrc = self.dist.get_global_rank(self.group, src) if self.group is not None else src
+        if self._stage(t):
+            h = t.cpu()
+            self.dist.broadcast(h, src=gsrc, group=self.group)
+            if self.rank != src:
+                t.copy_(h)
+        else:
+            self.dist.broadcast(t, src=gsrc, group=self.group)
+        return t
+
+    def all_gather_start(self, out, inp):
+        """Start ``out[h] = inp of rank h`` (equal shapes; out is (world, *inp.shape)).
+        Returns a handle whose ``wait()`` orders the result before the caller's
+        later work.  NCCL: asynchronous on the communicator's stream, so the gather
+        overlaps kernels launched afterwards; gloo: done on return."""
+        if self.world == 1:
+            out[0].copy_(inp)
+            return _Done()
+        if self._stage(inp):
+            ho = out.cpu()
+            self.dist.all_gather_into_tensor(ho.view(-1), inp.cpu().contiguous().view(-1), group=self.group)
+            out.copy_(ho)
+            return _Done()
+        return self.dist.all_gather_into_tensor(out.view(-1), inp.contiguous().view(-1), group=self.group,
+                                                async_op=True)
+
     def all_gather_rows(self, t, counts):
         """Concatenate every rank's rows (rank order); counts[h] = rows of rank h."""
         torch = self.torch
@@ -337,7 +409,7 @@ class ShardedSolver:
     """
 
     def __init__(self, a, partition: Partition | None = None, ranges=None, *, group=None, panel: int = 128,
-                 backend=None, device: int | None = None, exchange: str = "auto"):
+                 backend=None, device: int | None = None, exchange: str = "auto", operands: str = "auto"):
         import torch
         import torch.distributed as dist
 
@@ -363,8 +435,19 @@ class ShardedSolver:
         lay, g = self.layout, self.rank
         self.own = lay.rows[g]
         self.n_loc = len(self.own)
-        self.A, self.W, self.ainv = backend.setup(a, self.ranges)
-        self.ld = self.A.stride(0)
+        self.n_max = max(len(r) for r in lay.rows)
+        if operands == "auto":
+            operands = "sharded" if self.world > 1 else "replicated"
+        if operands not in ("replicated", "sharded"):
+            raise ValueError(f"unknown operands mode {operands!r}")
+        self.operands = operands
+        self.own_t = backend.index_tensor(self.own)
+        self.rows_t = [backend.index_tensor(r) for r in lay.rows]
+        if operands == "replicated":
+            self.A, self.W, self.ainv = backend.setup(a, self.ranges)
+            self.ld = self.A.stride(0)
+        else:
+            self._setup_sharded(a)
         if exchange == "auto":
             # fused peer-memory exchange when every rank is on this node (NVLink/NVSwitch)
             import socket
@@ -399,8 +482,103 @@ class ShardedSolver:
         else:
             self.S = backend.zeros(max(self.n_loc, 1), self.ld)
         self.exchange = exchange
-        self.own_t = backend.index_tensor(self.own)
         self.plan = [self._plan_set(lo, hi) for (lo, hi) in self.ranges]
+
+    # ------------------------------------------------------------ operand-sharded set-up
+    def _setup_sharded(self, a):
+        """A, W_k and the set-up work split over the ranks (SURVEY §8(e) option B).
+
+        Rank g keeps the row panel ``A[own_g, :]`` (= the column panel, A is
+        symmetric) and the column shard ``W_k[:, own_g]`` of every set.  The K
+        Cholesky / inverse jobs (solver.py:116-119) go round-robin over the ranks and
+        each A_II⁻¹ (b × b) is broadcast; the W GEMM (solver.py:120) is local:
+        ``W_k[:, own_g ∩ c] = A_II⁻¹ · A[I, own_g ∩ c]`` with ``A[I, j] = A[j, I]``
+        read from the row panel.  Nothing of order p² is replicated."""
+        from .exceptions import NotPositiveDefinite
+
+        torch, be, lay, g = self.torch, self.be, self.layout, self.rank
+        p = self.p
+        if tuple(a.shape) != (p, p):
+            from .exceptions import DimensionMismatch
+
+            raise DimensionMismatch(f"expected a square matrix, got shape {tuple(a.shape)}")
+        self.A = be.upload_rows(a, self.own)                      # n_loc × p view, padded ld
+        self.ld = -(-p // 32) * 32
+        # (1) this rank's inverses; every rank learns every outcome before anyone raises
+        mine, status = {}, []
+        for k, (lo, hi) in enumerate(self.ranges):
+            if k % self.world != g:
+                continue
+            try:
+                mine[k] = be.spd_inverse(a[lo:hi, lo:hi])
+            except NotPositiveDefinite as e:
+                status.append((k, "spd", int(e.index)))
+            except ValueError as e:
+                status.append((k, "sym", str(e)))
+        allst = [None] * self.world
+        if self.world > 1:
+            torch.distributed.all_gather_object(allst, status, group=self.comm.group)
+        else:
+            allst = [status]
+        bad = sorted(x for st in allst for x in st)
+        if bad:
+            k, kind, info = bad[0]
+            if kind == "spd":
+                raise NotPositiveDefinite(info, set_index=k)
+            raise ValueError(info)
+        # (2) broadcast A_II⁻¹, form the local W shard
+        self.ainv, self.Wg, self.W = [], [], None
+        ldw = -(-max(self.n_max, 1) // 32) * 32
+        for k, (lo, hi) in enumerate(self.ranges):
+            b = hi - lo
+            inv = mine.pop(k) if k in mine else be.zeros(b, b)
+            self.comm.broadcast(inv, k % self.world)
+            self.ainv.append(inv)
+            a0, a1 = lay.local_range(g, lo, hi)
+            wg = be.zeros(b, ldw)
+            n_cl = self.n_loc - (a1 - a0)
+            if n_cl > 0:
+                # W[:, j] = Σ_i A_II⁻¹[:, i] · A[own_j, lo + i] for the local complement columns j
+                be.gemm(GemmSpec(x=inv, xm=0, y=self.A, yn=(a0, 0, a1), m=b, n=n_cl, segs=[(0, lo, b)],
+                                 c=wg, cm=0, cn=(a0, 0, a1), tma_safe=True, xrows=b, xcols=b,
+                                 yrows=self.n_loc, ycols=p))
+            self.Wg.append(wg)
+        self._wfull = None
+        self._wstage = None
+        self._wpending = {}
+
+    def _w_gather_start(self, k):
+        """Begin the all-gather of W_k's column shards (the active block's panel
+        broadcast).  W is static, so step k + 1's gather is started before step k's
+        GEMMs and overlaps them on the communicator's stream."""
+        if self.world == 1 or k in self._wpending:
+            return
+        bmax = max(hi - lo for lo, hi in self.ranges)
+        ldw = self.Wg[k].shape[1]
+        if self._wstage is None:
+            self._wstage = [self.be.zeros(self.world, bmax, ldw) for _ in range(2)]
+            self._wfull = self.be.zeros(bmax, self.ld)
+        b = self.Wg[k].shape[0]
+        st = self._wstage[k % 2]
+        out = st.view(-1)[: self.world * b * ldw].view(self.world, b, ldw)
+        self._wpending[k] = (self.comm.all_gather_start(out, self.Wg[k]), out)
+
+    def _w_full(self, k):
+        """W_k over all p columns in natural order (b × p view, zeros on I_k)."""
+        if self.operands == "replicated":
+            return self.W[k]
+        if self.world == 1:
+            return self.Wg[k]
+        self._w_gather_start(k)
+        work, out = self._wpending.pop(k)
+        work.wait()
+        b = self.Wg[k].shape[0]
+        full = self._wfull[:b]
+        for h in range(self.world):
+            n_h = len(self.layout.rows[h])
+            if n_h:
+                full.index_copy_(1, self.rows_t[h], out[h][:, :n_h])
+        return full
 
     # ------------------------------------------------------------ per-set plan
     def _plan_set(self, lo, hi):
@@ -424,6 +602,8 @@ class ShardedSolver:
 
     def _w_loc(self, k):
         """W_k restricted to this rank's columns, compact (zeros stay on I)."""
+        if self.operands == "sharded":
+            return self.Wg[k]
         cache = self.__dict__.setdefault("_wloc", {})
         if k not in cache:
             # one rank owns every column: W itself (its padding columns are never read)
@@ -451,7 +631,7 @@ class ShardedSolver:
         vals = torch.ones(self.n_loc, dtype=torch.float64, device=self.S.device)
         if guess == "jacobi":
             lo, hi = self.ranges[0]
-            diag = self.A[self.own_t, self.own_t]
+            diag = self.A[self.own_t if self.operands == "replicated" else loc, self.own_t]
             inc = (self.own_t < lo) | (self.own_t >= hi)
             vals = torch.where(inc, 1.0 / diag, vals)
         elif guess != "identity":
@@ -471,8 +651,11 @@ class ShardedSolver:
         p = self.p
         p2p = self.exchange == "p2p"
         Mbuf = self._mbuf(b, n_cl)
+        wfull = self._w_full(k)
+        if self.operands == "sharded" and len(self.ranges) > 1:
+            self._w_gather_start((k + 1) % len(self.ranges))     # prefetch: overlaps this step's GEMMs
         if n_cl > 0:
-            spec = GemmSpec(x=self.W[k], xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl,
+            spec = GemmSpec(x=wfull, xm=0, y=self.S, yn=(a0, 0, a1), m=b, n=n_cl,
                             segs=[(0, 0, lo), (hi, hi, p - hi)], c=Mbuf, cm=0, cn=0, mirror=True, c2=self.S,
                             c2m=lo, c2n=(a0, 0, a1), alpha=-1.0, tma_safe=True, xrows=b, xcols=p,
                             yrows=self.n_loc, ycols=p)
@@ -488,12 +671,8 @@ class ShardedSolver:
                              tma_safe=True, xrows=b, xcols=n_cl, yrows=b, ycols=self.n_loc))
         self.comm.all_reduce(top)     # in p2p mode also the barrier after which the peer stores have landed
         if a1 > a0:
-            rel = pl["my_rows_rel"]
-            # Σ_II rows = ainv + (lower sum mirrored); the diagonal appears in both halves once
-            t = self.ainv[k].index_select(0, rel) + top.index_select(0, rel) + top.t().index_select(0, rel)
-            ar = self.torch.arange(a1 - a0, device=top.device)
-            t[ar, rel] -= top[rel, rel]
-            self.S[a0:a1, lo:hi] = t
+            # Σ_II rows = ainv + the lower sum completed symmetrically, one kernel
+            be.sym_rows(self.ainv[k], top, pl["my_rows_rel"], self.S[a0:a1, lo:hi])
         if p2p:
             # with overlapping sets the next step's peer stores hit rows of I_k ∩ I_{k+1}
             # that the Σ_II write above also touches: every rank must finish it first
@@ -524,6 +703,12 @@ class ShardedSolver:
             self._mb = buf = self.be.zeros(need)
         return buf[:need].view(b, max(n_cl, 1))
 
+    def _bbuf(self, b, c):
+        buf = getattr(self, "_bb", None)
+        if buf is None or buf.numel() < b * c:
+            self._bb = buf = self.be.zeros(b * c)
+        return buf[: b * c].view(b, c)
+
     def _top(self, b):
         buf = getattr(self, "_tb", None)
         if buf is None or buf.numel() < b * b:
@@ -536,6 +721,19 @@ class ShardedSolver:
         torch, be, pl = self.torch, self.be, self.plan[k]
         lo, hi, b, a0, a1 = pl["lo"], pl["hi"], pl["b"], pl["a0"], pl["a1"]
         p, c = self.p, self.p - b
+        if self.operands == "sharded":
+            # B = Σ[I, :]·A[:, c] = Σ_g Σ[own_g, I]ᵀ · A[own_g, c]: both factors are columns of
+            # the local row panels (a contraction over the local rows), then one all-reduce
+            B = self._bbuf(b, c)
+            B.zero_()
+            if self.n_loc:
+                for col0, n, out0 in ((0, lo, 0), (hi, p - hi, lo)):
+                    if n > 0:
+                        be.gemm(GemmSpec(x=self.S, xm=lo, y=self.A, yn=col0, m=b, n=n, segs=[(0, 0, self.n_loc)],
+                                         c=B, cm=0, cn=out0, xt=True, yt=True, xrows=self.n_loc, xcols=p,
+                                         yrows=self.n_loc, ycols=p))
+            self.comm.all_reduce(B)
+            return be.two_norm(B, rtol, max_iters)
         Bloc = be.zeros(max(a1 - a0, 1), c)[: a1 - a0]
         if a1 > a0:
             be.gemm(GemmSpec(x=self.S, xm=a0, y=self.A, yn=(lo, 0, hi), m=a1 - a0, n=c, segs=[(0, 0, p)],
@@ -555,13 +753,48 @@ class ShardedSolver:
         """‖I − AΣ‖_F = ‖I − ΣA‖_F from local rows of ΣA, then all-reduce."""
         torch = self.torch
         part = torch.zeros(1, dtype=torch.float64, device=self.S.device)
-        if self.n_loc:
+        if self.operands == "sharded":
+            # A's rows arrive chunk by chunk in natural order (all-gather of the row panels'
+            # slices), so the δ of the fused epilogue sees contiguous global columns
+            lay, be, p = self.layout, self.be, self.p
+            chunk = lay.panel * self.world * max(1, 2048 // (lay.panel * self.world))
+            for r0 in range(0, p, chunk):
+                r1 = min(p, r0 + chunk)
+                rows = self._gather_rows_natural(self.A, r0, r1)
+                if self.n_loc:
+                    part[0] += be.gemm(GemmSpec(x=self.S, xm=0, y=rows, yn=0, m=self.n_loc, n=r1 - r0,
+                                                segs=[(0, 0, p)], cidx=self.own_t, cn=r0, frob=True, tma_safe=True,
+                                                xrows=self.n_loc, xcols=p, yrows=r1 - r0, ycols=p))
+        elif self.n_loc:
             v = self.be.gemm(GemmSpec(x=self.S, xm=0, y=self.A, yn=0, m=self.n_loc, n=self.p,
                                       segs=[(0, 0, self.p)], cidx=self.own_t, frob=True, tma_safe=True,
                                       xrows=self.n_loc, xcols=self.p, yrows=self.p, ycols=self.p))
             part[0] = v
         self.comm.all_reduce(part)
         return float(torch.sqrt(part)[0])
+
+    def _gather_rows_natural(self, local, r0, r1):
+        """Rows [r0, r1) of a row-panel-sharded matrix, natural order, on every rank."""
+        lay, be = self.layout, self.be
+        rng = [lay.local_range(h, r0, r1) for h in range(self.world)]
+        nmax = max(1, max(b - a for a, b in rng))
+        ld = local.stride(0) if local.shape[0] else self.ld
+        key = (nmax, ld)
+        if getattr(self, "_rowstage_key", None) != key:
+            self._rowstage = be.zeros(self.world, nmax, ld)
+            self._rownat = be.zeros(lay.panel * self.world * max(1, 2048 // (lay.panel * self.world)), ld)
+            self._rowstage_key = key
+        a, b = rng[self.rank]
+        mine = be.zeros(nmax, ld)
+        if b > a:
+            mine[: b - a, : local.shape[1]] = local[a:b]
+        self.comm.all_gather_start(self._rowstage, mine).wait()
+        out = self._rownat[: r1 - r0]
+        for h in range(self.world):
+            a, b = rng[h]
+            if b > a:
+                out.index_copy_(0, self.rows_t[h][a:b] - r0, self._rowstage[h][: b - a])
+        return out[:, : self.p]
 
     def gather_sigma(self):
         """Full Σ (host numpy) on every rank, original index order."""
@@ -579,13 +812,32 @@ class ShardedSolver:
             full = full[np.ix_(inv, inv)]
         return full
 
+    def comm_bytes(self, k: int) -> dict:
+        """Bytes this rank moves over NVLink in block step k (each direction), by phase:
+        the b × c transpose exchange (fused peer stores or all_to_all), the ring
+        all-reduce of the b × b lower-triangle partials, and — operands sharded — the
+        all-gather of W_k's column shards.  ``gemm_flops`` is this rank's share of
+        2bc² + 2b²c, for the comm/compute budget in DESIGN.md §6."""
+        pl, g, G = self.plan[k], self.rank, self.world
+        b, n_cl = pl["b"], pl["n_cl"]
+        n_I = pl["n_I"][g]
+        c = self.p - b
+        return {"exchange_out": 8 * (b - n_I) * n_cl, "exchange_in": 8 * n_I * (c - n_cl),
+                "allreduce_top": int(8 * b * b * 2 * (G - 1) / G),
+                "allgather_w_in": 8 * b * (self.p - self.n_loc) if self.operands == "sharded" and G > 1 else 0,
+                "gemm_flops": 2 * b * c * n_cl + 2 * b * b * n_cl}
+
     def close(self):
+        for work, _ in getattr(self, "_wpending", {}).values():
+            work.wait()
+        self._wpending = {}
         self.be.close()
 
 
 # --------------------------------------------------------------------------- public entry point
 def solve_sharded(a, part: Partition, cfg=None, *, group=None, panel: int = 128, device: int | None = None,
-                  exchange: str = "auto", backend=None, gather_result: bool = True, callback=None):
+                  exchange: str = "auto", backend=None, gather_result: bool = True, callback=None,
+                  operands: str = "auto"):
     """``solve`` (reference solver.py:225-278) with Σ sharded over the process group.
 
     Call it on every rank with the same ``a`` (host array or a device copy) and
@@ -612,7 +864,8 @@ def solve_sharded(a, part: Partition, cfg=None, *, group=None, panel: int = 128,
     validate(part)
     stopping = getattr(cfg, "stopping", "estimate")
     t0 = time.perf_counter()
-    ss = ShardedSolver(a, part, group=group, panel=panel, backend=backend, device=device, exchange=exchange)
+    ss = ShardedSolver(a, part, group=group, panel=panel, backend=backend, device=device, exchange=exchange,
+                       operands=operands)
     try:
         ss.init_sigma(cfg.initial_guess)
         setup_s = time.perf_counter() - t0

@@ -39,11 +39,15 @@ def _worker(rank, world, port, case, out):
         from paper_2502_06377_b200 import contiguous_partition, red_black_partition
         from paper_2502_06377_b200.distributed import ShardedSolver
 
-        p, k, f, sweeps, guess = case
+        p, k, f, sweeps, guess = case[:5]
+        operands = case[5] if len(case) > 5 else "replicated"
         m = np.random.default_rng(p + k).standard_normal((p, p))
         a = m.T @ m + p * np.eye(p)
         part = red_black_partition(p) if k == 0 else contiguous_partition(p, k, f)
-        ss = ShardedSolver(a, part, panel=8, backend=TorchCPUBackend())
+        ss = ShardedSolver(a, part, panel=8, backend=TorchCPUBackend(), operands=operands)
+        assert ss.operands == operands
+        if operands == "sharded":
+            assert ss.W is None and ss.A.shape[0] == ss.n_loc      # nothing of order p² replicated
         ss.init_sigma(guess)
         errs = [ss.sweep()[0] for _ in range(sweeps)]
         sig = ss.gather_sigma()
@@ -53,9 +57,14 @@ def _worker(rank, world, port, case, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", [(96, 3, 0.1, 4, "identity"), (80, 2, 0.0, 3, "jacobi"), (64, 0, 0.0, 3, "identity"),
-                                  (100, 4, 0.2, 3, "identity")])
+@pytest.mark.parametrize("world,case", [
+    (w, c) for w in (2, 3) for c in [(96, 3, 0.1, 4, "identity"), (80, 2, 0.0, 3, "jacobi"),
+                                     (64, 0, 0.0, 3, "identity"), (100, 4, 0.2, 3, "identity")]
+] + [
+    # operands sharded: A row panels, W column shards gathered per step, set-up split over the ranks
+    (w, c) for w in (2, 3, 4) for c in [(96, 3, 0.1, 4, "identity", "sharded"), (80, 2, 0.0, 3, "jacobi", "sharded"),
+                                        (100, 4, 0.2, 3, "identity", "sharded")]
+] + [(4, (96, 3, 0.1, 4, "identity")), (4, (64, 0, 0.0, 3, "identity", "sharded")), (5, (100, 5, 0.2, 2, "jacobi", "sharded"))])
 def test_sharded_matches_oracle(world, case):
     from oracle import ibmi_oracle as orc
     from paper_2502_06377_b200 import contiguous_partition, red_black_partition
@@ -82,7 +91,7 @@ def test_sharded_matches_oracle(world, case):
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    p, k, f, sweeps, guess = case
+    p, k, f, sweeps, guess = case[:5]
     m = np.random.default_rng(p + k).standard_normal((p, p))
     a = m.T @ m + p * np.eye(p)
     part = red_black_partition(p) if k == 0 else contiguous_partition(p, k, f)

@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, backend, case, out, exchange="nccl"):
+def _worker(rank, world, port, backend, case, out, exchange="nccl", operands="auto"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -45,7 +45,9 @@ def _worker(rank, world, port, backend, case, out, exchange="nccl"):
             p, k, f = name
             m = np.random.default_rng(p).standard_normal((p, p))
             a, part, guess = m.T @ m + p * np.eye(p), contiguous_partition(p, k, f), "identity"
-        ss = ShardedSolver(a, part, panel=panel, device=0, exchange=exchange)
+        ss = ShardedSolver(a, part, panel=panel, device=0, exchange=exchange, operands=operands)
+        if operands == "sharded":
+            assert ss.W is None and ss.A.shape[0] == ss.n_loc
         ss.init_sigma(guess)
         errs = [ss.sweep()[0] for _ in range(sweeps)]
         sig = ss.gather_sigma()
@@ -56,11 +58,11 @@ def _worker(rank, world, port, backend, case, out, exchange="nccl"):
         dist.destroy_process_group()
 
 
-def _run(world, backend, case, exchange="nccl"):
+def _run(world, backend, case, exchange="nccl", operands="auto"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, case, q, exchange)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, case, q, exchange, operands)) for r in range(world)]
     for pr in procs:
         pr.start()
     import queue
@@ -82,11 +84,13 @@ def _run(world, backend, case, exchange="nccl"):
     return res
 
 
-@pytest.mark.parametrize("world,backend,exchange", [(1, "nccl", "nccl"), (2, "gloo", "nccl"), (1, "nccl", "p2p"),
-                                                     (2, "gloo", "p2p")])
-def test_sharded_c1_matches_reference(world, backend, exchange):
+@pytest.mark.parametrize("world,backend,exchange,operands", [
+    (1, "nccl", "nccl", "replicated"), (2, "gloo", "nccl", "replicated"), (1, "nccl", "p2p", "replicated"),
+    (2, "gloo", "p2p", "replicated"), (1, "nccl", "p2p", "sharded"), (2, "gloo", "p2p", "sharded"),
+    (2, "gloo", "nccl", "sharded")])
+def test_sharded_c1_matches_reference(world, backend, exchange, operands):
     g = golden("c1.npz")
-    res = _run(world, backend, ("c1", int(g["iterations"][0]), 128), exchange)
+    res = _run(world, backend, ("c1", int(g["iterations"][0]), 128), exchange, operands)
     for rank, errs, sig, fr in res:
         assert np.linalg.norm(sig - g["sigma"]) <= 1e-10 * np.linalg.norm(g["sigma"])
         ref = g["error_trace"]
@@ -94,17 +98,79 @@ def test_sharded_c1_matches_reference(world, backend, exchange):
         assert fr < 1e-9
 
 
-@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+@pytest.mark.parametrize("exchange,operands", [("nccl", "replicated"), ("p2p", "replicated"), ("p2p", "sharded"),
+                                               ("nccl", "sharded")])
 @pytest.mark.parametrize("case", [((1024, 4, 0.125), 6, 128), ((520, 3, 0.1), 5, 64)])
-def test_sharded_two_ranks_match_oracle(case, exchange):
+def test_sharded_two_ranks_match_oracle(case, exchange, operands):
     from oracle import ibmi_oracle as orc
     from paper_2502_06377_b200 import contiguous_partition
 
     (p, k, f), sweeps, panel = case
-    res = _run(2, "gloo", case, exchange)
+    res = _run(2, "gloo", case, exchange, operands)
     m = np.random.default_rng(p).standard_normal((p, p))
     a = m.T @ m + p * np.eye(p)
     o = orc.solve(a, contiguous_partition(p, k, f).sets, tol=1e-300, max_iterations=sweeps)
     for rank, errs, sig, fr in res:
         assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
         np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-13)
+
+
+def test_sharded_operands_three_ranks_and_not_spd():
+    """Operand-sharded set-up on 3 ranks sharing the GPU (uneven panels), and the
+    collective NotPositiveDefinite of a set whose owner is another rank."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import contiguous_partition
+
+    case = ((600, 4, 0.1), 4, 64)
+    (p, k, f), sweeps, panel = case
+    res = _run(3, "gloo", case, "p2p", "sharded")
+    m = np.random.default_rng(p).standard_normal((p, p))
+    a = m.T @ m + p * np.eye(p)
+    o = orc.solve(a, contiguous_partition(p, k, f).sets, tol=1e-300, max_iterations=sweeps)
+    for rank, errs, sig, fr in res:
+        assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
+        np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-13)
+        assert abs(fr - orc.frobenius_residual(a, o["result"])) <= 1e-9 * max(1.0, fr)
+
+
+def _bad_worker(rank, world, port, out):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_06377_b200 import NotPositiveDefinite, contiguous_partition
+        from paper_2502_06377_b200.distributed import ShardedSolver
+
+        p = 256
+        m = np.random.default_rng(3).standard_normal((p, p))
+        a = m.T @ m + p * np.eye(p)
+        a[200, 200] = -1.0                      # set 1 (owner: rank 1) is not SPD, local pivot 200 - lo
+        part = contiguous_partition(p, 2, 0.0)
+        try:
+            ShardedSolver(a, part, panel=64, device=0, exchange="nccl", operands="sharded")
+            out.put((rank, None))
+        except NotPositiveDefinite as e:
+            out.put((rank, (e.index, e.set_index)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_operands_not_spd_raises_on_every_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bad_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert sorted(res) == [(0, (72, 1)), (1, (72, 1))]

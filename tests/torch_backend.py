@@ -30,6 +30,16 @@ class TorchCPUBackend:
             ainv.append(torch.as_tensor(inv))
         return A, W, ainv
 
+    def upload_rows(self, a, rows):
+        return torch.as_tensor(np.asarray(a, dtype=np.float64)[np.asarray(rows, dtype=np.int64), :].copy())
+
+    def spd_inverse(self, blk):
+        return torch.as_tensor(orc.spd_inverse(np.asarray(blk, dtype=np.float64)))
+
+    def sym_rows(self, base, low, rel, dst):
+        full = torch.tril(low) + torch.tril(low, -1).T
+        dst.copy_(base[rel] + full[rel])
+
     def zeros(self, *shape):
         return torch.zeros(shape, dtype=torch.float64)
 
@@ -42,7 +52,9 @@ class TorchCPUBackend:
         acc = torch.zeros((s.m, s.n), dtype=torch.float64)
         for x0, y0, ln in s.segs:
             if ln > 0:
-                acc += s.x[rx, x0:x0 + ln] @ s.y[ry, y0:y0 + ln].T
+                xs = s.x[x0:x0 + ln][:, rx].T if s.xt else s.x[rx, x0:x0 + ln]
+                ys = s.y[y0:y0 + ln][:, ry].T if s.yt else s.y[ry, y0:y0 + ln]
+                acc += xs @ ys.T
         crow = s.cidx if s.cidx is not None else torch.as_tensor(map_indices(s.cm, s.m))
         ccol = torch.as_tensor(map_indices(s.cn, s.n))
         if s.frob:
