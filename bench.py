@@ -332,6 +332,32 @@ def run_reference(args):
     print(json.dumps(line), file=_JSON_OUT, flush=True)
 
 
+def panel_traffic(name: str) -> dict:
+    """`roofline.traffic` of the panel GEMM: ncu DRAM bytes per launch, measured per
+    config on the committed code (tools/panel_traffic.py -> profiles/*_panel_traffic.json);
+    null when no capture of this config is committed."""
+    best = None
+    prof = os.path.join(ROOT, "profiles")
+    for fn in sorted(os.listdir(prof)) if os.path.isdir(prof) else []:
+        if fn.endswith("_panel_traffic.json"):
+            try:
+                with open(os.path.join(prof, fn)) as fh:
+                    d = json.load(fh).get(name)
+            except (OSError, ValueError):
+                d = None
+            if d:
+                best = (fn, d)           # the latest round's file wins
+    if best is None:
+        return {"traffic": None, "traffic_note": "no ncu DRAM capture of this config committed"}
+    fn, d = best
+    return {"traffic": d["bytes_per_launch"],
+            "traffic_algorithmic": d["algorithmic_bytes_per_launch"],
+            "traffic_note": f"profiles/{fn}: {d['how']}; read {d['read_per_launch']:.3e} + written "
+                            f"{d['write_per_launch']:.3e} B per launch against an algorithmic "
+                            f"{d['algorithmic_bytes_per_launch']:.3e} (W + Sigma_cc read once, M written twice); "
+                            "operands exceed L2 at c3/c4, so resident CTAs re-stream them while the DMMA pipe is the bound"}
+
+
 def executed_flops(cfg):
     """FLOPs the kernels actually execute per sweep: K2 and the Gram product
     compute only the lower triangle of a symmetric result."""
@@ -651,14 +677,7 @@ def run_ours(args):
         panel_tf = panel_flops / (kt_["panel_gemm"] * 1e-3) / 1e12
         return {"bound": "tensor", "kernel": "gemm_tma_kernel (panel M = W Sigma_cc, FP64 DMMA, TMA)",
                 "achieved": panel_tf, "peak": peak, "unit": "TFLOP/s", "frac": panel_tf / peak,
-                "traffic": 15.78e9 if args.config == "c4" else None,
-                "traffic_note": ("ncu dram read+write bytes of one interior-set panel GEMM launch, split-K 3 "
-                                 "(profiles/r01_final2_c4_sweep.md): 14.94e9 read + 0.84e9 written (the partial "
-                                 "tiles; splitk_reduce_kernel writes M and its mirror). Algorithmic minimum 2.38e9 "
-                                 "(W + Sigma_cc read once, M written twice). W (283 MB) and Sigma_cc (1.53 GB) "
-                                 "exceed the 126 MB L2, so the resident CTAs re-stream them: 0.55 TB/s, 8% of HBM "
-                                 "bandwidth, while the DMMA pipe is 97.6% busy") if args.config == "c4"
-                else "measured for c4 only",
+                **panel_traffic(args.config),
                 "peak_source": "measured on this box: DMMA m8n8k4 throughput probe (ibmi_probe_fp64_peak)"}
 
     if rank == 0:

@@ -321,7 +321,9 @@ long long ibmi_launch_count(void);
  *         GEMM's operand reads, so overlapping them gained nothing);
  * key 11: INT8 GEMM on CTA pairs (cta_group::2, default 1) or single CTAs (0);
  * key 12: FP64 GEMM tile raster: bands of this many 128-row tile rows walked column by
- *         column (default 0 = tile-row-major). */
+ *         column (default 0 = tile-row-major);
+ * key 13: power iteration of mid-size Gram matrices (512 <= n <= 2220) with the
+ *         flag-carrying line exchange instead of a grid barrier per iteration (default 1). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

@@ -265,6 +265,7 @@ int g_split_diag = 0;       // split-K of the Σ_II GEMM (0 = auto)
 int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
+int g_power_ll = 1;         // mid-size Gram power iteration with the flag-carrying exchange (no grid barrier)
 int g_split_min_kt = 4;     // split-K keeps at least this many k-tiles per split
 int g_raster_group = 0;     // GEMM tile raster: bands of this many tile rows (0 = tm-major)
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
@@ -1739,7 +1740,7 @@ int ensure_estimate_buffers(ibmi_ctx* c, int64_t b, int64_t cc) {
   c->ldG = ldG;
   if (ensure_buf(&c->vec, &c->vec_cap, 2 * std::max(b, cc), &c->bytes)) return IBMI_ERR_OOM;
   int64_t pc = c->part_cap;
-  if (ensure_buf(&c->part, &pc, 4 * (int64_t)c->power_blocks, &c->bytes)) return IBMI_ERR_OOM;
+  if (ensure_buf(&c->part, &pc, (4 + 32) * (int64_t)c->power_blocks, &c->bytes)) return IBMI_ERR_OOM;  // + LL lines
   c->part_cap = (int)pc;
   return IBMI_OK;
 }
@@ -1916,6 +1917,43 @@ struct NormBufs {
   int oz_n = 0;
 };
 
+// Flag-exchange power iteration (power_gram_ll_kernel) when the Gram matrix fits its
+// shape: even n, ≤ 15 rows per CTA, ≤ 3072 columns, rows resident in registers + shared
+// memory.  Returns false when not applicable (the grid-barrier kernel runs instead).
+template <int RR, int Q>
+bool power_ll_inst(PowerParams& P, const NormBufs& nb, int grid, int rpc, size_t smem, cudaStream_t st) {
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    if (cudaFuncSetAttribute(power_gram_ll_kernel<RR, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024) !=
+        cudaSuccess) { cudaGetLastError(); return false; }
+    attr[dev & 63] = true;
+  }
+  double* msg = nb.part + 4 * (size_t)nb.blocks;
+  if (cudaMemsetAsync(msg, 0, (size_t)32 * nb.blocks * sizeof(double), st) != cudaSuccess) { cudaGetLastError(); return false; }
+  void* args[] = {&P, &msg, &rpc};
+  if (cudaLaunchCooperativeKernel((const void*)power_gram_ll_kernel<RR, Q>, dim3(grid), dim3(512), args, smem, st) !=
+      cudaSuccess) { cudaGetLastError(); return false; }
+  note_launch();
+  return true;
+}
+
+bool power_ll_launch(PowerParams& P, const NormBufs& nb, cudaStream_t st) {
+  const int n = P.n;
+  if (n < 512 || (n & 1) || n > 3072 || (P.ldg & 1) || !aligned16(P.G) || nb.threads != 512) return false;
+  const int rpc = (n + nb.blocks - 1) / nb.blocks;
+  if (rpc > LL_ROWS) return false;
+  const int grid = (n + rpc - 1) / rpc;
+  const int q = (n / 2 + 511) / 512;
+  const int rr = q == 1 ? 8 : (q == 2 ? 6 : 4);
+  const size_t smem = ((size_t)((grid * rpc + 1) & ~1) + 256 + 64 + (size_t)std::max(0, rpc - rr) * n) * sizeof(double);
+  if (smem > 220 * 1024) return false;
+  if (q == 1) return power_ll_inst<8, 1>(P, nb, grid, rpc, smem, st);
+  if (q == 2) return power_ll_inst<6, 2>(P, nb, grid, rpc, smem, st);
+  return power_ll_inst<4, 3>(P, nb, grid, rpc, smem, st);
+}
+
 int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, double rtol, int max_iters,
                      const NormBufs& nb, cudaStream_t st, cudaEvent_t ev_gram = nullptr) {
   const int mode = (b <= cc) ? 0 : 1;
@@ -1986,6 +2024,7 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
     if (cudaGetLastError() == cudaSuccess) return IBMI_OK;
     // cluster not schedulable here: fall through to the grid-wide kernel
   }
+  if (g_power_ll && power_ll_launch(P, nb, st)) return IBMI_OK;
   // rows of G kept resident in each CTA's shared memory, after the staged iterate
   const int64_t rpc = (n + nb.blocks - 1) / nb.blocks;
   P.resident = 0;
@@ -3172,7 +3211,7 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
   std::lock_guard<std::mutex> lock(nc.mu);
   if (!nc.blocks) {
     power_launch_shape(dev, &nc.blocks, &nc.threads, &nc.smem_cap);
-    CUDA_TRY(cudaMalloc(&nc.part, (size_t)4 * nc.blocks * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&nc.part, (size_t)(4 + 32) * nc.blocks * sizeof(double)));   // partials + LL lines
     CUDA_TRY(cudaMalloc(&nc.out, 4 * sizeof(double)));
     CUDA_TRY(cudaMallocHost(&nc.host, 4 * sizeof(double)));
   }
@@ -3467,6 +3506,9 @@ int ibmi_tune(int key, int value) {
       break;
     case 11:
       g_oz_pair = value ? 1 : 0;
+      break;
+    case 13:
+      g_power_ll = value ? 1 : 0;
       break;
     case 12:
       if (value < 0 || value > 1024) return fail(IBMI_ERR_INVALID, "raster group must be in [0, 1024]");

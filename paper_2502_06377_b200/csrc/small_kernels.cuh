@@ -529,6 +529,272 @@ __global__ void __launch_bounds__(512, 1) power_gram_kernel(PowerParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// The same power iteration with a flag-carrying exchange instead of a grid
+// barrier (mid-size Gram matrices: c2's 2048², c3's 1152²).
+//
+// One iteration of power_gram_kernel costs a grid barrier plus two dependent L2
+// round trips (partials, then the iterate): 6.1 µs at c2 against 0.9 µs of
+// arithmetic.  Here every CTA publishes its rows of z = G·y as ONE 128-byte line
+// — 15 doubles of payload and the iteration tag in the last 8 bytes, written by
+// a single 8-lane × 16-byte store, so the tag can only be seen together with
+// the payload (the LL128 idea of NCCL's low-latency protocol) — and every CTA
+// polls all lines.  One L2 round trip per iteration, no barrier, no partial sums:
+// each CTA recomputes yᵀz and zᵀz from the full z in the same fixed order, so
+// all CTAs take identical branches.
+//   * the iterate lives in registers, column-split: thread t owns the double2
+//     columns {q·512 + t}; G's rows are column-split the same way, RR rows per
+//     CTA in registers, the rest in shared memory (128 B/clk/SM is the matvec's
+//     bound, so registers halve it);
+//   * the 15 row sums per thread go through one transposing butterfly
+//     (16 shuffles) and a 16-warp shared-memory sum, fixed order;
+//   * the σ = 0 restart of mode 0 (y = B·vr) is the one place that still uses a
+//     grid barrier (the launch stays cooperative).
+// Preconditions (host): n even, rows per CTA ≤ 15, n ≤ 1024·Q, G 16-byte aligned
+// with even ldg, msg zeroed before the launch.
+constexpr int LL_ROWS = 15;
+
+__device__ __forceinline__ void ll_store16(double* p, double a, double b) {
+  asm volatile("st.volatile.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ double2 ll_load16(const double* p) {
+  double2 v;
+  asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+template <int RR, int Q>
+__global__ void __launch_bounds__(512, 1) power_gram_ll_kernel(PowerParams P, double* __restrict__ msg, int rpc) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double llsm[];
+  const int n = P.n, nblk = gridDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n2 = n >> 1;
+  const int rb0 = min(n, (int)blockIdx.x * rpc), myrows = min(n, rb0 + rpc) - rb0;
+  double* zr = llsm;                                  // nblk·rpc doubles: the raw new iterate
+  double* wred = zr + ((nblk * rpc + 1) & ~1);        // 16 warps × 16 row sums
+  double* red = wred + 256;                           // 2 × 32: block reductions, double-buffered
+  double* gres = red + 64;                            // (rpc − RR) rows × n, column-split reads
+  __shared__ double zloc[16];
+
+  // G rows: first RR in registers, the rest in shared memory
+  double2 greg[RR > 0 ? RR : 1][Q];
+#pragma unroll
+  for (int i = 0; i < RR; ++i)
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int c2 = q * 512 + tid;
+      greg[i][q] = (i < myrows && c2 < n2)
+                       ? *reinterpret_cast<const double2*>(P.G + (int64_t)(rb0 + i) * P.ldg + 2 * c2)
+                       : make_double2(0.0, 0.0);
+    }
+  for (int i = RR; i < myrows; ++i)
+    for (int c2 = tid; c2 < n2; c2 += 512)
+      reinterpret_cast<double2*>(gres + (size_t)(i - RR) * n)[c2] =
+          *reinterpret_cast<const double2*>(P.G + (int64_t)(rb0 + i) * P.ldg + 2 * c2);
+  __syncthreads();
+
+  int rpar = 0;
+  // Σ over the block of two values, identical in every thread (and every CTA)
+  auto block_sum2 = [&](double& a, double& b) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    double* r = red + rpar * 32;
+    rpar ^= 1;
+    if (lane == 0) { r[2 * wid] = a; r[2 * wid + 1] = b; }
+    __syncthreads();
+    double sa = 0.0, sb = 0.0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) { sa += r[2 * w]; sb += r[2 * w + 1]; }
+    a = sa;
+    b = sb;
+  };
+
+  long long tag = 0;
+  // z = G·y on this CTA's rows -> one tagged line -> every CTA's zr
+  auto exchange = [&](const double2 (&y)[Q]) {
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      double s = 0.0;
+      if (i < LL_ROWS && i < myrows) {
+        if (i < RR) {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) s = fma(greg[i < RR ? i : 0][q].x, y[q].x, fma(greg[i < RR ? i : 0][q].y, y[q].y, s));
+        } else {
+          const double2* row = reinterpret_cast<const double2*>(gres + (size_t)(i - RR) * n);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const int c2 = q * 512 + tid;
+            if (c2 < n2) {
+              const double2 g = row[c2];
+              s = fma(g.x, y[q].x, fma(g.y, y[q].y, s));
+            }
+          }
+        }
+      }
+      v[i] = s;
+    }
+    // transposing butterfly: 16 values × 32 lanes -> lane l holds the warp total of row l >> 1
+#pragma unroll
+    for (int half = 8, m = 16; half >= 1; half >>= 1, m >>= 1) {
+      const bool up = (lane & m) != 0;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double send = up ? v[i] : v[i + half];
+        const double keep = up ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    if ((lane & 1) == 0) wred[wid * 16 + (lane >> 1)] = v[0];
+    __syncthreads();
+    ++tag;
+    double* lines = msg + (size_t)(tag & 1) * nblk * 16;
+    if (wid == 0) {
+      double z = 0.0;
+      if (lane < 16) {
+#pragma unroll
+        for (int w = 0; w < 16; ++w) z += wred[w * 16 + lane];
+      }
+      const double a = __shfl_sync(0xffffffffu, z, (2 * lane) & 31);
+      double b = __shfl_sync(0xffffffffu, z, (2 * lane + 1) & 31);
+      if (lane == 7) b = __longlong_as_double(tag);
+      if (lane < 8) ll_store16(lines + (size_t)blockIdx.x * 16 + 2 * lane, a, b);
+    }
+    // poll: 8 lanes per line, 4 lines per warp and round
+    const int grp = tid >> 3, k = tid & 7;
+    for (int s0 = 0; s0 < nblk; s0 += 64) {
+      const int src = s0 + grp;
+      const bool live = src < nblk;
+      double2 d = make_double2(0.0, 0.0);
+      for (;;) {
+        if (live) d = ll_load16(lines + (size_t)src * 16 + 2 * k);
+        const long long f = __double_as_longlong(__shfl_sync(0xffffffffu, d.y, 7, 8));
+        if (__all_sync(0xffffffffu, !live || f == tag)) break;
+      }
+      if (live) {
+        const int base = src * rpc;
+        if (2 * k < rpc) zr[base + 2 * k] = d.x;
+        if (2 * k + 1 < rpc) zr[base + 2 * k + 1] = d.y;
+      }
+    }
+    __syncthreads();
+  };
+
+  double2 y[Q], ysc[Q], zz[Q];
+  auto load_iterate = [&](const double* src, bool through_l2) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int c2 = q * 512 + tid;
+      y[q] = make_double2(0.0, 0.0);
+      if (c2 < n2) y[q] = through_l2 ? make_double2(__ldcg(src + 2 * c2), __ldcg(src + 2 * c2 + 1))
+                                     : make_double2(src[2 * c2], src[2 * c2 + 1]);
+    }
+  };
+  auto fetch_z = [&](double& pyz, double& pzz) {
+    pyz = 0.0;
+    pzz = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int c2 = q * 512 + tid;
+      zz[q] = c2 < n2 ? reinterpret_cast<const double2*>(zr)[c2] : make_double2(0.0, 0.0);
+      pyz = fma(ysc[q].x, zz[q].x, fma(ysc[q].y, zz[q].y, pyz));
+      pzz = fma(zz[q].x, zz[q].x, fma(zz[q].y, zz[q].y, pzz));
+    }
+    block_sum2(pyz, pzz);
+  };
+
+  int it = 1;
+  bool restarted = false;
+  double prev = -1.0, sigma = 0.0, sc = 1.0, conv = 0.0;
+  if (P.mode == 0) {
+    load_iterate(P.vec, false);                        // y_1 = B·(1/√c), written by the previous kernel
+    double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) p1 = fma(y[q].x, y[q].x, fma(y[q].y, y[q].y, p1));
+    block_sum2(p0, p1);
+    sigma = sqrt(p1);
+    for (;;) {
+      if (sigma == 0.0) {
+        if (restarted) { conv = 1.0; break; }
+        // y = B·vr (linalg.py:237-244): rows over all warps of the grid, through global memory
+        const int gw = blockIdx.x * 16 + wid, tw = nblk * 16;
+        for (int r = gw; r < n; r += tw) {
+          const double* row = P.B + (int64_t)r * P.ldb;
+          double s = 0.0;
+          for (int j = lane; j < P.bcols; j += 32) s = fma(row[j], P.vr[j], s);
+          s = warp_sum(s);
+          if (lane == 0) P.vec[n + r] = s;
+        }
+        grid.sync();
+        load_iterate(P.vec + n, true);
+        restarted = true;
+        prev = -1.0;
+        if (it >= P.max_iters) { sigma = 0.0; conv = 0.0; it = P.max_iters; break; }
+        ++it;
+        p0 = 0.0; p1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) p1 = fma(y[q].x, y[q].x, fma(y[q].y, y[q].y, p1));
+        block_sum2(p0, p1);
+        sigma = sqrt(p1);
+        sc = 1.0;
+        continue;
+      }
+      if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
+      prev = sigma;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) ysc[q] = make_double2(sc * y[q].x, sc * y[q].y);
+      exchange(ysc);
+      double pyz, pzz;
+      fetch_z(pyz, pzz);
+      const double nw = sqrt(pyz);
+      if (nw == 0.0) { conv = 1.0; break; }
+      if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+      sigma = sqrt(pzz) / nw;
+      sc = 1.0 / nw;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) y[q] = zz[q];
+      ++it;
+    }
+  } else {
+    const double v1 = 1.0 / sqrt((double)n);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) y[q] = (q * 512 + tid < n2) ? make_double2(v1, v1) : make_double2(0.0, 0.0);
+    for (;;) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) ysc[q] = make_double2(sc * y[q].x, sc * y[q].y);
+      exchange(ysc);
+      double pyz, pzz;
+      fetch_z(pyz, pzz);
+      sigma = sqrt(fmax(pyz, 0.0));
+      if (sigma == 0.0) {
+        if (restarted) { conv = 1.0; break; }
+        if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+        load_iterate(P.vr, false);
+        restarted = true;
+        prev = -1.0;
+        sc = 1.0;
+        ++it;
+        continue;
+      }
+      if (fabs(sigma - prev) <= P.rtol * sigma) { conv = 1.0; break; }
+      prev = sigma;
+      const double nw = sqrt(pzz);
+      if (nw == 0.0) { conv = 1.0; break; }
+      if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
+      sc = 1.0 / nw;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) y[q] = zz[q];
+      ++it;
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    P.out[0] = sigma;
+    P.out[1] = conv;
+    P.out[2] = (double)it;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // DMMA throughput probe (the FP64 roofline denominator, measured on the box).
 __global__ void dmma_probe_kernel(double* out, int iters, double a, double b) {
   double c[8][2];

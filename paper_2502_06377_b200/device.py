@@ -256,6 +256,26 @@ class DeviceSolver:
                 return out
         return host
 
+    def sigma_view(self):
+        """Zero-copy CUDA tensor over the context's Σ (p × p view of the p × ld buffer, in
+        the context's own index order).  For sizes where a copy does not fit next to the
+        solve (c5: 34 GB); valid until ``close`` and only after the context's stream is
+        synchronised."""
+        import torch
+
+        if self.perm is not None:
+            raise ValueError("sigma_view is in the relabelled order; use sigma() for permuted partitions")
+        ptr, r, c, ld = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+        _abi.check(self._L.ibmi_export(self._h, 1, 0, C.byref(ptr), C.byref(r), C.byref(c), C.byref(ld)), "export")
+        torch.cuda.synchronize(self.device)
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(r.value), int(c.value)), "typestr": "<f8",
+                                        "data": (int(ptr.value), False), "strides": (int(ld.value) * 8, 8),
+                                        "version": 3}
+
+        return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
     def block_update(self, k: int):
         _abi.check(self._L.ibmi_block_update(self._h, int(k)), "block_update")
 

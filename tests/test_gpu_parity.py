@@ -147,6 +147,56 @@ def test_two_norm_zero_and_restart_paths():
     assert abs(two_norm.last_iterations - it_ref) <= 2
 
 
+@pytest.mark.parametrize("shape,seed", [((700, 1500), 6), ((1536, 900), 7), ((2048, 2048), 8), ((2100, 1800), 9),
+                                        ((2200, 2600), 10), ((1152, 7040), 11)])
+def test_two_norm_flag_exchange_kernel(shape, seed):
+    """Mid-size Gram matrices (640 < n ≤ 2220) run the flag-carrying line exchange
+    (power_gram_ll_kernel) instead of one grid barrier per iteration: same σ and
+    iteration count as the oracle and as the grid-barrier kernel (ibmi_tune key 13)."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import _abi
+    from paper_2502_06377_b200.linalg import two_norm
+
+    rng = np.random.default_rng(seed)
+    b = rng.standard_normal(shape) * np.exp(rng.uniform(-2, 2, size=(shape[0], 1)))
+    s = two_norm(b)
+    it = two_norm.last_iterations
+    s_ref, conv, it_ref = orc.power_sigma_max(b)
+    assert abs(s - s_ref) <= 1e-9 * s_ref
+    assert abs(it - it_ref) <= 2
+    _abi.check(_abi.lib().ibmi_tune(13, 0), "tune")
+    try:
+        s_bar = two_norm(b)
+        it_bar = two_norm.last_iterations
+    finally:
+        _abi.check(_abi.lib().ibmi_tune(13, 1), "tune")
+    assert abs(s - s_bar) <= 1e-12 * s_bar and abs(it - it_bar) <= 1
+
+
+@pytest.mark.parametrize("shape", [(800, 1024), (1500, 1024)])
+def test_two_norm_flag_exchange_restart_and_cap(shape):
+    """σ = 0 on the first iterate restarts from default_rng(0x5EED) inside the
+    flag-exchange kernel (linalg.py:237-244); the cap still warns.  Rows of dyadic
+    entries summing to zero over 1024 columns (1/√1024 is exact) make B·v₁ an exact 0
+    in both Gram forms (row Gram for 800 rows, column Gram for 1500)."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import NoConvergenceWarning
+    from paper_2502_06377_b200.linalg import two_norm
+
+    b = np.random.default_rng(12).standard_normal(shape)
+    b = b - b.mean(axis=1, keepdims=True)
+    b[:, -1] -= b.sum(axis=1)            # exact zero row sums up to rounding ...
+    b = np.round(b * 1024) / 1024        # ... made exact: dyadic entries
+    b[:, -1] -= b.sum(axis=1)
+    assert np.all(b.sum(axis=1) == 0.0)
+    s_ref, conv, it_ref = orc.power_sigma_max(b)
+    s = two_norm(b)
+    assert abs(s - s_ref) <= 1e-9 * s_ref
+    assert abs(two_norm.last_iterations - it_ref) <= 2
+    with pytest.warns(NoConvergenceWarning):
+        two_norm(np.random.default_rng(13).standard_normal(shape), rtol=1e-300, max_iters=4)
+
+
 def test_two_norm_warns_at_cap():
     from paper_2502_06377_b200 import NoConvergenceWarning
     from paper_2502_06377_b200.linalg import two_norm
@@ -354,6 +404,66 @@ def test_c4_first_sweeps_match_reference_and_converge():
         for _ in range(10):
             err, _, _ = ds.sweep(1e-9, 5000)
         assert err < 2e-6
+
+
+@pytest.mark.slow
+def test_c5_first_sweep_matches_oracle_fixture():
+    """c5 (p = 65536, 16 sets of 4608/5120) at full size: setup + the first sweep
+    against the fixture the CPU oracle produced on the GPU box's host
+    (tools/make_c5_fixture.py: 16 block updates + the estimate in solve()'s order,
+    ~20 min of 16 cores).  Σ is compared through a seeded Gaussian sketch Σ·R
+    (E‖XR‖_F² = cols·‖X‖_F²: an estimate of the full relative Frobenius distance),
+    its row sums, ‖Σ‖_F and 4096 sampled entries, all at 1e-10."""
+    from paper_2502_06377_b200 import configs
+    from paper_2502_06377_b200.device import DeviceSolver
+
+    g = golden("c5.npz")
+    free, _total = torch.cuda.mem_get_info()
+    if free < 150e9:
+        pytest.skip("c5 needs ~120 GB of HBM")
+    cfg = configs.get_config("c5")
+    p = cfg.p
+    a_dev = configs.make_matrix_c5_device(0)
+    chk = np.array([float(a_dev.sum()), float(torch.linalg.norm(a_dev)), float(a_dev[0, 0]), float(a_dev[-1, -1]),
+                    float(a_dev[123, 45678])])
+    assert np.allclose(chk, g["a_checksum"], rtol=1e-12, atol=0.0), (chk, g["a_checksum"])
+    ds = DeviceSolver(a_dev, partition=cfg.partition())
+    del a_dev
+    torch.cuda.empty_cache()
+    try:
+        ds.setup()
+        ds.init_sigma(0)
+        err, pit, conv = ds.sweep(1e-9, 5000)
+        ref_err = float(g["error_trace"][0])
+        assert abs(err - ref_err) <= 1e-6 * ref_err + 5e-2 * cfg.tol, (err, ref_err)
+        assert abs(pit - int(g["power_iters"][0])) <= 2
+        s = ds.sigma_view()
+        assert s.shape == (p, p)
+        r = torch.as_tensor(np.random.default_rng(2025).standard_normal((p, g["sweep1_sketch"].shape[1])),
+                            device=s.device)
+        sk = torch.empty((p, r.shape[1]), dtype=torch.float64, device=s.device)
+        rs = torch.empty(p, dtype=torch.float64, device=s.device)
+        fro2 = 0.0
+        for lo in range(0, p, 4096):
+            blk = s[lo:lo + 4096]
+            sk[lo:lo + 4096] = blk @ r
+            rs[lo:lo + 4096] = blk.sum(dim=1)
+            fro2 += float((blk * blk).sum())
+        ref_fro = float(g["sweep1_fro"][0])
+        assert rel_fro(sk.cpu().numpy(), g["sweep1_sketch"]) < 1e-10
+        assert np.linalg.norm(rs.cpu().numpy() - g["sweep1_rowsum"]) <= 1e-10 * ref_fro * np.sqrt(p)
+        assert abs(fro2 ** 0.5 - ref_fro) <= 1e-10 * ref_fro
+        si = torch.as_tensor(g["sample_i"], device=s.device)
+        sj = torch.as_tensor(g["sample_j"], device=s.device)
+        assert rel_fro(s[si, sj].cpu().numpy(), g["sweep1_sample"]) < 1e-10
+        # symmetric to the bit on sampled pairs
+        assert torch.equal(s[si, sj], s[sj, si])
+    finally:
+        ds.close()
+        from paper_2502_06377_b200 import _abi
+
+        _abi.lib().ibmi_release_cached_memory(-1)
+        torch.cuda.empty_cache()
 
 
 def test_solve_overlapping_noncontiguous_matches_oracle():

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--exchange", default="auto")
 ap.add_argument("--sweeps", type=int, default=3)
+ap.add_argument("--operands", default="auto")
 args = ap.parse_args()
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
 os.environ.setdefault("MASTER_PORT", "29541")
@@ -28,7 +29,8 @@ cfg = configs.get_config(args.config)
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 a = torch.as_tensor(configs.make_matrix(args.config), device="cuda")
-ss = ShardedSolver(a, cfg.partition(), exchange=args.exchange)
+ss = ShardedSolver(a, cfg.partition(), exchange=args.exchange, operands=args.operands)
+print("operands", ss.operands, "exchange", ss.exchange, flush=True)
 ss.init_sigma(cfg.guess if cfg.guess in ("identity", "jacobi") else "identity")
 ss.sweep()
 torch.cuda.synchronize()
