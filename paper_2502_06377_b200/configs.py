@@ -11,11 +11,14 @@ bit-identical matrices:
   (2, 0), (8, .125), (8, .125), (16, .125) (B1);
 * Σ₀ is ``diag(1/A_ii)`` on c1/c2 (guess ``"jacobi"``), identity otherwise (B3);
 * stopping: c1 estimate ≤ 1e-10, c2 ``‖I − AΣ‖_F < 1e-9``, c3/c5 estimate ≤ 1e-8 (B4);
-  c4 estimate ≤ 1e-5: the reference default 1e-8 lies below this problem's
-  FP64 floor (measured on the GPU: the estimate converges ×0.46 per sweep and
-  then stays at 9.47e-7, ‖I − AΣ‖_F at 2.37e-6, from sweep ~22 to 120+;
-  tools/trace_config.py), so 1e-8 is unreachable in double precision by any
-  evaluation order;
+  c4 estimate ≤ 1e-7: the reference default 1e-8 lies below this problem's FP64 floor
+  for the REFERENCE ITSELF — its own CPU run (tests/golden/c4long.json, 30 sweeps)
+  converges ×0.46 per sweep and then stays at 3.30e-8 (‖I − AΣ‖_F at 4.47e-7) from
+  sweep 26 on, so it never reports convergence at 1e-8.  1e-7 is three times above that
+  floor; the reference crosses it at sweep 24 (8.96e-8) and so does the GPU path
+  (9.03e-8; its floor is 2.2e-8).  Round 1 pinned 1e-5 because the GPU path then
+  stalled at 9.5e-7 — an artefact of forming A_II⁻¹ as the product L⁻ᵀ·L⁻¹, fixed in
+  round 2 (DESIGN.md §4);
 * ``max_iterations`` 1500 on c2, 500 otherwise (B5).
 
 No public dataset is involved: BASELINE's own recipes are the benchmark
@@ -59,7 +62,7 @@ CONFIGS = {
                         "p=4096 A=Q diag(10^U(0,3)) Q^T; 2 blocks 2048/2048; until ||I-A Sigma||_F<1e-9"),
     "c3": ProblemConfig("c3", 8192, 8, 0.125, "identity", 1e-8, "estimate", 500,
                         "p=8192 SE kernel l=0.1 on x-sorted U[0,1]^2 points + 1e-2 I; 8 blocks 1152/1280, overlap 256"),
-    "c4": ProblemConfig("c4", 16384, 8, 0.125, "identity", 1e-5, "estimate", 500,
+    "c4": ProblemConfig("c4", 16384, 8, 0.125, "identity", 1e-7, "estimate", 500,
                         "p=16384 Matern-3/2 l=0.2 on x-sorted U[0,1]^3 points + 1e-3 I; 8 blocks 2304/2560, overlap 512"),
     "c5": ProblemConfig("c5", 65536, 16, 0.125, "identity", 1e-8, "estimate", 500,
                         "p=65536 A=B B^T/p + 0.5 I, B standard normal; 16 blocks 4608/5120, overlap 1024"),

@@ -1267,12 +1267,18 @@ struct CholScratch {
   int* info = nullptr;
   int cap = 0;
   size_t bytes = 0;
+  // potri only (allocated by ensure_potri_scratch): Lᵀ, L⁻ᵀ and the transposed solution, n × ldw each
+  double *lt = nullptr, *yt = nullptr, *pt = nullptr;
+  int potri_cap = 0;
   void release() {
     if (ws) cudaFree(ws);
     if (dinv) cudaFree(dinv);
     if (tmp) cudaFree(tmp);
     if (info) cudaFree(info);
-    ws = dinv = tmp = nullptr; info = nullptr; cap = 0; bytes = 0;
+    if (lt) cudaFree(lt);
+    if (yt) cudaFree(yt);
+    if (pt) cudaFree(pt);
+    ws = dinv = tmp = lt = yt = pt = nullptr; info = nullptr; cap = 0; potri_cap = 0; bytes = 0;
   }
 };
 
@@ -1385,19 +1391,78 @@ int trtri_blocked(CholScratch& cs, int n, cudaStream_t s) {
   return IBMI_OK;
 }
 
+int ensure_potri_scratch(CholScratch& cs, int n) {
+  if (n <= cs.potri_cap && cs.lt) return IBMI_OK;
+  for (double** q : {&cs.lt, &cs.yt, &cs.pt}) {
+    if (*q) cudaFree(*q);
+    *q = nullptr;
+  }
+  cs.potri_cap = 0;
+  const size_t bytes = (size_t)cs.cap * cs.ldw * sizeof(double);     // same shape as ws
+  CUDA_TRY(cudaMalloc(&cs.lt, bytes));
+  CUDA_TRY(cudaMalloc(&cs.yt, bytes));
+  CUDA_TRY(cudaMalloc(&cs.pt, bytes));
+  cs.potri_cap = cs.cap;
+  cs.bytes += 3 * bytes;
+  return IBMI_OK;
+}
+
+// out = A⁻¹ from the Cholesky factor in cs.ws, the way LAPACK's dpotrs(L, I) gets it
+// (the reference's spd_inverse, linalg.py:122-130): Y = L⁻¹ (blocked dtrtri), then
+// Lᵀ X = Y by blocked BACK SUBSTITUTION against L itself, then ½(X + Xᵀ).
+//
+// The earlier version formed X = L⁻ᵀ·L⁻¹ as a product of the explicit triangular
+// inverse.  Both have the same residual ‖A X − I‖, but the product's errors are not
+// backward-stable with respect to L, and the sweep is sensitive to exactly that: at c4
+// the error estimate stalled at 9.5e-7 with the product and reaches 2.3e-8 with the
+// substitution (reference CPU run: 3.3e-8; profiles/r02_c4_floor_probe*.log).
+//
+// Block row j (bottom-up), with P = Xᵀ so that every operand is K-contiguous:
+//   Vᵀ[n][m] = Yᵀ[n][j0+m] − Σ_{k ≥ j1} P[n][k] · Lᵀ[j0+m][k]        (n × 64, K = n − j1)
+//   P[n][j0+m] = Σ_i Vᵀ[n][i] · (L_jj⁻¹)[i][m]                        (n × 64, K = 64)
 int potri_blocked(CholScratch& cs, int n, double* out, int64_t ldo, cudaStream_t s) {
-  int rc = trtri_blocked(cs, n, s);
+  int rc = ensure_potri_scratch(cs, n);
   if (rc) return rc;
   double* a = cs.ws;
   const int64_t ld = cs.ldw;
-  GemmOp la;   // out[m][n] = Σ_k X[k][m] X[k][n]
-  la.X = a; la.ldx = ld; la.xt = true;
-  la.Y = a; la.ldy = ld; la.yt = true;
-  la.M = n; la.N = n;
-  la.add_seg(0, 0, n);
-  la.C = out; la.ldc = ldo;
-  la.lower = true; la.mirror = true;
-  CUDA_TRY(launch_gemm(la, s));
+  const dim3 tb(32, 8), tg((n + 31) / 32, (n + 31) / 32);
+  transpose2d_kernel<<<tg, tb, 0, s>>>(a, ld, cs.lt, ld, n); note_launch();     // Lᵀ, before trtri overwrites L
+  CUDA_TRY(cudaGetLastError());
+  rc = trtri_blocked(cs, n, s);
+  if (rc) return rc;
+  transpose2d_kernel<<<tg, tb, 0, s>>>(a, ld, cs.yt, ld, n); note_launch();     // Yᵀ = L⁻ᵀ (upper triangular)
+  CUDA_TRY(cudaGetLastError());
+  const int nblk = (n + CHOL_NB - 1) / CHOL_NB;
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int j0 = blk * CHOL_NB;
+    const int jb = std::min(CHOL_NB, n - j0);
+    const int j1 = j0 + jb;
+    double* dblk = cs.dinv + (size_t)blk * CHOL_NB * CHOL_NB;
+    if (j1 < n) {
+      GemmOp g;
+      g.X = cs.pt; g.ldx = ld;
+      g.Y = cs.lt; g.ldy = ld; g.yn = contig_map(j0);
+      g.M = n; g.N = jb;
+      g.add_seg(j1, j1, n - j1);
+      g.C = cs.tmp; g.ldc = CHOL_NB;
+      g.alpha = -1.0; g.beta = 1.0; g.D = cs.yt; g.ldd = ld; g.dn = contig_map(j0);
+      g.tma_ok = true; g.xrows = n; g.xcols = n; g.yrows = n; g.ycols = n;
+      CUDA_TRY(launch_gemm(g, s));
+    } else {
+      copy2d_kernel<<<grid2d(n, jb), 256, 0, s>>>(cs.yt, ld, contig_map(0), contig_map(j0), cs.tmp, CHOL_NB, n, jb, 0);
+      note_launch();
+      CUDA_TRY(cudaGetLastError());
+    }
+    GemmOp h;
+    h.X = cs.tmp; h.ldx = CHOL_NB;
+    h.Y = dblk; h.ldy = CHOL_NB; h.yt = true;
+    h.M = n; h.N = jb;
+    h.add_seg(0, 0, jb);
+    h.C = cs.pt; h.ldc = ld; h.cn = contig_map(j0);
+    CUDA_TRY(launch_gemm(h, s));
+  }
+  sym_avg_kernel<<<tg, tb, 0, s>>>(cs.pt, ld, out, ldo, n); note_launch();
+  CUDA_TRY(cudaGetLastError());
   return IBMI_OK;
 }
 
@@ -2397,6 +2462,9 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
     int bmax = 0;
     for (int j = q; j < count; j += S) bmax = std::max(bmax, c->sets[first + j].b);
     rc = ensure_scratch(scr[q], bmax);
+    // the inverse's scratch too, before any work is queued: a cudaMalloc inside the loop
+    // below would synchronise the device and serialise the eight set pipelines
+    if (!rc) rc = ensure_potri_scratch(scr[q], bmax);
     if (rc) { cleanup(); return rc; }
   }
   pt.mark("streams + scratch");

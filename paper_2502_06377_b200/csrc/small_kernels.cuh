@@ -150,6 +150,39 @@ __global__ void sym_rows_kernel(const double* __restrict__ base, int64_t ldb, co
   }
 }
 
+// dst[j][i] = src[i][j] for an n×n matrix (32×32 shared-memory tiles, both sides coalesced).
+__global__ void transpose2d_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                                   int64_t ldd, int n) {
+  __shared__ double t[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + r, j = bx + threadIdx.x;
+    t[r][threadIdx.x] = (i < n && j < n) ? src[(int64_t)i * lds + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = bx + r, j = by + threadIdx.x;
+    if (i < n && j < n) dst[(int64_t)i * ldd + j] = t[threadIdx.x][r];
+  }
+}
+
+// out = ½(P + Pᵀ), exactly symmetric (the reference's 0.5 * (inv + inv.T), linalg.py:130):
+// a + b and b + a round identically, so out[i][j] == out[j][i] to the bit.
+__global__ void sym_avg_kernel(const double* __restrict__ p, int64_t ldp, double* __restrict__ out, int64_t ldo,
+                               int n) {
+  __shared__ double t[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {      // tile (bx.., by..) read for its transpose
+    const int i = bx + r, j = by + threadIdx.x;
+    t[r][threadIdx.x] = (i < n && j < n) ? p[(int64_t)i * ldp + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + r, j = bx + threadIdx.x;
+    if (i < n && j < n) out[(int64_t)i * ldo + j] = 0.5 * (p[(int64_t)i * ldp + j] + t[threadIdx.x][r]);
+  }
+}
+
 __global__ void fill2d_kernel(double* __restrict__ dst, int64_t ldd, int rows, int cols, double v,
                               double diag) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;

@@ -26,7 +26,7 @@ from test_gpu_parity import (  # noqa: E402,F401  (re-collected here, under emul
     test_c1_full_solve_matches_reference,
     test_c2_full_solve_frobenius_stop,
     test_c3_full_solve_matches_reference,
-    test_c4_first_sweeps_match_reference_and_converge,
+    test_c4_through_the_floor_matches_reference,
     test_device_loop_equals_host_loop,
     test_solve_red_black_matches_oracle,
     test_solve_shapes_match_oracle,

@@ -52,6 +52,18 @@ def check_trace(errs, ref_errs, tol):
         assert near and abs(len(errs) - len(ref_errs)) <= 1, (len(errs), len(ref_errs))
 
 
+def check_sketch(sigma, g, key, tol=1e-10):
+    """‖(Σ − Σ_ref)·R‖_F / ‖Σ_ref·R‖_F with the seeded Gaussian R of make_golden.sketch_matrix:
+    an unbiased estimate of the full relative Frobenius distance (E‖XR‖_F² = cols·‖X‖_F²),
+    from a fixture of p × cols doubles instead of p²; plus ‖Σ‖_F and the row sums."""
+    ref = g[f"{key}_sketch"]
+    r = np.random.default_rng(2025).standard_normal((sigma.shape[0], ref.shape[1]))
+    assert rel_fro(sigma @ r, ref) < tol
+    fro = float(g[f"{key}_fro"][0])
+    assert abs(np.linalg.norm(sigma) - fro) <= tol * fro
+    assert np.linalg.norm(sigma.sum(axis=1) - g[f"{key}_rowsum"]) <= tol * fro * np.sqrt(sigma.shape[0])
+
+
 # ----------------------------------------------------------------- kernels
 @pytest.mark.parametrize("m,n,k", [(128, 128, 16), (256, 384, 512), (1, 1, 1), (129, 77, 33), (300, 257, 1000),
                                    (1000, 64, 7), (5, 700, 300)])
@@ -348,6 +360,7 @@ def test_c2_full_solve_frobenius_stop():
     sample = rep.result[g["sample_i"], g["sample_j"]]
     assert rel_fro(sample, g["sample"]) < 1e-10
     assert rel_fro(np.diag(rep.result), g["diag"]) < 1e-10
+    check_sketch(rep.result, golden("c2_sketch.npz"), "final")
 
 
 def test_c3_full_solve_matches_reference():
@@ -363,47 +376,55 @@ def test_c3_full_solve_matches_reference():
     assert rel_fro(sample, g["sample"]) < 1e-10
     dr = np.linalg.norm(rep.result.sum(axis=1) - g["rowsum"])
     assert dr <= 1e-10 * float(g["fro"][0]) * np.sqrt(rep.result.shape[0])
+    check_sketch(rep.result, golden("c3_sketch.npz"), "final")
 
 
-def test_c4_first_sweeps_match_reference_and_converge():
-    """c4 (p=16384): first 3 sweeps against the reference snapshots, then the
-    size-independent properties at convergence (exact symmetry, ‖I−AΣ‖_F small,
-    monotone error decay)."""
-    import paper_2502_06377_b200 as pkg
+def test_c4_through_the_floor_matches_reference():
+    """c4 (p=16384) against the reference's own 30-sweep CPU run (tests/golden/c4long.npz,
+    generated by make_golden.py c4long from the reference package): the whole error
+    trajectory down to the FP64 floor, the sweep at which tol is met, and Σ at seven
+    checkpoints through a Gaussian sketch, row sums, ‖Σ‖_F and sampled entries at 1e-10.
+
+    The reference stalls at 3.30e-8 (never reaching its default tol 1e-8); c4's tol is
+    pinned at 1e-7 (configs.py), which the reference meets at sweep 24."""
     from paper_2502_06377_b200 import configs
     from paper_2502_06377_b200.device import DeviceSolver
 
-    g = golden("c4.npz")
+    g = golden("c4long.npz")
     cfg = configs.get_config("c4")
+    assert cfg.tol == 1e-7
     a = configs.make_matrix("c4")
-    part = cfg.partition()
-    with DeviceSolver(a, partition=part) as ds:
+    ref = g["error_trace"]
+    cps = {int(c) for c in g["checkpoints"]}
+    r = np.random.default_rng(2025).standard_normal((cfg.p, g["snap3_sketch"].shape[1]))
+    errs = []
+    with DeviceSolver(a, partition=cfg.partition()) as ds:
         ds.setup()
         ds.init_sigma(0)
-        for it in (1, 2, 3):
-            err, _, _ = ds.sweep(1e-9, 5000)
-            assert band_ok(err, g["error_trace"][it - 1], cfg.tol)
-            s = ds.sigma()
-            assert rel_fro(s[g["sample_i"], g["sample_j"]], g[f"snap{it}_sample"]) < 1e-10
-            # ‖ΔΣ·1‖ ≤ √p ‖ΔΣ‖_F: necessary condition for rel. Frobenius ≤ 1e-10
-            dr = np.linalg.norm(s.sum(axis=1) - g[f"snap{it}_rowsum"])
-            assert dr <= 1e-10 * float(g[f"snap{it}_fro"][0]) * np.sqrt(s.shape[0])
-            assert abs(np.linalg.norm(s) - float(g[f"snap{it}_fro"][0])) <= 1e-10 * float(g[f"snap{it}_fro"][0])
-        errs = []
-        for _ in range(cfg.max_iterations):
-            err, _, _ = ds.sweep(1e-9, 5000)
+        for it in range(1, len(ref) + 1):
+            err, pit, _ = ds.sweep(1e-9, 5000)
             errs.append(err)
-            if err <= cfg.tol:
-                break
-        assert errs[-1] <= cfg.tol and len(errs) < 40
-        s = ds.sigma()
-        assert np.array_equal(s, s.T)
+            if ref[it - 1] > 5e-8:          # above the floor the estimates agree inside the B7 band
+                assert band_ok(err, ref[it - 1], cfg.tol), (it, err, ref[it - 1])
+            if it in cps:
+                s = ds.sigma()
+                fro = float(g[f"snap{it}_fro"][0])
+                assert rel_fro(s @ r, g[f"snap{it}_sketch"]) < 1e-10, it
+                assert rel_fro(s[g["sample_i"], g["sample_j"]], g[f"snap{it}_sample"]) < 1e-10, it
+                assert np.linalg.norm(s.sum(axis=1) - g[f"snap{it}_rowsum"]) <= 1e-10 * fro * np.sqrt(cfg.p), it
+                assert abs(np.linalg.norm(s) - fro) <= 1e-10 * fro, it
+                if it == len(ref):
+                    assert np.array_equal(s, s.T)
+                del s
         fr = ds.frobenius()
-        assert fr < 1e-4
-        # past convergence the estimate sits on its FP64 floor (~9.5e-7), below tol
-        for _ in range(10):
-            err, _, _ = ds.sweep(1e-9, 5000)
-        assert err < 2e-6
+    errs = np.array(errs)
+    # same sweep count to tol as the reference (24)
+    n_gpu = int(np.argmax(errs <= cfg.tol)) + 1
+    n_ref = int(np.argmax(ref <= cfg.tol)) + 1
+    assert n_ref == 24 and n_gpu == n_ref, (n_gpu, n_ref)
+    # the floor: the reference sits at 3.30e-8 / ‖I − AΣ‖_F = 4.47e-7; not worse than 1.5x that
+    assert np.all(errs[25:] < 1.5 * ref[25:].max()), errs[25:]
+    assert fr < 1.5 * float(g["snap30_frobenius"][0]), fr
 
 
 @pytest.mark.slow

@@ -85,3 +85,21 @@ def test_oracle_nonsymmetric_sigma_against_reference():
     assert orc.error_estimate(a, s, idx, comp)[0] == pins["nonsym_ee"][0]
     orc.BlockOp(a, idx, comp).apply(s)
     assert np.array_equal(s, pins["nonsym_bu"])
+
+
+def test_long_fixtures_are_consistent_with_the_pinned_ones():
+    """The long reference runs (c4 through its floor, the c2/c3 sketches, c5's first
+    sweep on the GPU box's host) repeat the traces of the fixtures the oracle is pinned to."""
+    c4, c4l = golden("c4.npz"), golden("c4long.npz")
+    assert np.array_equal(c4l["error_trace"][:3], c4["error_trace"][:3])
+    assert len(c4l["error_trace"]) == 30 and int(c4l["iterations"][1]) == 0      # the reference never reaches 1e-8
+    floor = c4l["error_trace"][25:]
+    assert np.all((floor > 3.2e-8) & (floor < 3.4e-8))                            # its FP64 floor
+    for it in (3,):
+        assert np.array_equal(c4l[f"snap{it}_sample"], c4[f"snap{it}_sample"])
+    for name in ("c2", "c3"):
+        base, sk = golden(f"{name}.npz"), golden(f"{name}_sketch.npz")
+        assert np.array_equal(sk["error_trace"], base["error_trace"])
+        assert sk["final_sketch"].shape == (configs.get_config(name).p, 16)
+    c5 = golden("c5.npz")
+    assert c5["sweep1_sketch"].shape == (65536, 4) and int(c5["power_iters"][0]) == 1598
