@@ -179,6 +179,13 @@ class CudaBackend:
                 out[:n, :p] = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)[rows, :]))
         return out[:n, :p] if n else out[:0, :p]
 
+    def transposed(self, t):
+        """Contiguous transpose of a 2-D device tensor, rows padded to 32 doubles (TMA alignment)."""
+        r, c = t.shape
+        out = self.torch.zeros((max(c, 1), -(-max(r, 1) // 32) * 32), dtype=self.torch.float64, device=self.device)
+        out[:c, :r] = t.t()
+        return out[:c, :r]
+
     def spd_inverse(self, blk):
         """A_II⁻¹ on the device (linalg.py:122-130): symmetric check (linalg.py:68-77),
         blocked Cholesky + inverse; raises NotPositiveDefinite(index) like the reference."""
@@ -503,6 +510,7 @@ class ShardedSolver:
 
             raise DimensionMismatch(f"expected a square matrix, got shape {tuple(a.shape)}")
         self.A = be.upload_rows(a, self.own)                      # n_loc × p view, padded ld
+        self.AT = be.transposed(self.A)                           # p × n_loc: the column panel A[:, own_g], K-contiguous
         self.ld = -(-p // 32) * 32
         # (1) this rank's inverses; every rank learns every outcome before anyone raises
         mine, status = {}, []
@@ -727,11 +735,12 @@ class ShardedSolver:
             B = self._bbuf(b, c)
             B.zero_()
             if self.n_loc:
-                for col0, n, out0 in ((0, lo, 0), (hi, p - hi, lo)):
-                    if n > 0:
-                        be.gemm(GemmSpec(x=self.S, xm=lo, y=self.A, yn=col0, m=b, n=n, segs=[(0, 0, self.n_loc)],
-                                         c=B, cm=0, cn=out0, xt=True, yt=True, xrows=self.n_loc, xcols=p,
-                                         yrows=self.n_loc, ycols=p))
+                # both operands K-contiguous (K = local rows): Σ[own_g, I]ᵀ is transposed per call
+                # (b × n_loc, small), A[own_g, c]ᵀ = rows c of the static column panel AT
+                sit = be.transposed(self.S[: self.n_loc, lo:hi])
+                be.gemm(GemmSpec(x=sit, xm=0, y=self.AT, yn=(lo, 0, hi), m=b, n=c, segs=[(0, 0, self.n_loc)],
+                                 c=B, cm=0, cn=0, tma_safe=True, xrows=b, xcols=self.n_loc, yrows=p,
+                                 ycols=self.n_loc))
             self.comm.all_reduce(B)
             return be.two_norm(B, rtol, max_iters)
         Bloc = be.zeros(max(a1 - a0, 1), c)[: a1 - a0]

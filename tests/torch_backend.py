@@ -33,6 +33,9 @@ class TorchCPUBackend:
     def upload_rows(self, a, rows):
         return torch.as_tensor(np.asarray(a, dtype=np.float64)[np.asarray(rows, dtype=np.int64), :].copy())
 
+    def transposed(self, t):
+        return t.t().contiguous()
+
     def spd_inverse(self, blk):
         return torch.as_tensor(orc.spd_inverse(np.asarray(blk, dtype=np.float64)))
 
