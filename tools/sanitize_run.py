@@ -22,4 +22,22 @@ part = pkg.load_partition_json({"p": 256, "sets": [np.sort(perm[:150]).tolist(),
 pkg.solve(a, part, pkg.IbmiConfig(tol=1e-300, max_iterations=2, initial_guess="mc", mc_samples=20))
 linalg.spd_inverse(random_spd(200, 4))
 linalg.two_norm(np.random.default_rng(0).standard_normal((700, 900)))
+linalg.two_norm(np.random.default_rng(1).standard_normal((1300, 800)))       # column-Gram form, flag-exchange kernel
+# the sharded driver's kernels (ibmi_gemm descriptors, ibmi_sym_rows) at world size 1, both operand modes
+import torch.distributed as dist  # noqa: E402
+
+from paper_2502_06377_b200.distributed import ShardedSolver  # noqa: E402
+
+os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+os.environ.setdefault("MASTER_PORT", "29577")
+dist.init_process_group("gloo", rank=0, world_size=1)
+for operands in ("replicated", "sharded"):
+    a = random_spd(520, 5)
+    ss = ShardedSolver(a, pkg.contiguous_partition(520, 4, 0.125), panel=64, device=0, exchange="nccl",
+                       operands=operands)
+    ss.init_sigma("jacobi")
+    ss.sweep()
+    ss.frobenius()
+    ss.close()
+dist.destroy_process_group()
 print("sanitize workload done")
