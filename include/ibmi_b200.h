@@ -323,7 +323,9 @@ long long ibmi_launch_count(void);
  * key 12: FP64 GEMM tile raster: bands of this many 128-row tile rows walked column by
  *         column (default 0 = tile-row-major);
  * key 13: power iteration of mid-size Gram matrices (512 <= n <= 2220) with the
- *         flag-carrying line exchange instead of a grid barrier per iteration (default 1). */
+ *         flag-carrying line exchange instead of a grid barrier per iteration (default 1);
+ * key 14: p <= 1024 (FP64 DMMA, contiguous sets): ibmi_sweep / ibmi_solve_loop run the K block updates,
+ *         the estimate matrix and its Gram form as one cooperative kernel (default 1). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libibmi_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", "ibmi_b200.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "gemm_nt.cuh", "gemm_tma.cuh", "small_kernels.cuh", "igemm_tc.cuh", "ozaki.cuh")] + [
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "gemm_nt.cuh", "gemm_tma.cuh", "small_kernels.cuh", "small_sweep.cuh", "igemm_tc.cuh", "ozaki.cuh")] + [
     os.path.join(ROOT, "include", "ibmi_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

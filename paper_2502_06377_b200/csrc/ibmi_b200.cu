@@ -29,6 +29,7 @@
 #include "gemm_nt.cuh"
 #include "gemm_tma.cuh"
 #include "small_kernels.cuh"
+#include "small_sweep.cuh"
 #include "igemm_tc.cuh"
 #include "ozaki.cuh"
 
@@ -266,6 +267,7 @@ int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
 int g_power_ll = 1;         // mid-size Gram power iteration with the flag-carrying exchange (no grid barrier)
+int g_small_fused = 1;      // p <= 1024: the whole sweep's GEMM phases in one cooperative kernel (small_sweep.cuh)
 int g_split_min_kt = 4;     // split-K keeps at least this many k-tiles per split
 int g_raster_group = 0;     // GEMM tile raster: bands of this many tile rows (0 = tm-major)
 int g_tune_gen = 0;         // bumped by ibmi_tune: captured graphs are re-captured
@@ -2020,9 +2022,10 @@ bool power_ll_launch(PowerParams& P, const NormBufs& nb, cudaStream_t st) {
 }
 
 int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, double rtol, int max_iters,
-                     const NormBufs& nb, cudaStream_t st, cudaEvent_t ev_gram = nullptr) {
+                     const NormBufs& nb, cudaStream_t st, cudaEvent_t ev_gram = nullptr, bool have_gram = false) {
   const int mode = (b <= cc) ? 0 : 1;
   const int64_t n = mode == 0 ? b : cc;
+  if (have_gram && mode != 0) return fail(IBMI_ERR_INVALID, "precomputed Gram matrix needs the row form");
   GemmOp gg;
   if (mode == 0) {   // G = B Bᵀ
     gg.X = Bm; gg.ldx = ldB;
@@ -2041,7 +2044,9 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
   const bool emu = mode == 0 && nb.oz && nb.oz_n > 0 && n <= 65535 && n <= nb.oz->ex_cap &&
                    (int64_t)nb.oz_n * n * round_up(n, 16) <= nb.oz->rq_cap &&
                    (int64_t)nb.oz_n * n * round_up(cc, 16) <= nb.oz->xq_cap;
-  if (emu) {
+  if (have_gram) {
+    // G and y₁ were written by the fused small-problem sweep kernel
+  } else if (emu) {
     // G = B Bᵀ: X and Y are the same rows, one conversion serves both
     OzPre same;
     same.q = nb.oz->xq;
@@ -2056,7 +2061,7 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
     }
     CUDA_TRY(launch_gemm(gg, st));
   }
-  if (mode == 0) {
+  if (mode == 0 && !have_gram) {
     const int threads = 256;
     const int blocks = (int)((b * 32 + threads - 1) / threads);
     rowsum_scaled_kernel<<<blocks, threads, 0, st>>>(Bm, ldB, (int)b, (int)cc, 1.0 / std::sqrt((double)cc), nb.vec); note_launch();
@@ -2733,7 +2738,53 @@ int ibmi_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, double* 
   return read_power(c, err, iters, conv);
 }
 
+// ---- small problems: the sweep's GEMM phases as one cooperative kernel (small_sweep.cuh)
+bool small_fused_ok(const ibmi_ctx* c) {
+  if (!g_small_fused || c->oz_n > 0 || c->p > 1024 || c->sets.empty() || (int)c->sets.size() > SS_MAX_SETS) return false;
+  for (const SetDev& s : c->sets)
+    if (s.general || !s.ready) return false;
+  const SetDev& last = c->sets.back();
+  return last.b <= c->p - last.b && c->Bm && c->Gm && c->vec && c->vr_n == c->p - last.b;
+}
+
+// All K block updates and, with `estimate`, B, G = B·Bᵀ and y₁ of the last set; then the power iteration.
+// ev (optional): [0] after the fused kernel, [1] after the power iteration.
+int enqueue_small_sweep(ibmi_ctx* c, double rtol, int max_iters, cudaEvent_t* ev, bool copy_out) {
+  static bool attr[64] = {false};
+  if (!attr[c->device & 63]) {
+    CUDA_TRY(cudaFuncSetAttribute(small_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SS_SMEM));
+    attr[c->device & 63] = true;
+  }
+  SmallSweepParams P;
+  memset(&P, 0, sizeof(P));
+  P.S = c->S; P.A = c->A; P.ld = c->ld; P.p = (int)c->p; P.K = (int)c->sets.size();
+  int tiles = 1;
+  for (int k = 0; k < P.K; ++k) {
+    const SetDev& s = c->sets[k];
+    P.set[k] = SmallSet{(int)s.lo, (int)s.hi, s.W, s.ainv, s.ldb};
+    const int ntm = (s.b + SS_TILE - 1) / SS_TILE, ntn = (int)((c->p - s.b + SS_TILE - 1) / SS_TILE);
+    tiles = std::max(tiles, ntm * ntn);
+  }
+  P.estimate = 1;
+  P.B = c->Bm; P.ldB = c->ldB; P.G = c->Gm; P.ldG = c->ldG; P.y1 = c->vec;
+  const int grid = std::min(tiles, c->sms);
+  void* args[] = {&P};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)small_sweep_kernel, dim3(grid), dim3(SS_THREADS), args, SS_SMEM,
+                                       c->stream));
+  note_launch();
+  if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
+  const SetDev& last = c->sets.back();
+  NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,
+              c->power_smem_cap, c->splitws, c->splitws_cap, c->sms};
+  int rc = enqueue_two_norm(c->Bm, c->ldB, last.b, c->p - last.b, rtol, max_iters, nb, c->stream, nullptr, true);
+  if (rc) return rc;
+  if (ev) CUDA_TRY(cudaEventRecord(ev[1], c->stream));
+  if (copy_out) CUDA_TRY(cudaMemcpyAsync(c->hpin, c->dscal, 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  return IBMI_OK;
+}
+
 static int enqueue_sweep(ibmi_ctx* c, double rtol, int max_iters) {
+  if (small_fused_ok(c)) return enqueue_small_sweep(c, rtol, max_iters, nullptr, true);
   for (int k = 0; k < (int)c->sets.size(); ++k) {
     int rc = enqueue_block_update(c, k);
     if (rc) return rc;
@@ -2797,6 +2848,28 @@ int ibmi_sweep_timed(ibmi_ctx* c, double rtol, int max_iters, double* err, int* 
   for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
   float t[6] = {0, 0, 0, 0, 0, 0};
   CUDA_TRY(cudaEventRecord(ev[0], c->stream));
+  {
+    const SetDev& last = c->sets.back();
+    rc = ensure_estimate_buffers(c, last.b, c->p - last.b);
+    if (rc) return rc;
+  }
+  if (small_fused_ok(c)) {
+    // fused small-problem sweep: times[0] = the fused kernel (all GEMM phases), times[4] = power iteration
+    rc = enqueue_small_sweep(c, rtol, max_iters, &ev[1], true);
+    if (rc) return rc;
+    rc = read_power(c, err, iters, conv);
+    if (rc) return rc;
+    float ms;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+    t[0] = ms;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+    t[4] = ms;
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[2]));
+    t[5] = ms;
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (times) memcpy(times, t, sizeof(t));
+    return IBMI_OK;
+  }
   for (int k = 0; k < K; ++k) {
     rc = enqueue_block_update(c, k, ev[1 + 2 * k]);
     if (rc) return rc;
@@ -2872,6 +2945,7 @@ int frontier(cudaStream_t st, std::vector<cudaGraphNode_t>& out) {
 }
 
 int enqueue_sweep_body(ibmi_ctx* c, double rtol, int max_iters) {
+  if (small_fused_ok(c)) return enqueue_small_sweep(c, rtol, max_iters, nullptr, false);
   for (int k = 0; k < (int)c->sets.size(); ++k) {
     int rc = enqueue_block_update(c, k);
     if (rc) return rc;
@@ -3577,6 +3651,9 @@ int ibmi_tune(int key, int value) {
       break;
     case 13:
       g_power_ll = value ? 1 : 0;
+      break;
+    case 14:
+      g_small_fused = value ? 1 : 0;
       break;
     case 12:
       if (value < 0 || value > 1024) return fail(IBMI_ERR_INVALID, "raster group must be in [0, 1024]");

@@ -645,6 +645,34 @@ def test_solve_shapes_match_oracle(p, k, f):
     assert np.array_equal(rep.result, rep.result.T)
 
 
+@pytest.mark.parametrize("p,k,f", [(512, 2, 0.0), (9, 4, 0.0), (300, 3, 0.1), (777, 5, 0.2), (1024, 8, 0.125),
+                                   (1000, 2, 0.3)])
+def test_fused_small_sweep_equals_unfused(p, k, f):
+    """p ≤ 1024: the sweep's GEMM phases run as one cooperative kernel (small_sweep.cuh,
+    ibmi_tune key 14).  Same Σ (≤ 1e-12 relative Frobenius), same error trace and sweep
+    count as the per-GEMM launches, and both match the oracle."""
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import _abi
+
+    a = random_spd(p, p + k)
+    part = pkg.contiguous_partition(p, k, f)
+    cfg = pkg.IbmiConfig(tol=1e-11, max_iterations=60)
+    fused = pkg.solve(a, part, cfg)
+    _abi.check(_abi.lib().ibmi_tune(14, 0), "tune")
+    try:
+        plain = pkg.solve(a, part, cfg)
+    finally:
+        _abi.check(_abi.lib().ibmi_tune(14, 1), "tune")
+    assert fused.iterations == plain.iterations and fused.converged == plain.converged
+    assert rel_fro(fused.result, plain.result) < 1e-12
+    np.testing.assert_allclose(fused.error_trace, plain.error_trace, rtol=1e-6, atol=1e-13)
+    assert np.array_equal(fused.result, fused.result.T)
+    o = orc.solve(a, part.sets, tol=1e-11, max_iterations=60)
+    assert abs(fused.iterations - o["iterations"]) <= 1
+    assert rel_fro(fused.result, o["result"]) < 1e-10
+
+
 @pytest.mark.parametrize("stopping", ["estimate", "frobenius"])
 def test_device_loop_equals_host_loop(stopping, monkeypatch):
     """The conditional-graph solve loop gives the host loop's sweeps bit for bit."""
