@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/ibmi_b200.h"
+#include <nvtx3/nvToolsExt.h>
 #include <cudaTypedefs.h>
 #include "gemm_nt.cuh"
 #include "gemm_tma.cuh"
@@ -383,6 +384,22 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path);
 
 // IBMI_PROFILE=1: device-synchronised phase timings of the host entry points
 // on stderr (diagnostic only; the syncs change nothing but timing).
+// NVTX ranges around the host-side phases (setup, block update k, estimate, sweep, solve loop)
+// so a timeline (nsys, ncu --nvtx) shows the algorithm's structure.  Header-only NVTX v3:
+// the calls are no-ops unless a tool injects itself; IBMI_NVTX=0 skips even those.
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) {
+    static int en = -1;
+    if (en < 0) { const char* e = getenv("IBMI_NVTX"); en = (e && e[0] == '0') ? 0 : 1; }
+    on = en != 0;
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() { if (on) nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 struct PhaseTimer {
   bool on;
   const char* fn;
@@ -1708,6 +1725,7 @@ bool ozg_ready(const ibmi_ctx* c, int k) {
 }
 
 int enqueue_block_update(ibmi_ctx* c, int k, cudaEvent_t mid = nullptr) {
+  NvtxRange nvtx_("block_update");
   if (ozg_ready(c, k)) return enqueue_block_update_ozg(c, k, mid);
   c->oz_s.valid = false;             // Σ changes outside the planes' bookkeeping
   const SetDev& s = c->sets[k];
@@ -2121,6 +2139,7 @@ void power_launch_shape(int device, int* blocks, int* threads, size_t* smem_cap)
 // ev (optional): [0] after the B GEMM, [1] after the Gram GEMM.
 int enqueue_error_estimate(ibmi_ctx* c, int k, double rtol, int max_iters, cudaEvent_t* ev = nullptr,
                            bool copy_out = true) {
+  NvtxRange nvtx_("error_estimate");
   const SetDev& s = c->sets[k];
   const int64_t p = c->p, b = s.b, cc = p - b;
   if (cc <= 0) return fail(IBMI_ERR_DIM, "set covers every index: empty complement");
@@ -2284,6 +2303,7 @@ int ibmi_destroy(ibmi_ctx* c) {
 }
 
 int ibmi_set_matrix(ibmi_ctx* c, const double* a, int64_t lda, int on_device) {
+  NvtxRange nvtx_("set_matrix");
   if (!c || !a) return fail(IBMI_ERR_INVALID, "null argument");
   if (lda < c->p) return fail(IBMI_ERR_DIM, "lda < p");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -2388,6 +2408,7 @@ int ibmi_set_partition_general(ibmi_ctx* c, int k, const int64_t* set_ptr, const
 }
 
 int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_pivot) {
+  NvtxRange nvtx_("ibmi_setup");
   if (!c) return fail(IBMI_ERR_INVALID, "null context");
   if (c) c->oz_s.valid = false;   // Σ (or W) changes outside the residue planes' bookkeeping
   if (!c->a_set) return fail(IBMI_ERR_STATE, "matrix not set");
@@ -2549,6 +2570,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
 }
 
 int ibmi_init_sigma(ibmi_ctx* c, int kind, const double* guess, int64_t ldg, int on_device) {
+  NvtxRange nvtx_("init_sigma");
   int rc = check_ready(c);
   if (c) c->oz_s.valid = false;   // Σ (or W) changes outside the residue planes' bookkeeping
   if (rc) return rc;
@@ -2669,6 +2691,7 @@ int ibmi_set_sigma(ibmi_ctx* c, const double* s, int64_t lds, int on_device) {
 }
 
 int ibmi_get_sigma(ibmi_ctx* c, double* out, int64_t ldo, int on_device) {
+  NvtxRange nvtx_("get_sigma");
   if (!c || !out) return fail(IBMI_ERR_INVALID, "null argument");
   if (ldo < c->p) return fail(IBMI_ERR_DIM, "ldo < p");
   CUDA_TRY(cudaSetDevice(c->device));
@@ -2793,6 +2816,7 @@ static int enqueue_sweep(ibmi_ctx* c, double rtol, int max_iters) {
 }
 
 int ibmi_sweep(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters, int* conv) {
+  NvtxRange nvtx_("ibmi_sweep");
   int rc = check_ready(c);
   if (rc) return rc;
   for (auto& s : c->sets)
@@ -2837,6 +2861,7 @@ int ibmi_sweep(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters,
 }
 
 int ibmi_sweep_timed(ibmi_ctx* c, double rtol, int max_iters, double* err, int* iters, int* conv, float* times) {
+  NvtxRange nvtx_("ibmi_sweep_timed");
   int rc = check_ready(c);
   if (rc) return rc;
   for (auto& s : c->sets)
@@ -3021,6 +3046,7 @@ int build_loop_graph(ibmi_ctx* c, const LoopState& L, double gate, double rtol, 
 int ibmi_solve_loop(ibmi_ctx* c, double tol, int max_sweeps, double rtol, int max_iters, int stopping, int* sweeps,
                     int* converged, double* err_trace, int* pow_iters, int* pow_conv, double* resid_trace,
                     double* sweep_ms) {
+  NvtxRange nvtx_("ibmi_solve_loop");
   int rc = check_ready(c);
   if (rc) return rc;
   for (auto& s : c->sets)
@@ -3103,6 +3129,7 @@ int ibmi_solve_loop(ibmi_ctx* c, double tol, int max_sweeps, double rtol, int ma
 extern "C" {
 
 int ibmi_frobenius_residual(ibmi_ctx* c, double* out) {
+  NvtxRange nvtx_("frobenius_residual");
   int rc = check_ready(c);
   if (rc) return rc;
   rc = enqueue_frobenius(c);

@@ -48,6 +48,10 @@ def _worker(rank, world, port, backend, case, out, exchange="nccl", operands="au
         ss = ShardedSolver(a, part, panel=panel, device=0, exchange=exchange, operands=operands)
         if operands == "sharded":
             assert ss.W is None and ss.A.shape[0] == ss.n_loc
+        if os.environ.get("IBMI_TEST_LATE_RANK") == str(rank):
+            import time
+
+            time.sleep(1.5)          # this rank seeds (and zeroes) its panel long after the others
         ss.init_sigma(guess)
         errs = [ss.sweep()[0] for _ in range(sweeps)]
         sig = ss.gather_sigma()
@@ -174,3 +178,22 @@ def test_sharded_operands_not_spd_raises_on_every_rank():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert sorted(res) == [(0, (72, 1)), (1, (72, 1))]
+
+
+def test_sharded_p2p_late_rank_cannot_wipe_peer_stores(monkeypatch):
+    """in the fused p2p exchange K1's epilogue stores −M into the OWNERS' panels.
+    A rank that zeroes its panel late (init_sigma) must not wipe stores of a rank that is
+    already sweeping: init_sigma ends with a barrier.  Rank 1 enters init_sigma 1.5 s late."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import contiguous_partition
+
+    monkeypatch.setenv("IBMI_TEST_LATE_RANK", "1")
+    case = ((520, 3, 0.1), 3, 64)
+    (p, k, f), sweeps, panel = case
+    res = _run(2, "gloo", case, "p2p", "sharded")
+    m = np.random.default_rng(p).standard_normal((p, p))
+    a = m.T @ m + p * np.eye(p)
+    o = orc.solve(a, contiguous_partition(p, k, f).sets, tol=1e-300, max_iterations=sweeps)
+    for rank, errs, sig, fr in res:
+        assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
+        np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-13)
