@@ -223,6 +223,15 @@ int ibmi_mc_guess(int64_t p, const double* a, int64_t lda, const double* w, int6
 int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* restart_v, double rtol,
                   int max_iters, double* sigma, int* iters, int* converged, void* stream);
 
+/* The same power iteration on a Gram matrix the caller already holds (rows <= cols):
+ * g = b·bᵀ (device rows × rows, full symmetric storage) and y1 = b·(1/√cols)·1 (device, rows).
+ * The sharded sweep forms g from per-rank partial products over column chunks of b and one
+ * all-reduce instead of a replicated rows² × cols product; b itself is only
+ * read on the σ = 0 restart path (linalg.py:237-244). */
+int ibmi_two_norm_gram(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* g, int64_t ldg,
+                       const double* y1, const double* restart_v, double rtol, int max_iters, double* sigma, int* iters,
+                       int* converged, void* stream);
+
 /* ---- composable pieces for the sharded (multi-GPU) sweep ---- */
 
 /* One-gap index map: logical i -> (i < split ? off0 + i : off1 + (i - split)),

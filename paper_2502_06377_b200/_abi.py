@@ -66,6 +66,8 @@ SIGNATURES = [
     ("ibmi_mc_guess", C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
     ("ibmi_two_norm", C.c_int, [_I64, _I64, _P, _I64, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), _P]),
+    ("ibmi_two_norm_gram", C.c_int, [_I64, _I64, _P, _I64, _P, _I64, _P, _D, C.c_double, C.c_int, _D,
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int), _P]),
     ("ibmi_gemm", C.c_int, [_P, _P]),
     ("ibmi_gemm_workspace", C.c_int, [_P, C.POINTER(_I64)]),
     ("ibmi_context_stream", C.c_int, [_P, C.POINTER(_P)]),

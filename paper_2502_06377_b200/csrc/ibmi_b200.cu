@@ -3422,6 +3422,44 @@ static RowMap to_map(const ibmi_map& m) {
   return r;
 }
 
+int ibmi_two_norm_gram(int64_t rows, int64_t cols, const double* b, int64_t ldb, const double* g, int64_t ldg,
+                       const double* y1, const double* restart_v, double rtol, int max_iters, double* sigma, int* iters,
+                       int* converged, void* stream) {
+  if (rows < 1 || cols < 1) return fail(IBMI_ERR_DIM, "matrix must be nonempty");
+  if (rows > cols) return fail(IBMI_ERR_DIM, "two_norm_gram needs rows <= cols (row Gram form)");
+  if (!b || !g || !y1 || !restart_v) return fail(IBMI_ERR_INVALID, "null pointer");
+  if (ldg < rows) return fail(IBMI_ERR_DIM, "ldg < rows");
+  if (max_iters < 1) return fail(IBMI_ERR_INVALID, "max_iters must be >= 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  NormCache& nc = g_norm[dev & 63];
+  std::lock_guard<std::mutex> lock(nc.mu);
+  if (!nc.blocks) {
+    power_launch_shape(dev, &nc.blocks, &nc.threads, &nc.smem_cap);
+    CUDA_TRY(cudaMalloc(&nc.part, (size_t)(4 + 32) * nc.blocks * sizeof(double)));   // partials + LL lines
+    CUDA_TRY(cudaMalloc(&nc.out, 4 * sizeof(double)));
+    CUDA_TRY(cudaMallocHost(&nc.host, 4 * sizeof(double)));
+  }
+  size_t dummy = 0;
+  if (ensure_buf(&nc.vec, &nc.vec_cap, 2 * std::max(rows, cols), &dummy)) return IBMI_ERR_OOM;
+  if (ensure_buf(&nc.vr, &nc.vr_cap, cols, &dummy)) return IBMI_ERR_OOM;
+  CUDA_TRY(cudaMemcpyAsync(nc.vr, restart_v, (size_t)cols * sizeof(double), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(nc.vec, y1, (size_t)rows * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  NormBufs nb{const_cast<double*>(g), ldg, nc.vec, nc.part, nc.out, nc.vr, nc.blocks, nc.threads, nc.smem_cap,
+              nullptr, 0, sms};
+  int rc = enqueue_two_norm(b, ldb, rows, cols, rtol, max_iters, nb, st, nullptr, true);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(nc.host, nc.out, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (sigma) *sigma = nc.host[0];
+  if (converged) *converged = nc.host[1] != 0.0;
+  if (iters) *iters = (int)nc.host[2];
+  return IBMI_OK;
+}
+
 static int desc_to_op(const ibmi_gemm_desc* d, GemmOp& op) {
   if (!d) return fail(IBMI_ERR_INVALID, "null descriptor");
   if (d->m < 0 || d->n < 0 || d->m > INT_MAX || d->n > INT_MAX) return fail(IBMI_ERR_DIM, "bad m/n");

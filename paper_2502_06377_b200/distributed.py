@@ -293,6 +293,18 @@ class CudaBackend:
                                         C.byref(cv), stream), "two_norm")
         return sig.value, it.value, bool(cv.value)
 
+    def two_norm_gram(self, b, g, y1, rtol, max_iters):
+        """‖b‖₂ from the caller's Gram matrix g = b·bᵀ and y₁ = b·(1/√cols) (rows ≤ cols)."""
+        torch = self.torch
+        v = restart_vector(b.shape[1])
+        sig, it, cv = C.c_double(), C.c_int(), C.c_int()
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        _abi.check(self.L.ibmi_two_norm_gram(b.shape[0], b.shape[1], C.c_void_p(b.data_ptr()), b.stride(0),
+                                             C.c_void_p(g.data_ptr()), g.stride(0), C.c_void_p(y1.data_ptr()),
+                                             _abi.dbl_ptr(v), float(rtol), int(max_iters), C.byref(sig),
+                                             C.byref(it), C.byref(cv), stream), "two_norm_gram")
+        return sig.value, it.value, bool(cv.value)
+
     def close(self):
         self.torch.cuda.synchronize(self.device)
         for ptr in getattr(self, "_opened", []):
@@ -742,7 +754,7 @@ class ShardedSolver:
                                  c=B, cm=0, cn=0, tma_safe=True, xrows=b, xcols=self.n_loc, yrows=p,
                                  ycols=self.n_loc))
             self.comm.all_reduce(B)
-            return be.two_norm(B, rtol, max_iters)
+            return self._two_norm_sharded(B, rtol, max_iters)
         Bloc = be.zeros(max(a1 - a0, 1), c)[: a1 - a0]
         if a1 > a0:
             be.gemm(GemmSpec(x=self.S, xm=a0, y=self.A, yn=(lo, 0, hi), m=a1 - a0, n=c, segs=[(0, 0, p)],
@@ -750,7 +762,36 @@ class ShardedSolver:
         parts = self.comm.all_gather_rows(Bloc, pl["n_I"])
         order = np.argsort(np.concatenate(pl["rows_I"]), kind="stable")
         B = parts.index_select(0, be.index_tensor(order)).contiguous()
-        return be.two_norm(B, rtol, max_iters)
+        return self._two_norm_sharded(B, rtol, max_iters)
+
+    def _two_norm_sharded(self, B, rtol, max_iters):
+        """‖B‖₂ with B (b × c) on every rank.  One rank: the library forms the Gram matrix.
+        Several ranks (row form, b ≤ c): rank g forms ``B[:, chunk_g]·B[:, chunk_g]ᵀ`` over its
+        share of the columns (lower tiles mirrored), one all-reduce of b × b sums them, and
+        the power iteration runs replicated on the result — the b²·c Gram product is split G
+        ways instead of repeated on every rank.  Same σ on every rank (identical inputs)."""
+        be = self.be
+        b, c = B.shape
+        if self.world == 1 or b > c or not hasattr(be, "two_norm_gram"):
+            return be.two_norm(B, rtol, max_iters)
+        step = -(-c // self.world)
+        step = -(-step // 16) * 16                      # K chunks on 16-column boundaries (TMA k-tiles)
+        c0, c1 = min(c, self.rank * step), min(c, (self.rank + 1) * step)
+        G = self._gbuf(b)
+        G.zero_()
+        if c1 > c0:
+            be.gemm(GemmSpec(x=B, xm=0, y=B, yn=0, m=b, n=b, segs=[(c0, c0, c1 - c0)], c=G, lower=True,
+                             mirror=True, tma_safe=True, xrows=b, xcols=c, yrows=b, ycols=c))
+        self.comm.all_reduce(self._gb[:b])          # the contiguous b × ldg block (padding columns are zero)
+        y1 = B.sum(dim=1) * (1.0 / float(np.sqrt(c)))
+        return be.two_norm_gram(B, G, y1, rtol, max_iters)
+
+    def _gbuf(self, b):
+        buf = getattr(self, "_gb", None)
+        ldg = -(-b // 32) * 32
+        if buf is None or buf.shape[0] < b or buf.shape[1] != ldg:
+            self._gb = buf = self.be.zeros(b, ldg)
+        return buf[:b, :b]
 
     def sweep(self, rtol: float = 1e-9, max_iters: int = 5000):
         for k in range(len(self.ranges)):

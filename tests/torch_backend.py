@@ -91,5 +91,13 @@ class TorchCPUBackend:
         s, conv, it = orc.power_sigma_max(b.numpy(), rtol, max_iters)
         return s, it, conv
 
+    def two_norm_gram(self, b, g, y1, rtol, max_iters):
+        # the caller's Gram matrix and y1 must be what the library would have formed itself
+        bn = b.numpy()
+        assert np.allclose(g.numpy(), bn @ bn.T, rtol=1e-10, atol=1e-10 * float(np.abs(g.numpy()).max() + 1e-300))
+        assert np.allclose(y1.numpy(), bn.sum(axis=1) / np.sqrt(bn.shape[1]), rtol=1e-10, atol=1e-12)
+        s, conv, it = orc.power_sigma_max(bn, rtol, max_iters)
+        return s, it, conv
+
     def close(self):
         pass
