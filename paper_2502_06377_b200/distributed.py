@@ -631,14 +631,35 @@ class ShardedSolver:
         return cache[k]
 
     # ------------------------------------------------------------ Σ₀
-    def init_sigma(self, guess: str = "identity"):
-        """Σ = I, Σ[c₁,c₁] = identity or diag(1/A_ii) (solver.py:244-251 + BASELINE jacobi)."""
+    def init_sigma(self, guess: str = "identity", sigma0_cc=None):
+        """Σ = I, Σ[c₁,c₁] = identity or diag(1/A_ii) (solver.py:244-251 + BASELINE jacobi),
+        or the given c₁ × c₁ matrix ``sigma0_cc`` (any other reference guess, solver.py:215-222,
+        computed by the caller and identical on every rank)."""
         torch = self.torch
         self.S.zero_()
-        if self.n_loc:
+        if sigma0_cc is not None:
+            lo, hi = self.ranges[0]
+            comp = np.concatenate([np.arange(0, lo), np.arange(hi, self.p)])
+            g = np.asarray(sigma0_cc, dtype=np.float64)
+            if g.shape != (comp.size, comp.size):
+                from .exceptions import DimensionMismatch
+
+                raise DimensionMismatch(f"guess must be {comp.size} x {comp.size}, got {g.shape}")
+            if self.perm is not None:
+                raise NotImplementedError("explicit guesses with relabelled (non-contiguous) partitions")
+            if self.n_loc:
+                self._seed_sigma("identity")                      # the rows of I₁ keep their unit diagonal
+                inc = (self.own < lo) | (self.own >= hi)          # my rows inside c₁
+                pos = np.searchsorted(comp, self.own[inc])
+                rows = self.be.index_tensor(np.nonzero(inc)[0])
+                vals = torch.as_tensor(g[pos, :], device=self.S.device)
+                blk = torch.zeros((len(pos), self.p), dtype=torch.float64, device=self.S.device)
+                blk[:, self.be.index_tensor(comp)] = vals
+                self.S[rows, : self.p] = blk
+        elif self.n_loc:
             self._seed_sigma(guess)
         elif guess not in ("identity", "jacobi"):
-            raise NotImplementedError(f"guess {guess!r} on the sharded path")
+            raise NotImplementedError(f"guess {guess!r} on the sharded path needs sigma0_cc")
         # No rank may start its first panel GEMM before every panel is seeded: in the
         # p2p exchange K1's epilogue stores −M into the OWNERS' panels, and a late
         # zero_() on a slow rank would wipe those stores.
@@ -887,7 +908,7 @@ class ShardedSolver:
 # --------------------------------------------------------------------------- public entry point
 def solve_sharded(a, part: Partition, cfg=None, *, group=None, panel: int = 128, device: int | None = None,
                   exchange: str = "auto", backend=None, gather_result: bool = True, callback=None,
-                  operands: str = "auto"):
+                  operands: str = "auto", sigma0_cc=None):
     """``solve`` (reference solver.py:225-278) with Σ sharded over the process group.
 
     Call it on every rank with the same ``a`` (host array or a device copy) and
@@ -897,7 +918,9 @@ def solve_sharded(a, part: Partition, cfg=None, *, group=None, panel: int = 128,
     once the estimate is below 1.01·tol, since ‖I − AΣ‖_F ≥ the estimate).
     Every rank returns the same trace; ``result`` is the full Σ (host numpy,
     original index order) on every rank when ``gather_result``, else None.
-    Supported guesses: identity and jacobi; FP64 DMMA GEMMs only.
+    Every reference guess is supported (identity / jacobi are seeded per panel; local, mc
+    and takahashi are formed replicated by the single-GPU kernels, or passed as
+    ``sigma0_cc``); FP64 DMMA GEMMs only.
     """
     import time
     import warnings
@@ -909,15 +932,23 @@ def solve_sharded(a, part: Partition, cfg=None, *, group=None, panel: int = 128,
     cfg = cfg or IbmiConfig()
     if getattr(cfg, "gemm", None) == "ozaki":
         raise NotImplementedError("the sharded sweep runs FP64 DMMA GEMMs only (gemm='ozaki' is single-GPU)")
-    if cfg.initial_guess not in ("identity", "jacobi"):
-        raise NotImplementedError(f"guess {cfg.initial_guess!r} on the sharded path")
     validate(part)
     stopping = getattr(cfg, "stopping", "estimate")
     t0 = time.perf_counter()
     ss = ShardedSolver(a, part, group=group, panel=panel, backend=backend, device=device, exchange=exchange,
                        operands=operands)
     try:
-        ss.init_sigma(cfg.initial_guess)
+        if sigma0_cc is None and cfg.initial_guess not in ("identity", "jacobi"):
+            # local / mc / takahashi (solver.py:162-222): the single-GPU kernels form Σ₀[c₁,c₁] on
+            # every rank from the same inputs (replicated, O(c³) once per solve)
+            from .solver import make_initial_guess
+
+            lo, hi = ss.ranges[0]
+            if ss.perm is not None:
+                raise NotImplementedError("non-trivial guesses with relabelled (non-contiguous) partitions")
+            comp0 = np.concatenate([np.arange(0, lo), np.arange(hi, ss.p)])
+            sigma0_cc = make_initial_guess(a, comp0, cfg)
+        ss.init_sigma(cfg.initial_guess, sigma0_cc)
         setup_s = time.perf_counter() - t0
         errs, walls, pits, resid = [], [], [], []
         converged = False

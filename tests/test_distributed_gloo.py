@@ -123,16 +123,24 @@ def _solve_worker(rank, world, port, case, out):
         p, k, f, tol, guess, stopping = case
         m = np.random.default_rng(p + k).standard_normal((p, p))
         a = m.T @ m + 0.05 * p * np.eye(p)
-        rep = solve_sharded(a, contiguous_partition(p, k, f),
+        part = contiguous_partition(p, k, f)
+        s0 = None
+        if guess not in ("identity", "jacobi"):       # CPU test: Σ₀[c₁,c₁] from the oracle's guess
+            from oracle import ibmi_oracle as orc
+
+            comp0 = orc.complement(p, part.sets[0])
+            s0 = orc.initial_sigma(a, comp0, guess)[np.ix_(comp0, comp0)]
+        rep = solve_sharded(a, part,
                             IbmiConfig(tol=tol, initial_guess=guess, stopping=stopping, max_iterations=300),
-                            panel=8, backend=TorchCPUBackend())
+                            panel=8, backend=TorchCPUBackend(), sigma0_cc=s0)
         out.put((rank, rep.iterations, rep.converged, rep.error_trace, rep.result, rep.residual_trace))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("case", [(72, 3, 0.1, 1e-10, "identity", "estimate"),
-                                  (64, 2, 0.0, 1e-9, "jacobi", "frobenius")])
+                                  (64, 2, 0.0, 1e-9, "jacobi", "frobenius"),
+                                  (72, 3, 0.1, 1e-10, "local", "estimate")])
 def test_solve_sharded_matches_oracle(case):
     """solve_sharded (the public N-rank solve) stops on the same sweep as the oracle's solve."""
     from oracle import ibmi_oracle as orc

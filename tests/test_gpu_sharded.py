@@ -197,3 +197,56 @@ def test_sharded_p2p_late_rank_cannot_wipe_peer_stores(monkeypatch):
     for rank, errs, sig, fr in res:
         assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
         np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-13)
+
+
+def _solve_worker(rank, world, port, guess, out):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2502_06377_b200 import IbmiConfig, contiguous_partition
+        from paper_2502_06377_b200.distributed import solve_sharded
+
+        p = 520
+        m = np.random.default_rng(p).standard_normal((p, p))
+        a = m.T @ m + 0.05 * p * np.eye(p)
+        rep = solve_sharded(a, contiguous_partition(p, 4, 0.125),
+                            IbmiConfig(tol=1e-10, initial_guess=guess, max_iterations=200, mc_samples=40, mc_seed=3),
+                            panel=64, device=0)
+        out.put((rank, rep.iterations, rep.converged, rep.error_trace, rep.result))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("guess", ["local", "mc", "takahashi"])
+def test_solve_sharded_reference_guesses(guess):
+    """solve_sharded with the reference's non-trivial initial guesses (solver.py:162-222):
+    Σ₀[c₁,c₁] is formed by the single-GPU kernels on every rank and seeded panel by panel."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import contiguous_partition
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_solve_worker, args=(r, 2, port, guess, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = 520
+    m = np.random.default_rng(p).standard_normal((p, p))
+    a = m.T @ m + 0.05 * p * np.eye(p)
+    o = orc.solve(a, contiguous_partition(p, 4, 0.125).sets, tol=1e-10, guess=guess, max_iterations=200,
+                  mc_samples=40, mc_seed=3)
+    for rank, iters, conv, errs, sig in res:
+        assert conv and abs(iters - o["iterations"]) <= 1
+        assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
