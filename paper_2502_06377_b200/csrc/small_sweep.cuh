@@ -92,7 +92,7 @@ __device__ __forceinline__ void ss_tile(const SsOperand& X, const SsOperand& Y, 
     const int steps = (len + 3) >> 2;
     const int per = (steps + 7) >> 3;                  // k-steps per warp, contiguous slice
     const int s0 = wid * per, s1 = min(steps, s0 + per);
-#pragma unroll 4
+#pragma unroll 2
     for (int ks = s0; ks < s1; ++ks) {
       const int k = 4 * ks + t;
       const bool kv = k < len;
