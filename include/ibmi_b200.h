@@ -334,7 +334,10 @@ long long ibmi_launch_count(void);
  * key 13: power iteration of mid-size Gram matrices (512 <= n <= 2220) with the
  *         flag-carrying line exchange instead of a grid barrier per iteration (default 1);
  * key 14: p <= 1024 (FP64 DMMA, contiguous sets): ibmi_sweep / ibmi_solve_loop run the K block updates,
- *         the estimate matrix and its Gram form as one cooperative kernel (default 1). */
+ *         the estimate matrix and its Gram form as one cooperative kernel (default 1);
+ * key 15: split-K GEMMs on the TMA kernel reduce their partial tiles inside the GEMM (the split
+ *         that arrives last at a tile sums them in split order and runs the epilogue) instead of
+ *         a separate reduction launch (default 1; same bits either way). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

@@ -83,6 +83,9 @@ struct GemmParams {
   int tiles_m, tiles_n;
   int group_m = 0;                           // raster: bands of group_m tile rows, tn-major inside (0: tm-major)
   double* partial;                           // EPI_FROB: one partial sum per CTA; EPI_PARTIAL: split tiles
+  int* tile_count = nullptr;                 // EPI_PARTIAL on the TMA kernel: per-tile arrival counters (zeroed
+                                             // before the launch); the split that arrives last reduces the tile
+                                             // and runs the epilogue, so no separate reduction launch is needed
 };
 
 // Output tile of linear tile index `tile` (the GEMM kernels and the split-K
@@ -397,10 +400,9 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
 // keeps 16 row accumulators and streams the split partials with the split
 // loop outside, so 16 independent loads are in flight per thread; every
 // element is still summed in split order 0..s-1 (deterministic, unchanged bits).
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) {
-  __shared__ double tr[32][129];
-  const int tile = blockIdx.x / (GB_M / 32);
-  const int rc = (blockIdx.x % (GB_M / 32)) * 32;
+// One 32-row chunk (rows rc..rc+31) of output tile `tile`: sum the split partials in split order and run the
+// STORE epilogue.  All 256 threads of the CTA call it together; `tr` is 32 × 129 doubles of shared memory.
+__device__ __forceinline__ void splitk_reduce_chunk(const GemmParams& P, int tile, int rc, double (*tr)[129]) {
   int tm, tn;
   tile_coords(P, tile, tm, tn);
   const bool diag_tile = P.lower && tm == tn;
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) 
   for (int sp = 0; sp < P.splits; ++sp) {
     const double* base = src + (size_t)sp * GB_M * GB_N + (size_t)r0 * GB_N + c;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] += __ldcs(base + 2 * q * GB_N);
+    for (int q = 0; q < 16; ++q) acc[q] += __ldcg(base + 2 * q * GB_N);
   }
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
@@ -445,6 +447,11 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) 
       if (P.peers) peer_store(P, m, nn, v);
     }
   }
+}
+
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) {
+  __shared__ double tr[32][129];
+  splitk_reduce_chunk(P, blockIdx.x / (GB_M / 32), (blockIdx.x % (GB_M / 32)) * 32, tr);
   if (P.peers) __threadfence_system();
 }
 

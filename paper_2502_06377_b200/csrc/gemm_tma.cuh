@@ -228,6 +228,26 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) dst[xrow[i] * GB_N + wn0 + 8 * j + perm8(2 * t + e)] = acc[i][j][e];
+    if (P.tile_count != nullptr) {
+      // Fix-up inside the GEMM: the split that arrives last at this tile sums all partials in
+      // split order (same bits as the separate reduction kernel) and runs the STORE epilogue.
+      // The stage ring is free by now (every issued TMA load was consumed) and serves as the
+      // 32 × 129 transpose buffer.
+      __shared__ int last;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) last = atomicAdd(P.tile_count + tile, 1) == P.splits - 1;
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        double(*tr)[129] = reinterpret_cast<double(*)[129]>(gbase);
+        for (int rc = 0; rc < GB_M; rc += 32) {
+          splitk_reduce_chunk(P, tile, rc, tr);
+          __syncthreads();
+        }
+        if (P.peers) __threadfence_system();
+      }
+    }
   } else {
     double s = 0.0;
 #pragma unroll

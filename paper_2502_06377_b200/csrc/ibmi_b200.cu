@@ -260,6 +260,10 @@ struct GemmOp {
   }
 };
 
+// Split-K workspace: s partial tiles per output tile, then one int arrival counter per tile
+// (the fused fix-up of the TMA kernel), in doubles.
+inline int64_t split_ws_doubles(int64_t tiles, int s) { return tiles * s * GB_M * GB_N + (tiles + 1) / 2; }
+
 // Tuning knobs (ibmi_tune): GEMM configuration of the hot NT kernels and
 // split-K factors of the small-grid GEMMs.
 int g_variant = 0;          // 0: CfgA (8 warps 64x32), 1: CfgB (16 warps 32x32), 2: CfgC (BK 32)
@@ -268,6 +272,7 @@ int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
 int g_power_ll = 1;         // mid-size Gram power iteration with the flag-carrying exchange (no grid barrier)
+int g_split_fused = 1;      // split-K partial tiles reduced by the last-arriving split inside the TMA GEMM (no reduction launch)
 int g_small_fused = 1;      // p <= 1024: the whole sweep's GEMM phases in one cooperative kernel (small_sweep.cuh)
 int g_split_min_kt = 4;     // split-K keeps at least this many k-tiles per split
 int g_raster_group = 0;     // GEMM tile raster: bands of this many tile rows (0 = tm-major)
@@ -511,6 +516,13 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
     }
     if (ok) {
       *path = 1;
+      if (epi == EPI_PARTIAL && g_split_fused) {
+        // arrival counters behind the partial tiles; the last split of a tile reduces it in the kernel
+        P.tile_count = reinterpret_cast<int*>(op.ws + (size_t)tiles * op.splits * GB_M * GB_N);
+        err = cudaMemsetAsync(P.tile_count, 0, (size_t)tiles * sizeof(int), s);
+        if (err != cudaSuccess) return err;
+        return launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
+      }
       if (epi == EPI_PARTIAL) err = launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
       else if (epi == EPI_FROB) err = launch_tma_inst<EPI_FROB>(P, maps, grid, s);
       else err = launch_tma_inst<EPI_STORE>(P, maps, grid, s);
@@ -1648,7 +1660,7 @@ int plan_split(const ibmi_ctx* c, const GemmOp& op, int forced, int64_t* ws_need
   for (int i = 0; i < op.nseg; ++i) klen += op.seg[i].len;
   const int bk = g_variant == 2 ? 32 : 16;
   const int s = forced > 0 ? forced : auto_split(tiles, (int)((klen + bk - 1) / bk), c->sms);
-  if (ws_need) *ws_need = s > 1 ? (int64_t)tiles * s * GB_M * GB_N : 0;
+  if (ws_need) *ws_need = s > 1 ? split_ws_doubles(tiles, s) : 0;
   return s;
 }
 
@@ -2074,7 +2086,7 @@ int enqueue_two_norm(const double* Bm, int64_t ldB, int64_t b, int64_t cc, doubl
     if (nb.ws && mode == 0) {
       const int bk = g_variant == 2 ? 32 : 16;
       gg.splits = g_split_gram > 0 ? g_split_gram : auto_split(gemm_tiles(gg), (int)((cc + bk - 1) / bk), nb.sms);
-      if ((int64_t)gemm_tiles(gg) * gg.splits * GB_M * GB_N > nb.ws_cap) gg.splits = 1;
+      if (split_ws_doubles(gemm_tiles(gg), gg.splits) > nb.ws_cap) gg.splits = 1;
       gg.ws = nb.ws;
     }
     CUDA_TRY(launch_gemm(gg, st));
@@ -3399,7 +3411,7 @@ int ibmi_two_norm(int64_t rows, int64_t cols, const double* b, int64_t ldb, cons
     gg.add_seg(0, 0, cols);
     const int bk = g_variant == 2 ? 32 : 16;
     const int sp = g_split_gram > 0 ? g_split_gram : auto_split(gemm_tiles(gg), (int)((cols + bk - 1) / bk), sms);
-    if (sp > 1 && ensure_buf(&nc.ws, &nc.ws_cap, (int64_t)gemm_tiles(gg) * sp * GB_M * GB_N, &dummy))
+    if (sp > 1 && ensure_buf(&nc.ws, &nc.ws_cap, split_ws_doubles(gemm_tiles(gg), sp), &dummy))
       return IBMI_ERR_OOM;
   }
   NormBufs nb{nc.G, ldG, nc.vec, nc.part, nc.out, nc.vr, nc.blocks, nc.threads, nc.smem_cap, nc.ws, nc.ws_cap, sms};
@@ -3526,7 +3538,7 @@ int ibmi_gemm_workspace(const ibmi_gemm_desc* d, int64_t* doubles) {
   const int64_t tiles = gemm_tiles(op);
   int64_t need = 0;
   if (d->frob_out) need = tiles;
-  else if (op.splits > 1) need = tiles * op.splits * GB_M * GB_N;
+  else if (op.splits > 1) need = split_ws_doubles(tiles, op.splits);
   if (doubles) *doubles = need;
   return IBMI_OK;
 }
@@ -3719,6 +3731,9 @@ int ibmi_tune(int key, int value) {
       break;
     case 14:
       g_small_fused = value ? 1 : 0;
+      break;
+    case 15:
+      g_split_fused = value ? 1 : 0;
       break;
     case 12:
       if (value < 0 || value > 1024) return fail(IBMI_ERR_INVALID, "raster group must be in [0, 1024]");
