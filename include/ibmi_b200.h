@@ -337,7 +337,8 @@ long long ibmi_launch_count(void);
  *         the estimate matrix and its Gram form as one cooperative kernel (default 1);
  * key 15: split-K GEMMs on the TMA kernel reduce their partial tiles inside the GEMM (the split
  *         that arrives last at a tile sums them in split order and runs the epilogue) instead of
- *         a separate reduction launch (default 1; same bits either way). */
+ *         a separate reduction launch (default 0: measured 1-4% slower than the reduction kernel,
+ *         DESIGN.md §3; same bits either way). */
 int ibmi_tune(int key, int value);
 
 /* Measured FP64 DMMA throughput of `device` (TFLOP/s), the roofline denominator. */

@@ -272,7 +272,9 @@ int g_split_gram = 0;       // split-K of the Gram GEMM (0 = auto)
 int g_split_panel = 0;      // split-K of the panel and estimate GEMMs (0 = auto)
 int g_cluster_power = 1;    // small Gram power iteration on one 16-CTA cluster
 int g_power_ll = 1;         // mid-size Gram power iteration with the flag-carrying exchange (no grid barrier)
-int g_split_fused = 1;      // split-K partial tiles reduced by the last-arriving split inside the TMA GEMM (no reduction launch)
+int g_split_fused = 0;      // split-K partial tiles reduced by the last-arriving split inside the TMA GEMM (no reduction
+                            // launch).  Measured slower than the separate reduction kernel (c4 274.2 vs 269.6 ms per sweep,
+                            // profiles/r02_splitk_fused_ab.log): off by default
 int g_small_fused = 1;      // p <= 1024: the whole sweep's GEMM phases in one cooperative kernel (small_sweep.cuh)
 int g_split_min_kt = 4;     // split-K keeps at least this many k-tiles per split
 int g_raster_group = 0;     // GEMM tile raster: bands of this many tile rows (0 = tm-major)
