@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(CF::THREADS, 1) gemm_nt_kernel(const GemmParam
 // element is still summed in split order 0..s-1 (deterministic, unchanged bits).
 // One 32-row chunk (rows rc..rc+31) of output tile `tile`: sum the split partials in split order and run the
 // STORE epilogue.  All 256 threads of the CTA call it together; `tr` is 32 × 129 doubles of shared memory.
+template <bool STREAM>
 __device__ __forceinline__ void splitk_reduce_chunk(const GemmParams& P, int tile, int rc, double (*tr)[129]) {
   int tm, tn;
   tile_coords(P, tile, tm, tn);
@@ -420,7 +421,7 @@ __device__ __forceinline__ void splitk_reduce_chunk(const GemmParams& P, int til
   for (int sp = 0; sp < P.splits; ++sp) {
     const double* base = src + (size_t)sp * GB_M * GB_N + (size_t)r0 * GB_N + c;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] += __ldcg(base + 2 * q * GB_N);
+    for (int q = 0; q < 16; ++q) acc[q] += STREAM ? __ldcs(base + 2 * q * GB_N) : __ldcg(base + 2 * q * GB_N);
   }
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
@@ -451,7 +452,7 @@ __device__ __forceinline__ void splitk_reduce_chunk(const GemmParams& P, int til
 
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const GemmParams P) {
   __shared__ double tr[32][129];
-  splitk_reduce_chunk(P, blockIdx.x / (GB_M / 32), (blockIdx.x % (GB_M / 32)) * 32, tr);
+  splitk_reduce_chunk<true>(P, blockIdx.x / (GB_M / 32), (blockIdx.x % (GB_M / 32)) * 32, tr);
   if (P.peers) __threadfence_system();
 }
 

@@ -75,7 +75,9 @@ __device__ __forceinline__ void tma_operand(uint32_t dst, const CUtensorMap* big
   }
 }
 
-template <int EPI>
+// FIX (EPI_PARTIAL only): the split-K fix-up inside the kernel.  A template parameter, not a run-time
+// branch: even never taken, the extra code cost the default split-K instance 0.3-1.4% (register allocation).
+template <int EPI, bool FIX = false>
 __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, const __grid_constant__ TmaMaps maps) {
   constexpr int MI = 8, NJ = 4;
   extern __shared__ __align__(1024) unsigned char tsmem_raw[];
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) dst[xrow[i] * GB_N + wn0 + 8 * j + perm8(2 * t + e)] = acc[i][j][e];
-    if (P.tile_count != nullptr) {
+    if (FIX) {
       // Fix-up inside the GEMM: the split that arrives last at this tile sums all partials in
       // split order (same bits as the separate reduction kernel) and runs the STORE epilogue.
       // The stage ring is free by now (every issued TMA load was consumed) and serves as the
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tma_kernel(const GemmParams P, co
         __threadfence();
         double(*tr)[129] = reinterpret_cast<double(*)[129]>(gbase);
         for (int rc = 0; rc < GB_M; rc += 32) {
-          splitk_reduce_chunk(P, tile, rc, tr);
+          splitk_reduce_chunk<false>(P, tile, rc, tr);
           __syncthreads();
         }
         if (P.peers) __threadfence_system();

@@ -309,19 +309,19 @@ bool encode_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, 
   return r == CUDA_SUCCESS;
 }
 
-template <int EPI>
+template <int EPI, bool FIX = false>
 cudaError_t launch_tma_inst(const GemmParams& P, const TmaMaps& maps, int grid, cudaStream_t s) {
   static bool attr_done[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
   if (!attr_done[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tma_kernel<EPI, FIX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)TMA_SMEM);
     if (e != cudaSuccess) return e;
     attr_done[dev] = true;
   }
-  gemm_tma_kernel<EPI><<<grid, 256, TMA_SMEM, s>>>(P, maps); note_launch();
+  gemm_tma_kernel<EPI, FIX><<<grid, 256, TMA_SMEM, s>>>(P, maps); note_launch();
   return cudaGetLastError();
 }
 
@@ -523,7 +523,7 @@ cudaError_t launch_gemm_impl(const GemmOp& op, cudaStream_t s, int* path) {
         P.tile_count = reinterpret_cast<int*>(op.ws + (size_t)tiles * op.splits * GB_M * GB_N);
         err = cudaMemsetAsync(P.tile_count, 0, (size_t)tiles * sizeof(int), s);
         if (err != cudaSuccess) return err;
-        return launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
+        return launch_tma_inst<EPI_PARTIAL, true>(P, maps, grid, s);
       }
       if (epi == EPI_PARTIAL) err = launch_tma_inst<EPI_PARTIAL>(P, maps, grid, s);
       else if (epi == EPI_FROB) err = launch_tma_inst<EPI_FROB>(P, maps, grid, s);
@@ -2044,6 +2044,7 @@ bool power_ll_launch(PowerParams& P, const NormBufs& nb, cudaStream_t st) {
   const int rpc = (n + nb.blocks - 1) / nb.blocks;
   if (rpc > LL_ROWS) return false;
   const int grid = (n + rpc - 1) / rpc;
+  if (grid > 192) return false;                  // the kernel polls at most 3 rounds of 64 lines
   const int q = (n / 2 + 511) / 512;
   const int rr = q == 1 ? 8 : (q == 2 ? 6 : 4);
   const size_t smem = ((size_t)((grid * rpc + 1) & ~1) + 256 + 64 + (size_t)std::max(0, rpc - rr) * n) * sizeof(double);

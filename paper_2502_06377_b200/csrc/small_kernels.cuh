@@ -693,21 +693,37 @@ __global__ void __launch_bounds__(512, 1) power_gram_ll_kernel(PowerParams P, do
       if (lane == 7) b = __longlong_as_double(tag);
       if (lane < 8) ll_store16(lines + (size_t)blockIdx.x * 16 + 2 * lane, a, b);
     }
-    // poll: 8 lanes per line, 4 lines per warp and round
+    // poll: 8 lanes per line, 64 lines per round; the loads of all rounds are issued before any
+    // flag is examined, so the rounds cost one L2 round trip together, not one each
     const int grp = tid >> 3, k = tid & 7;
-    for (int s0 = 0; s0 < nblk; s0 += 64) {
-      const int src = s0 + grp;
-      const bool live = src < nblk;
-      double2 d = make_double2(0.0, 0.0);
-      for (;;) {
-        if (live) d = ll_load16(lines + (size_t)src * 16 + 2 * k);
-        const long long f = __double_as_longlong(__shfl_sync(0xffffffffu, d.y, 7, 8));
-        if (__all_sync(0xffffffffu, !live || f == tag)) break;
+    constexpr int LL_ROUNDS = 3;                       // grids of up to 192 CTAs
+    double2 d[LL_ROUNDS];
+    bool done[LL_ROUNDS];
+#pragma unroll
+    for (int r = 0; r < LL_ROUNDS; ++r) {
+      d[r] = make_double2(0.0, 0.0);
+      done[r] = r * 64 + grp >= nblk;
+    }
+    for (;;) {
+#pragma unroll
+      for (int r = 0; r < LL_ROUNDS; ++r)
+        if (!done[r]) d[r] = ll_load16(lines + (size_t)(r * 64 + grp) * 16 + 2 * k);
+      bool all = true;
+#pragma unroll
+      for (int r = 0; r < LL_ROUNDS; ++r) {
+        const long long f = __double_as_longlong(__shfl_sync(0xffffffffu, d[r].y, 7, 8));
+        done[r] = done[r] || f == tag;
+        all = all && done[r];
       }
-      if (live) {
+      if (__all_sync(0xffffffffu, all)) break;
+    }
+#pragma unroll
+    for (int r = 0; r < LL_ROUNDS; ++r) {
+      const int src = r * 64 + grp;
+      if (src < nblk) {
         const int base = src * rpc;
-        if (2 * k < rpc) zr[base + 2 * k] = d.x;
-        if (2 * k + 1 < rpc) zr[base + 2 * k + 1] = d.y;
+        if (2 * k < rpc) zr[base + 2 * k] = d[r].x;
+        if (2 * k + 1 < rpc) zr[base + 2 * k + 1] = d[r].y;
       }
     }
     __syncthreads();

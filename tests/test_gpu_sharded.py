@@ -119,9 +119,8 @@ def test_sharded_two_ranks_match_oracle(case, exchange, operands):
         np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-13)
 
 
-def test_sharded_operands_three_ranks_and_not_spd():
-    """Operand-sharded set-up on 3 ranks sharing the GPU (uneven panels), and the
-    collective NotPositiveDefinite of a set whose owner is another rank."""
+def test_sharded_operands_three_ranks():
+    """Operand-sharded set-up and sweeps on 3 ranks sharing the GPU (uneven panels)."""
     from oracle import ibmi_oracle as orc
     from paper_2502_06377_b200 import contiguous_partition
 
