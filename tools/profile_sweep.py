@@ -34,6 +34,7 @@ torch.cuda.synchronize()
 torch.cuda.profiler.start()
 for _ in range(args.sweeps):
     err, it, conv, t = ds.sweep_timed(1e-9, 5000)
+    print(f"power iterations {it}: {t['power_iteration'] * 1e3:.1f} us", flush=True)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print("sweep ms", t)
