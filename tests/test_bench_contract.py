@@ -79,3 +79,21 @@ def test_our_arm_line_on_gpu():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("operands", ["replicated", "sharded"])
+def test_sharded_driver_line_on_gpu(operands):
+    """The N-rank driver of bench.py at world size 1 (`--sharded`): same contract keys, plus the
+    `sharded` block (operand mode, exchange, this rank's NVLink bytes per sweep) and an e2e
+    through solve_sharded."""
+    d = _run(["--config", "c1", "--steps", "3", "--warmup", "3", "--no-alt", "--no-cpu-baseline", "--sharded",
+              "--operands", operands], timeout=900)
+    assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] > 0
+    sh = d["sharded"]
+    assert sh["operands"] == operands and sh["exchange_mode"] in ("p2p", "nccl")
+    assert sh["comm_bytes_per_sweep_this_rank"]["gemm_flops"] > 0
+    assert sh["comm_bytes_per_sweep_this_rank"]["exchange_out"] == 0      # one rank: nothing crosses NVLink
+    assert d["time_to_tol"]["sweeps"] == 107
+    assert d["e2e"]["value"] > 0
