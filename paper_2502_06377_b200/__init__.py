@@ -1,8 +1,11 @@
 """B200-native IBMI sweep (iterative block matrix inversion, arXiv 2502.06377).
 
 Drop-in for the reference package's solver path: the names re-exported here
-follow ``ibmi/__init__.py:11-79`` for the solver, partition and exception
-surfaces.  All arithmetic runs in ``libibmi_b200.so`` (FP64 DMMA kernels for
+follow ``ibmi/__init__.py:11-79``: the solver, partition, exception, dense-core
+(``linalg``), diagnostics (``analysis``) and matrix-file (``matio``) surfaces.  Not
+re-exported, out of scope: the covariance-kernel generators
+(``kernel_matrix``, ``KernelSpec``, ``PointSet``, ``grid_1d/2d``, ``FAMILIES``), the
+CSV experiment harness (``run_experiment`` …) and the public ``ldlt``.  All arithmetic runs in ``libibmi_b200.so`` (FP64 DMMA kernels for
 sm_100a, C ABI in ``include/ibmi_b200.h``); there is no CPU fallback.
 """
 
@@ -22,6 +25,26 @@ from .exceptions import (  # noqa: F401
     UncoveredIndices,
     ZeroPivot,
 )
+from .analysis import (  # noqa: F401
+    CostBreakdown,
+    condition_number_2,
+    contraction_factor,
+    flop_cost,
+    lemma_error_recurrence_check,
+    newton_schultz,
+    spectral_radius_condition,
+)
+from .linalg import (  # noqa: F401
+    CholeskyFactor,
+    chol_solve,
+    cholesky,
+    gather,
+    matmul,
+    scatter_add_assign,
+    spd_inverse,
+    two_norm,
+)
+from .matio import load_csv, load_ibmi, load_matrix, save_csv, save_ibmi, save_matrix  # noqa: F401
 from .partition import (  # noqa: F401
     Partition,
     complement,
