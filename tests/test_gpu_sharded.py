@@ -249,3 +249,24 @@ def test_solve_sharded_reference_guesses(guess):
     for rank, iters, conv, errs, sig in res:
         assert conv and abs(iters - o["iterations"]) <= 1
         assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_sharded_four_ranks_overlapping_mid_size(exchange):
+    """Four ranks sharing the GPU, p = 2048 in 128-row block-cyclic panels (four panels per rank),
+    eight overlapping sets, operands sharded: W panel gathers, fused peer-store exchange through
+    CUDA IPC between four processes, split Gram — against the oracle."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import contiguous_partition
+
+    case = ((2048, 8, 0.125), 4, 128)
+    (p, k, f), sweeps, panel = case
+    res = _run(4, "gloo", case, exchange, "sharded")
+    m = np.random.default_rng(p).standard_normal((p, p))
+    a = m.T @ m + p * np.eye(p)
+    o = orc.solve(a, contiguous_partition(p, k, f).sets, tol=1e-300, max_iterations=sweeps)
+    assert len(res) == 4
+    for rank, errs, sig, fr in res:
+        assert np.linalg.norm(sig - o["result"]) <= 1e-10 * np.linalg.norm(o["result"])
+        np.testing.assert_allclose(errs, o["error_trace"], rtol=1e-6, atol=1e-13)
+        assert abs(fr - orc.frobenius_residual(a, o["result"])) <= 1e-9 * max(1.0, fr)
