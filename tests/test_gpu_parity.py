@@ -379,6 +379,72 @@ def test_c3_full_solve_matches_reference():
     check_sketch(rep.result, golden("c3_sketch.npz"), "final")
 
 
+@pytest.mark.parametrize("seed", [1, 2])
+def test_c1_repeat_seeds_full_solve_matches_oracle(seed):
+    """repeats use seeds 1 and 2.  Full c1 solves against the oracle (bit-identical to
+    the reference on seed 0): same sweep count, trace in band, the whole Σ within 1e-10."""
+    import paper_2502_06377_b200 as pkg
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import configs
+
+    cfg = configs.get_config("c1")
+    a = configs.make_matrix("c1", seed)
+    rep = pkg.solve(a, cfg.partition(), pkg.IbmiConfig(tol=cfg.tol, max_iterations=cfg.max_iterations,
+                                                       initial_guess="jacobi"))
+    o = orc.solve(a, cfg.partition().sets, tol=cfg.tol, max_iterations=cfg.max_iterations, guess="jacobi")
+    assert rep.converged and o["converged"]
+    check_trace(rep.error_trace, o["error_trace"], cfg.tol)
+    assert rel_fro(rep.result, o["result"]) < 1e-10
+
+
+@pytest.mark.slow
+def test_c4_first_sweep_whole_sigma_matches_oracle():
+    """c4 at full size, the north-star metric itself: the WHOLE Σ (16384², not a sketch) after the
+    first sweep against the oracle's first sweep run on this host's cores (about a minute of CPU)."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import configs
+    from paper_2502_06377_b200.device import DeviceSolver
+
+    cfg = configs.get_config("c4")
+    a = configs.make_matrix("c4")
+    part = cfg.partition()
+    with DeviceSolver(a, partition=part) as ds:
+        ds.setup()
+        ds.init_sigma(0)
+        err = ds.sweep(1e-9, 5000)[0]
+        s = ds.sigma()
+    sigma = np.eye(cfg.p)
+    for idx in part.sets:                       # W per set on the fly: same arithmetic, 2 GB less RAM
+        orc.BlockOp(a, idx, orc.complement(cfg.p, idx)).apply(sigma)
+    ref_err = orc.error_estimate(a, sigma, part.sets[-1], orc.complement(cfg.p, part.sets[-1]))[0]
+    assert rel_fro(s, sigma) < 1e-10
+    assert abs(err - ref_err) <= 1e-6 * ref_err
+    assert abs(ref_err - float(golden("c4long.npz")["error_trace"][0])) <= 1e-9 * ref_err   # the reference's value
+
+
+@pytest.mark.parametrize("name,seed,sweeps", [("c2", 1, 2), ("c3", 1, 1)])
+def test_c2_c3_repeat_seed_whole_sigma_matches_oracle(name, seed, sweeps):
+    """The north-star metric on the WHOLE Σ (not a sketch) at full c2 / c3 size: the first sweeps
+    of a repeat seed on the GPU against the oracle's, relative Frobenius ≤ 1e-10."""
+    from oracle import ibmi_oracle as orc
+    from paper_2502_06377_b200 import configs
+    from paper_2502_06377_b200.device import DeviceSolver
+
+    cfg = configs.get_config(name)
+    a = configs.make_matrix(name, seed)
+    part = cfg.partition()
+    with DeviceSolver(a, partition=part) as ds:
+        ds.setup()
+        ds.init_sigma(1 if cfg.guess == "jacobi" else 0)
+        errs = [ds.sweep(1e-9, 5000)[0] for _ in range(sweeps)]
+        s = ds.sigma()
+    o = orc.solve(a, part.sets, tol=1e-300, max_iterations=sweeps, guess=cfg.guess)
+    assert rel_fro(s, o["result"]) < 1e-10
+    assert np.array_equal(s, s.T)
+    for e, r in zip(errs, o["error_trace"]):
+        assert abs(e - r) <= 1e-6 * r + 5e-2 * cfg.tol
+
+
 def test_c4_through_the_floor_matches_reference():
     """c4 (p=16384) against the reference's own 30-sweep CPU run (tests/golden/c4long.npz,
     generated by make_golden.py c4long from the reference package): the whole error
