@@ -634,11 +634,16 @@ __global__ void __launch_bounds__(512, 1) power_gram_ll_kernel(PowerParams P, do
     rpar ^= 1;
     if (lane == 0) { r[2 * wid] = a; r[2 * wid + 1] = b; }
     __syncthreads();
-    double sa = 0.0, sb = 0.0;
+    // fixed-shape pairwise tree over the 16 warps (4 dependent adds instead of 16)
+    double ta[16], tb[16];
 #pragma unroll
-    for (int w = 0; w < 16; ++w) { sa += r[2 * w]; sb += r[2 * w + 1]; }
-    a = sa;
-    b = sb;
+    for (int w = 0; w < 16; ++w) { ta[w] = r[2 * w]; tb[w] = r[2 * w + 1]; }
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+      for (int w = 0; w < h; ++w) { ta[w] += ta[w + h]; tb[w] += tb[w + h]; }
+    a = ta[0];
+    b = tb[0];
   };
 
   long long tag = 0;
@@ -685,8 +690,14 @@ __global__ void __launch_bounds__(512, 1) power_gram_ll_kernel(PowerParams P, do
     if (wid == 0) {
       double z = 0.0;
       if (lane < 16) {
+        double t[16];
 #pragma unroll
-        for (int w = 0; w < 16; ++w) z += wred[w * 16 + lane];
+        for (int w = 0; w < 16; ++w) t[w] = wred[w * 16 + lane];
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+          for (int w = 0; w < h; ++w) t[w] += t[w + h];
+        z = t[0];
       }
       const double a = __shfl_sync(0xffffffffu, z, (2 * lane) & 31);
       double b = __shfl_sync(0xffffffffu, z, (2 * lane + 1) & 31);
@@ -798,8 +809,8 @@ __global__ void __launch_bounds__(512, 1) power_gram_ll_kernel(PowerParams P, do
       const double nw = sqrt(pyz);
       if (nw == 0.0) { conv = 1.0; break; }
       if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
-      sigma = sqrt(pzz) / nw;
       sc = 1.0 / nw;
+      sigma = sqrt(pzz) * sc;
 #pragma unroll
       for (int q = 0; q < Q; ++q) y[q] = zz[q];
       ++it;
@@ -898,19 +909,30 @@ __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(256)
     if (lane == 0) { red[2 * warp] = a; red[2 * warp + 1] = b; }
     __syncthreads();
     if (tid < CLUSTER_CTAS) {
-      double sa = 0.0, sb = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { sa += red[2 * w]; sb += red[2 * w + 1]; }
+      // 8 warps (launch: 256 threads), pairwise tree: 3 dependent adds instead of 8
+      double ta[8], tb[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) { ta[w] = red[2 * w]; tb[w] = red[2 * w + 1]; }
+#pragma unroll
+      for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+        for (int w = 0; w < h; ++w) { ta[w] += ta[w + h]; tb[w] += tb[w + h]; }
       double* dst = cluster.map_shared_rank(part, tid);
-      dst[slot * 2 * CLUSTER_CTAS + 2 * rank] = sa;
-      dst[slot * 2 * CLUSTER_CTAS + 2 * rank + 1] = sb;
+      dst[slot * 2 * CLUSTER_CTAS + 2 * rank] = ta[0];
+      dst[slot * 2 * CLUSTER_CTAS + 2 * rank + 1] = tb[0];
     }
     cluster.sync();
-    double sa = 0.0, sb = 0.0;
+    double ua[CLUSTER_CTAS], ub[CLUSTER_CTAS];
+#pragma unroll
     for (int q = 0; q < CLUSTER_CTAS; ++q) {
-      sa += part[slot * 2 * CLUSTER_CTAS + 2 * q];
-      sb += part[slot * 2 * CLUSTER_CTAS + 2 * q + 1];
+      ua[q] = part[slot * 2 * CLUSTER_CTAS + 2 * q];
+      ub[q] = part[slot * 2 * CLUSTER_CTAS + 2 * q + 1];
     }
-    return make_double2(sa, sb);
+#pragma unroll
+    for (int h = CLUSTER_CTAS / 2; h >= 1; h >>= 1)
+#pragma unroll
+      for (int q = 0; q < h; ++q) { ua[q] += ua[q + h]; ub[q] += ub[q + h]; }
+    return make_double2(ua[0], ub[0]);
   };
 
   // z = G·(sc·y[cur]) on this CTA's rows; the slice goes into every CTA's y[nxt].
@@ -919,18 +941,36 @@ __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(256)
     const int nxt = cur ^ 1;
     pyz = 0.0;
     pzz = 0.0;
-    for (int r = warp; r < nr; r += (int)(blockDim.x >> 5)) {
+    // two rows per pass: their dot products and warp reductions interleave (independent chains)
+    const int nwarp = (int)(blockDim.x >> 5);
+    for (int r = warp; r < nr; r += 2 * nwarp) {
+      const int r2 = r + nwarp;
+      const bool two = r2 < nr;
       const double* row = g + (size_t)r * n;
-      double s = 0.0;
-      for (int j = lane; j < n; j += 32) s = fma(row[j], sc * yc[j], s);
-      s = warp_sum(s);
+      const double* row2 = g + (size_t)(two ? r2 : r) * n;
+      double s = 0.0, t = 0.0;
+      for (int j = lane; j < n; j += 32) {
+        const double yj = sc * yc[j];
+        s = fma(row[j], yj, s);
+        t = fma(row2[j], yj, t);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        t += __shfl_xor_sync(0xffffffffu, t, o);
+      }
       if (lane < CLUSTER_CTAS) {
         double* dst = cluster.map_shared_rank(y, lane);
         dst[(size_t)nxt * n + r0 + r] = s;
+        if (two) dst[(size_t)nxt * n + r0 + r2] = t;
       }
       if (lane == 0) {
         pyz = fma(sc * yc[r0 + r], s, pyz);
         pzz = fma(s, s, pzz);
+        if (two) {
+          pyz = fma(sc * yc[r0 + r2], t, pyz);
+          pzz = fma(t, t, pzz);
+        }
       }
     }
   };
@@ -978,8 +1018,8 @@ __global__ void __cluster_dims__(CLUSTER_CTAS, 1, 1) __launch_bounds__(256)
       const double nw = sqrt(s2.x);
       if (nw == 0.0) { conv = 1.0; break; }
       if (it >= P.max_iters) { conv = 0.0; it = P.max_iters; break; }
-      sigma = sqrt(s2.y) / nw;
       sc = 1.0 / nw;
+      sigma = sqrt(s2.y) * sc;
       cur ^= 1;
       ++it;
     }
