@@ -2800,16 +2800,36 @@ int enqueue_small_sweep(ibmi_ctx* c, double rtol, int max_iters, cudaEvent_t* ev
   for (int k = 0; k < P.K; ++k) {
     const SetDev& s = c->sets[k];
     P.set[k] = SmallSet{(int)s.lo, (int)s.hi, s.W, s.ainv, s.ldb};
-    const int ntm = (s.b + SS_TILE - 1) / SS_TILE, ntn = (int)((c->p - s.b + SS_TILE - 1) / SS_TILE);
+    const int ntm = (s.b + SS_TM - 1) / SS_TM, ntn = (int)((c->p - s.b + SS_TILE - 1) / SS_TILE);
     tiles = std::max(tiles, ntm * ntn);
   }
   P.estimate = 1;
   P.B = c->Bm; P.ldB = c->ldB; P.G = c->Gm; P.ldG = c->ldG; P.y1 = c->vec;
+  // IBMI_SS_TRACE=1 (eager launches only): per-phase %globaltimer stamps of block 0, printed to stderr
+  static int trace_on = -1;
+  if (trace_on < 0) trace_on = getenv("IBMI_SS_TRACE") ? 1 : 0;
+  static unsigned long long* trace_dev = nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cap);
+  const bool tracing = trace_on && cap == cudaStreamCaptureStatusNone;
+  if (tracing) {
+    if (!trace_dev) CUDA_TRY(cudaMalloc(&trace_dev, 128 * sizeof(unsigned long long)));
+    P.trace = trace_dev;
+  }
   const int grid = std::min(tiles, c->sms);
   void* args[] = {&P};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)small_sweep_kernel, dim3(grid), dim3(SS_THREADS), args, SS_SMEM,
                                        c->stream));
   note_launch();
+  if (tracing) {
+    unsigned long long h[128];
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(h, trace_dev, sizeof(h), cudaMemcpyDeviceToHost));
+    const int stamps = 4 * P.K + 4;
+    fprintf(stderr, "[ibmi] small_sweep phases (ns, block 0; phase, barrier, ...):");
+    for (int i = 1; i < stamps && i < 128; ++i) fprintf(stderr, " %llu", h[i] - h[i - 1]);
+    fprintf(stderr, "\n");
+  }
   if (ev) CUDA_TRY(cudaEventRecord(ev[0], c->stream));
   const SetDev& last = c->sets.back();
   NormBufs nb{c->Gm, c->ldG, c->vec, c->part, c->dscal, c->vr, c->power_blocks, c->power_threads,

@@ -30,9 +30,10 @@ namespace ibmi {
 namespace cg = cooperative_groups;
 
 constexpr int SS_MAX_SETS = 16;
-constexpr int SS_TILE = 32;
+constexpr int SS_TILE = 32;       // tile columns (N)
+constexpr int SS_TM = 16;         // tile rows (M): 16 × 32 tiles put 128+ CTAs on a 256 × 256 product (c1)
 constexpr int SS_THREADS = 256;
-constexpr int SS_SMEM = 8 * SS_TILE * (SS_TILE + 1) * (int)sizeof(double);   // 8 warps × 32 × 33 doubles
+constexpr int SS_SMEM = 8 * SS_TM * (SS_TILE + 1) * (int)sizeof(double);   // 8 warps × 16 × 33 doubles
 
 struct SmallSet {
   int lo, hi;
@@ -51,6 +52,7 @@ struct SmallSweepParams {
   double* B; int64_t ldB;
   double* G; int64_t ldG;
   double* y1;
+  unsigned long long* trace;   // optional (IBMI_SS_TRACE=1): %globaltimer of block 0 after each phase
 };
 
 struct SsOperand {
@@ -69,64 +71,86 @@ __device__ __forceinline__ int ss_row(const SsOperand& o, int i) { return i < o.
 template <class Epi>
 __device__ __forceinline__ void ss_tile(const SsOperand& X, const SsOperand& Y, int nseg, const int* seg_k0,
                                         const int* seg_len, int tm, int tn, double* red, Epi epi) {
+  constexpr int MI = SS_TM / 8, NJ = SS_TILE / 8;      // 2 × 4 DMMA tiles of 8 × 8 per warp
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  double acc[4][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const double* xr[4];
-  const double* yr[4];
-  bool xv[4], yv[4];
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double* xr[MI];
+  const double* yr[NJ];
+  bool xv[MI], yv[NJ];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = tm * SS_TILE + 8 * i + g, n = tn * SS_TILE + 8 * i + g;
+  for (int i = 0; i < MI; ++i) {
+    const int m = tm * SS_TM + 8 * i + g;
     xv[i] = m < X.rows;
-    yv[i] = n < Y.rows;
     xr[i] = X.base + (int64_t)(xv[i] ? ss_row(X, m) : 0) * X.ld;
-    yr[i] = Y.base + (int64_t)(yv[i] ? ss_row(Y, n) : 0) * Y.ld;
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int n = tn * SS_TILE + 8 * j + g;
+    yv[j] = n < Y.rows;
+    yr[j] = Y.base + (int64_t)(yv[j] ? ss_row(Y, n) : 0) * Y.ld;
   }
   for (int s = 0; s < nseg; ++s) {
     const int k0 = seg_k0[s], len = seg_len[s];
     const int steps = (len + 3) >> 2;
     const int per = (steps + 7) >> 3;                  // k-steps per warp, contiguous slice
     const int s0 = wid * per, s1 = min(steps, s0 + per);
-#pragma unroll 2
+#pragma unroll 4
     for (int ks = s0; ks < s1; ++ks) {
       const int k = 4 * ks + t;
       const bool kv = k < len;
-      double a[4], b[4];
+      double a[MI], b[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a[i] = (kv && xv[i]) ? (X.cg ? __ldcg(xr[i] + k0 + k) : __ldg(xr[i] + k0 + k)) : 0.0;
-        b[i] = (kv && yv[i]) ? (Y.cg ? __ldcg(yr[i] + k0 + k) : __ldg(yr[i] + k0 + k)) : 0.0;
-      }
+      for (int i = 0; i < MI; ++i) a[i] = (kv && xv[i]) ? (X.cg ? __ldcg(xr[i] + k0 + k) : __ldg(xr[i] + k0 + k)) : 0.0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < NJ; ++j) b[j] = (kv && yv[j]) ? (Y.cg ? __ldcg(yr[j] + k0 + k) : __ldg(yr[j] + k0 + k)) : 0.0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
-  double* mine = red + wid * SS_TILE * (SS_TILE + 1);
+  double* mine = red + wid * SS_TM * (SS_TILE + 1);
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       mine[(8 * i + g) * (SS_TILE + 1) + 8 * j + 2 * t] = acc[i][j][0];
       mine[(8 * i + g) * (SS_TILE + 1) + 8 * j + 2 * t + 1] = acc[i][j][1];
     }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < SS_TILE * SS_TILE / SS_THREADS; ++q) {
+  for (int q = 0; q < SS_TM * SS_TILE / SS_THREADS; ++q) {
     const int e = tid + SS_THREADS * q;
     const int r = e >> 5, c = e & 31;
-    double v = 0.0;
+    double v[8];
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += red[w * SS_TILE * (SS_TILE + 1) + r * (SS_TILE + 1) + c];
-    epi(tm * SS_TILE + r, tn * SS_TILE + c, v);
+    for (int w = 0; w < 8; ++w) v[w] = red[w * SS_TM * (SS_TILE + 1) + r * (SS_TILE + 1) + c];
+    epi(tm * SS_TM + r, tn * SS_TILE + c, ((v[0] + v[4]) + (v[2] + v[6])) + ((v[1] + v[5]) + (v[3] + v[7])));
   }
   __syncthreads();
+}
+
+// Lower-triangle tile walk of a b × b symmetric product with SS_TM × SS_TILE tiles: tile (tm, tn) is kept when
+// its first column is not above its last row; elements above the diagonal are masked by the epilogue.
+__device__ __forceinline__ bool ss_lower_tile(int tile, int b, int& tm, int& tn) {
+  const int ntn = (b + SS_TILE - 1) / SS_TILE;
+  tm = tile / ntn;
+  tn = tile % ntn;
+  return tn * SS_TILE <= tm * SS_TM + SS_TM - 1;
+}
+
+__device__ __forceinline__ void ss_stamp(const SmallSweepParams& P, int& slot) {
+  if (P.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.trace[slot] = t;
+  }
+  ++slot;
 }
 
 __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepParams P) {
@@ -134,6 +158,8 @@ __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepPa
   extern __shared__ __align__(16) double ss_red[];
   const int p = P.p;
   const int64_t ld = P.ld;
+  int slot = 0;
+  ss_stamp(P, slot);
   for (int k = 0; k < P.K; ++k) {
     const SmallSet st = P.set[k];
     const int lo = st.lo, hi = st.hi, b = hi - lo, c = p - b;
@@ -143,7 +169,7 @@ __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepPa
     {
       const SsOperand X{st.W, ld, INT_MAX, 0, 0, b, false};
       const SsOperand Y{P.S, ld, lo, 0, hi, c, true};
-      const int ntm = (b + SS_TILE - 1) / SS_TILE, ntn = (c + SS_TILE - 1) / SS_TILE;
+      const int ntm = (b + SS_TM - 1) / SS_TM, ntn = (c + SS_TILE - 1) / SS_TILE;
       for (int tile = blockIdx.x; tile < ntm * ntn; tile += gridDim.x) {
         ss_tile(X, Y, 2, seg_k0, seg_len, tile / ntn, tile % ntn, ss_red, [&](int m, int n, double v) {
           if (m < b && n < c) {
@@ -154,19 +180,18 @@ __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepPa
         });
       }
     }
+    ss_stamp(P, slot);
     __threadfence();
     grid.sync();
+    ss_stamp(P, slot);
     // ---- B_k: Σ[I, I] = A_II⁻¹ − Σ[I, c]·Wᵀ, lower tiles mirrored
     {
       const SsOperand X{P.S, ld, INT_MAX, lo, 0, b, true};
       const SsOperand Y{st.W, ld, INT_MAX, 0, 0, b, false};
-      const int nt = (b + SS_TILE - 1) / SS_TILE;
-      const int ntiles = nt * (nt + 1) / 2;
+      const int ntiles = ((b + SS_TM - 1) / SS_TM) * ((b + SS_TILE - 1) / SS_TILE);
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int tm = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
-        while (tm * (tm + 1) / 2 > tile) --tm;
-        while ((tm + 1) * (tm + 2) / 2 <= tile) ++tm;
-        const int tn = tile - tm * (tm + 1) / 2;
+        int tm, tn;
+        if (!ss_lower_tile(tile, b, tm, tn)) continue;
         ss_tile(X, Y, 2, seg_k0, seg_len, tm, tn, ss_red, [&](int m, int n, double v) {
           if (m < b && n <= m) {
             const double r = st.ainv[(int64_t)m * st.ldb + n] - v;
@@ -176,8 +201,10 @@ __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepPa
         });
       }
     }
+    ss_stamp(P, slot);
     __threadfence();
     grid.sync();
+    ss_stamp(P, slot);
   }
   if (!P.estimate) return;
   const SmallSet st = P.set[P.K - 1];
@@ -187,26 +214,25 @@ __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepPa
     const int k0[1] = {0}, len[1] = {p};
     const SsOperand X{P.S, ld, INT_MAX, lo, 0, b, true};
     const SsOperand Y{P.A, ld, lo, 0, hi, c, false};
-    const int ntm = (b + SS_TILE - 1) / SS_TILE, ntn = (c + SS_TILE - 1) / SS_TILE;
+    const int ntm = (b + SS_TM - 1) / SS_TM, ntn = (c + SS_TILE - 1) / SS_TILE;
     for (int tile = blockIdx.x; tile < ntm * ntn; tile += gridDim.x) {
       ss_tile(X, Y, 1, k0, len, tile / ntn, tile % ntn, ss_red, [&](int m, int n, double v) {
         if (m < b && n < c) P.B[(int64_t)m * P.ldB + n] = v;
       });
     }
   }
+  ss_stamp(P, slot);
   __threadfence();
   grid.sync();
+  ss_stamp(P, slot);
   // ---- D: G = B·Bᵀ (lower tiles mirrored), y₁ = B·(1/√c)
   {
     const int k0[1] = {0}, len[1] = {c};
     const SsOperand X{P.B, P.ldB, INT_MAX, 0, 0, b, true};
-    const int nt = (b + SS_TILE - 1) / SS_TILE;
-    const int ntiles = nt * (nt + 1) / 2;
+    const int ntiles = ((b + SS_TM - 1) / SS_TM) * ((b + SS_TILE - 1) / SS_TILE);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      int tm = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
-      while (tm * (tm + 1) / 2 > tile) --tm;
-      while ((tm + 1) * (tm + 2) / 2 <= tile) ++tm;
-      const int tn = tile - tm * (tm + 1) / 2;
+      int tm, tn;
+      if (!ss_lower_tile(tile, b, tm, tn)) continue;
       ss_tile(X, X, 1, k0, len, tm, tn, ss_red, [&](int m, int n, double v) {
         if (m < b && n <= m) {
           P.G[(int64_t)m * P.ldG + n] = v;
@@ -225,6 +251,7 @@ __global__ void __launch_bounds__(SS_THREADS, 1) small_sweep_kernel(SmallSweepPa
       if (lane == 0) P.y1[r] = s;
     }
   }
+  ss_stamp(P, slot);
 }
 
 }  // namespace ibmi
