@@ -8,18 +8,21 @@
 // tensor work, but each launch of the big-tile TMA GEMM costs 15-35 µs of
 // latency (pipeline fill, 128×128 tiles on 4 of 148 SMs, split-K reduction
 // launches).  The 14 launches of a c1 sweep took 0.235 ms for 0.2 GFLOP.  Here
-// the phases are separated by grid barriers (1.2 µs each) instead of launches,
-// tiles are 32×32 so 64+ CTAs share each product, and operands stream from L2
-// straight into DMMA fragments (Σ, A and W are 2 MB each at c1: L2-resident).
+// the phases are separated by grid barriers (1.3-1.7 µs each) instead of launches,
+// tiles are 16×32 so 128 CTAs share a 256×256 product (a 32×32 tile with K = 256
+// is 2.1 µs of DMMA on one SM: the first version's 64 CTAs left 84 SMs idle and
+// spent 5.7 µs per phase, this one 4.0), and operands stream from L2 straight
+// into DMMA fragments (Σ, A and W are 2 MB each at c1: L2-resident; staging them
+// through shared memory with cp.async was measured slower, 7.1 µs per phase).
 //
 // Phases (set k: I = [lo, hi), b rows, complement c through a one-gap map):
 //   A_k  Σ[I, c] = −W_k·Σ[c, c],  Σ[c, I] = its transpose          (b × c tiles, K = c)
 //   B_k  Σ[I, I] = A_II⁻¹ − Σ[I, c]·W_kᵀ, lower tiles mirrored     (b × b lower tiles, K = c)
 //   C    B = Σ[I_K, :]·A[:, c_K]                                   (b × c tiles, K = p)
 //   D    G = B·Bᵀ (lower tiles mirrored), y₁ = B·(1/√c)            (feeds the power iteration)
-// Each CTA computes 32×32 output tiles; its 8 warps split K, each holding a
-// 32×32 accumulator in DMMA fragments, summed through shared memory in warp
-// order (deterministic).  Σ and B are read with ld.global.cg: other CTAs wrote
+// Each CTA computes 16×32 output tiles; its 8 warps split K, each holding a
+// 16×32 accumulator in DMMA fragments, summed through shared memory in a fixed
+// pairwise order (deterministic).  Σ and B are read with ld.global.cg: other CTAs wrote
 // them earlier in this kernel, so L1 must be bypassed.
 #pragma once
 #include <cooperative_groups.h>
