@@ -2509,6 +2509,7 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
     if (rc) { cleanup(); return rc; }
   }
   pt.mark("streams + scratch");
+  const auto t_enq0 = std::chrono::steady_clock::now();
   for (int j = 0; j < count; ++j) {
     const int q = j % S;
     SetDev& s = c->sets[first + j];
@@ -2555,6 +2556,9 @@ int ibmi_setup(ibmi_ctx* c, int first, int count, int* fail_set, int64_t* fail_p
       SETUP_TRY(launch_gemm(gw, sq));
     }
   }
+  if (getenv("IBMI_PROFILE"))
+    fprintf(stderr, "[ibmi] setup: host time to enqueue all sets %.1f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enq0).count());
   for (int q = 0; q < S; ++q) SETUP_TRY(cudaStreamSynchronize(ss[q]));
   SETUP_TRY(cudaMemcpy(infos.data(), dinfo, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost));
 #undef SETUP_TRY
