@@ -883,20 +883,28 @@ class ShardedSolver:
             full = full[np.ix_(inv, inv)]
         return full
 
+    @staticmethod
+    def comm_model(p: int, lo: int, hi: int, world: int, rank: int, panel: int = 128, operands: str = "sharded") -> dict:
+        """The byte / flop model behind :meth:`comm_bytes`, from the layout alone (no process group):
+        rank ``rank`` of ``world`` in the block step of set [lo, hi)."""
+        lay = RowPanels(p, world, panel)
+        b = hi - lo
+        a0, a1 = lay.local_range(rank, lo, hi)
+        n_loc = len(lay.rows[rank])
+        n_I, n_cl, c = a1 - a0, n_loc - (a1 - a0), p - b
+        return {"exchange_out": 8 * (b - n_I) * n_cl, "exchange_in": 8 * n_I * (c - n_cl),
+                "allreduce_top": int(8 * b * b * 2 * (world - 1) / world),
+                "allgather_w_in": 8 * b * (p - n_loc) if operands == "sharded" and world > 1 else 0,
+                "gemm_flops": 2 * b * c * n_cl + 2 * b * b * n_cl}
+
     def comm_bytes(self, k: int) -> dict:
         """Bytes this rank moves over NVLink in block step k (each direction), by phase:
         the b × c transpose exchange (fused peer stores or all_to_all), the ring
         all-reduce of the b × b lower-triangle partials, and — operands sharded — the
         all-gather of W_k's column shards.  ``gemm_flops`` is this rank's share of
         2bc² + 2b²c, for the comm/compute budget in DESIGN.md §6."""
-        pl, g, G = self.plan[k], self.rank, self.world
-        b, n_cl = pl["b"], pl["n_cl"]
-        n_I = pl["n_I"][g]
-        c = self.p - b
-        return {"exchange_out": 8 * (b - n_I) * n_cl, "exchange_in": 8 * n_I * (c - n_cl),
-                "allreduce_top": int(8 * b * b * 2 * (G - 1) / G),
-                "allgather_w_in": 8 * b * (self.p - self.n_loc) if self.operands == "sharded" and G > 1 else 0,
-                "gemm_flops": 2 * b * c * n_cl + 2 * b * b * n_cl}
+        pl = self.plan[k]
+        return self.comm_model(self.p, pl["lo"], pl["hi"], self.world, self.rank, self.layout.panel, self.operands)
 
     def close(self):
         for work, _ in getattr(self, "_wpending", {}).values():

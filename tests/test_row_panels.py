@@ -52,3 +52,23 @@ def test_complement_shares_are_balanced_at_the_baseline_configs():
 def test_map_indices_gap_map():
     assert list(map_indices((3, 0, 7), 6)) == [0, 1, 2, 7, 8, 9]
     assert list(map_indices(5, 3)) == [5, 6, 7]
+
+
+def test_comm_model_conserves_bytes_and_matches_the_design_table():
+    """ShardedSolver.comm_model: what the ranks send in the transpose exchange is what they receive,
+    the GEMM flops add up to 2bc² + 2b²c, and the per-step figures quoted in DESIGN.md §6 hold."""
+    from paper_2502_06377_b200.distributed import ShardedSolver
+
+    table = {  # (p, lo, hi, world): (exchange MB, all-reduce MB, W all-gather MB) of DESIGN.md §6
+        (16384, 1792, 4352, 8): (31, 92, 294), (16384, 1792, 4352, 2): (71, 52, 168),
+        (65536, 3584, 8704, 8): (271, 367, 2350), (65536, 3584, 8704, 2): (619, 210, 1340),
+    }
+    for (p, lo, hi, world), (ex, ar, ag) in table.items():
+        ms = [ShardedSolver.comm_model(p, lo, hi, world, r) for r in range(world)]
+        b, c = hi - lo, p - (hi - lo)
+        assert sum(m["exchange_out"] for m in ms) == sum(m["exchange_in"] for m in ms)
+        assert sum(m["gemm_flops"] for m in ms) == 2 * b * c * c + 2 * b * b * c
+        assert abs(sum(m["exchange_out"] for m in ms) / world / 1e6 - ex) <= 0.02 * ex      # mean over ranks
+        assert abs(ms[0]["allreduce_top"] / 1e6 - ar) <= 0.02 * ar
+        assert abs(max(m["allgather_w_in"] for m in ms) / 1e6 - ag) <= 0.02 * ag
+        assert ShardedSolver.comm_model(p, lo, hi, world, 0, operands="replicated")["allgather_w_in"] == 0
